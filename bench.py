@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the FastLSH hot path on B200 (BASELINE.json metric: hashes/s and roofline fraction).
+
+One step = one pass of the whole hot path over the workload resident in HBM:
+  K1 fastlsh_hash (stage X, gather S_i(v), project, +b, /w, floor, int32 codes)
+  K3 fastlsh_build_keys (L tables of K codes -> 64-bit keys)
+  (N>1 GPUs) NCCL all-gather of the keys, one all_gather_into_tensor per table.
+Default workload: BASELINE.json configs[1] (C1: N=1e6, n=960, k=500, m=60, w=1, L=50 x K=10).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl reference]
+
+Rank 0 prints ONE JSON line. See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FastLSH hashes/sec (N*k) and % of HBM/smem roofline"
+SMEM_GATHERS_PER_CLK_PER_SM = 32  # one 128-B wavefront of 4-B words per SM per clock
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the measured region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.gpu), "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _cores():
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(cfg, seconds_target: float = 12.0):
+    """The CPU oracle as it stands, on a bounded row sample of the same workload, all host cores."""
+    import oracle
+    from fastlsh_inputs import data, fastlsh_arrays
+    idx, a, b = fastlsh_arrays(cfg.n, cfg.m, cfg.k, cfg.w, cfg.seed)
+    cores = _cores()
+    # calibrate on a small sample, then size the measured sample to ~seconds_target
+    rows0 = 256
+    X0 = data.generate(cfg.data, cfg.n, 0, rows0, seed=cfg.seed).numpy()
+    t = time.perf_counter()
+    oracle.fastlsh(X0, idx, a, b, cfg.w, threads=cores)
+    dt = max(time.perf_counter() - t, 1e-4)
+    rows = int(min(cfg.N, max(rows0, rows0 * seconds_target / dt)))
+    X = data.generate(cfg.data, cfg.n, 0, rows, seed=cfg.seed).numpy()
+    t = time.perf_counter()
+    oracle.fastlsh(X, idx, a, b, cfg.w, threads=cores)
+    dt = time.perf_counter() - t
+    return {"value": rows * cfg.k / dt, "unit": "hashes/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {rows} of {cfg.N} rows ({cfg.name}), double-precision oracle, OpenMP "
+                      f"{cores} threads, {dt:.2f} s (codes only; keys not included)",
+            "seconds": dt}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, seconds_target=2.0)
+    for _ in range(args.steps):
+        steps.append(cpu_baseline(cfg, seconds_target=args.ref_seconds))
+    vals = [s["value"] for s in steps]
+    v = statistics.median(vals)
+    cb = dict(steps[-1])
+    cb["value"] = v
+    cb.pop("seconds", None)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "hashes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg, world),
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "hashes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def _config_dict(cfg, world):
+    return {"workload": f"{cfg.name}: N={cfg.N} rows/GPU, n={cfg.n}, k={cfg.k}, m={cfg.m}, w={cfg.w}, "
+                        f"keys L={cfg.L} x K={cfg.K}, recipe {cfg.data}",
+            "N_per_gpu": cfg.N, "n": cfg.n, "k": cfg.k, "m": cfg.m, "w": cfg.w, "L": cfg.L, "K": cfg.K,
+            "global_rows": cfg.N * world, "parallelism": f"row-sharded x{world}, params replicated",
+            "l2": f"inputs {cfg.N * cfg.n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
+
+
+def _traffic_from_profiles(kernel_substr: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_gather_full.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from fastlsh_inputs import configs
+    cfg = configs.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import data
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    P = fl.Params.create(cfg.n, cfg.m, cfg.k, cfg.w, seed=cfg.seed)
+    info = P.info()
+    Kobj = fl.Keys.create(cfg.L, cfg.K, seed=cfg.seed) if cfg.L else None
+    N = cfg.N
+    X = data.generate(cfg.data, cfg.n, rank * N, (rank + 1) * N, seed=cfg.seed, device=dev)
+    codes = torch.empty((N, cfg.k), dtype=torch.int32, device=dev)
+    keys = torch.empty((cfg.L, N), dtype=torch.int64, device=dev) if Kobj else None
+    gathered = torch.empty((cfg.L, world * N), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
+    stream = torch.cuda.current_stream()
+
+    launches_per_step = 1 + (1 if Kobj else 0)
+    ev = []
+
+    def step(record: bool):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+        if record:
+            e[0].record(stream)
+        fl.fastlsh_hash(P, X, out=codes)
+        if record:
+            e[1].record(stream)
+        if Kobj:
+            fl.build_keys(Kobj, codes, out=keys)
+        if record:
+            e[2].record(stream)
+        if gathered is not None:
+            for l in range(cfg.L):
+                dist.all_gather_into_tensor(gathered[l], keys[l])
+        if record:
+            e[3].record(stream)
+            ev.append(e)
+
+    smi_index = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            smi_index = int(vis.split(",")[local])
+        except Exception:
+            pass
+    sampler = ClockSampler(smi_index)
+    sampler.start()
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = t0.elapsed_time(t1)
+    hash_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    keys_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ag_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    tt = torch.tensor([total_ms, statistics.mean(hash_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms_max, hash_ms_max = float(tt[0]), float(tt[1])
+    ms_per_step = total_ms_max / args.steps
+    hashes_per_step = world * N * cfg.k
+    value = hashes_per_step / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (K1): smem gathers vs the north_star bound
+    peaks = _peaks()
+    t_hash = statistics.mean(hash_ms) / 1e3
+    gathers = N * cfg.k * cfg.m
+    g_peak = 148 * SMEM_GATHERS_PER_CLK_PER_SM * peaks["sm_max_mhz"] * 1e6
+    hbm_bytes = 4.0 * N * cfg.n + 4.0 * N * cfg.k
+    t_roof = max(hbm_bytes / (peaks["hbm_gbs"] * 1e9), gathers / g_peak)
+    t_roof_nominal = max(hbm_bytes / 8.0e12, gathers / g_peak)
+    roofline = {"bound": "smem", "achieved": gathers / t_hash / 1e9, "peak": g_peak / 1e9,
+                "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
+                "traffic": _traffic_from_profiles("gather_kernel"),
+                "kernel": "gather_kernel (K1 fastlsh_hash)",
+                "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
+                "north_star_frac": t_roof / t_hash, "north_star_frac_nominal_8TBs": t_roof_nominal / t_hash,
+                "hbm_achieved_gbs": hbm_bytes / t_hash / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"],
+                "peak_source": peaks["source"] + f"; smem peak = 148 SM x 32 x {peaks['sm_max_mhz']:.0f} MHz",
+                "kernel_share_of_step": statistics.mean(hash_ms) / ms_per_step if ms_per_step else None}
+
+    # end to end through the public host-buffer API: H2D of X, hash + keys, D2H of codes + keys
+    Xh = X.cpu().pin_memory()
+    codes_h = torch.empty((N, cfg.k), dtype=torch.int32).pin_memory()
+    keys_h = torch.empty((cfg.L, N), dtype=torch.int64).pin_memory() if Kobj else None
+    fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=131072)  # warm (workspace allocation)
+    if world > 1:
+        dist.barrier()
+    te = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=131072)
+    e2e_s = (time.perf_counter() - te) / args.e2e_steps
+    et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e = {"value": hashes_per_step / float(et[0]), "unit": "hashes/s",
+           "h2d_bytes_per_step": int(Xh.numel() * 4),
+           "d2h_bytes_per_step": int(codes_h.numel() * 4 + (keys_h.numel() * 8 if keys_h is not None else 0)),
+           "api": "fastlsh_hash_host (pinned host buffers, 2-stream chunked pipeline)", "steps": args.e2e_steps}
+    del Xh, codes_h, keys_h
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg)
+        cb.pop("seconds", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "hashes/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, resident in HBM)",
+                "config": _config_dict(cfg, world), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps,
+                "clocks": clocks,
+                "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
+                                 "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
+                                 "hash_max_over_ranks": hash_ms_max},
+                "packing": {k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
+                                                 "bank_efficiency", "conflict_wavefronts")}}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * fastlsh.h — C ABI of libfastlsh, a B200 (sm_100a) implementation of FastLSH hash evaluation
+ * (Tan et al., "Fast Locality Sensitive Hashing with Theoretical Guarantee", arXiv 2309.15479).
+ *
+ * Method (§3.1, Eq. 5): for every row v of X[N x n] and hash i < k,
+ *     h_i(v) = floor( (a_i . S_i(v) + b_i) / w )
+ * where S_i(v) gathers m coordinates of v at a multiset of m indices drawn i.i.d. uniformly from
+ * [0, n) with replacement, a_i ~ N(0,1)^m and b_i ~ U[0, w).
+ * E2LSH (Eq. 1) is the special case m = n with the identity sample.
+ *
+ * Conventions for every call:
+ *  - X, codes, proj and keys are DEVICE pointers owned by the caller, row-major, contiguous.
+ *    X must be 4-byte aligned; 16-byte alignment and n % 4 == 0 select the 128-bit load path.
+ *  - Calls are asynchronous and ordered on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream). No call synchronises except fastlsh_read_flags and the *_host entry points.
+ *  - N == 0 is a no-op returning FASTLSH_OK.
+ *  - Errors are returned, never aborted on. Data-dependent conditions inside a kernel (a
+ *    non-finite projection, a quotient outside int32) write the sentinel INT32_MIN into that code
+ *    and increment a per-params device counter, read back by fastlsh_read_flags.
+ *  - Params and keys objects are immutable after creation/upload; concurrent calls on different
+ *    streams with the same objects are safe.
+ */
+#ifndef FASTLSH_H
+#define FASTLSH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fastlsh_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    FASTLSH_OK = 0,
+    FASTLSH_EINVAL = -1,       /* bad argument: sizes, null/misaligned pointer, w <= 0 or NaN */
+    FASTLSH_ENOMEM = -2,       /* host or device allocation failed */
+    FASTLSH_ECUDA = -3,        /* a CUDA runtime call failed (see fastlsh_last_cuda_error) */
+    FASTLSH_EUNSUPPORTED = -4, /* current device is not sm_100 (B200), or shape unsupported */
+    FASTLSH_ESTATE = -5        /* params/keys not uploaded to the current device */
+} fastlsh_status;
+
+typedef struct fastlsh_params fastlsh_params; /* opaque: S_i, a_i, b_i, w + GPU packing */
+typedef struct fastlsh_keys fastlsh_keys;     /* opaque: L, K, multipliers r[L][K+1]     */
+
+/* Packing summary of a params object (filled by fastlsh_params_info). */
+typedef struct {
+    int32_t n, m, k;
+    float w;
+    int32_t is_e2lsh;          /* created by e2lsh_params_create (identity S, m == n)          */
+    int32_t parts;             /* lanes per hash: each lane owns <= ceil(m/parts) slots         */
+    int32_t slots;             /* slot positions per lane after bank scheduling (incl. padding) */
+    int32_t units;             /* k * parts lane units                                          */
+    int32_t warps_per_block;   /* warps in one CTA hash block                                    */
+    int32_t hash_blocks;       /* CTAs per row group (disjoint hash ranges)                      */
+    int32_t rows_per_group;    /* rows staged together per pipeline stage                        */
+    double bank_efficiency;    /* useful gathers / (lanes * slots) over all warps                 */
+    int64_t conflict_wavefronts; /* extra smem wavefronts per row left by the scheduler          */
+} fastlsh_params_info_t;
+
+/* ---- parameters: S_i, a_i, b_i, w --------------------- */
+
+/* Draw params from `seed` with the library's counter-based Philox4x32-10 (R11):
+ *   idx[i][j] = hi64(u64(philox(j,i,1)) * n),  a[i][j] = BoxMuller(philox(j,i,2)) as f32,
+ *   b[i] = f32(w * u53(philox(0,i,3))) clamped to [0, w).
+ * n, m, k >= 1; w finite and > 0; m > n is legal (sampling with replacement).
+ * EINVAL otherwise. EUNSUPPORTED if n > 16352 (offsets are packed as 16-bit smem byte offsets)
+ * or m > 16384. */
+fastlsh_status fastlsh_params_create(int32_t n, int32_t m, int32_t k, float w, uint64_t seed,
+                                     fastlsh_params** out);
+
+/* Same, from caller-provided host arrays (copied): idx int32[k*m] (0 <= idx < n), a f32[k*m],
+ * b f32[k] (any finite values). Used for parity with the oracle on shared seeded inputs. */
+fastlsh_status fastlsh_params_create_from_arrays(int32_t n, int32_t m, int32_t k, float w,
+                                                 const int32_t* idx, const float* a,
+                                                 const float* b, fastlsh_params** out);
+
+/* E2LSH params (Eq. 1): m = n, idx[i][j] = j; a and b drawn from the same
+ * (seed, i, j) streams as fastlsh_params_create, so identity-FastLSH == E2LSH. */
+fastlsh_status e2lsh_params_create(int32_t n, int32_t k, float w, uint64_t seed,
+                                   fastlsh_params** out);
+
+void fastlsh_params_destroy(fastlsh_params* p); /* frees host and all device copies; NULL ok */
+
+/* Copy the canonical (paper-order) params out: idx int32[k*m], a f32[k*m], b f32[k], w.
+ * Any output pointer may be NULL. */
+fastlsh_status fastlsh_params_export(const fastlsh_params* p, int32_t* idx, float* a, float* b,
+                                     float* w);
+
+fastlsh_status fastlsh_params_info(const fastlsh_params* p, fastlsh_params_info_t* info);
+
+/* Diagnostic: copy the GPU packing out (for host-side verification of the bank scheduler).
+ * sizes[0..7] = {parts, slots, warps, hash_blocks, kb_max, nq, stage_chunks, n_lanes_total}.
+ * Arrays (any may be NULL): offp u32[HB*W*slots/2*32], coef f32[HB*W*slots*32],
+ * unit_lane u16[HB*kb_max*parts], block_h0 int32[HB], block_kb int32[HB]. */
+fastlsh_status fastlsh_params_packing(const fastlsh_params* p, int32_t* sizes, uint32_t* offp,
+                                      float* coef, uint16_t* unit_lane, int32_t* block_h0,
+                                      int32_t* block_kb);
+
+/* Pack the bank-scheduled GPU layout and copy it to the CURRENT device (cudaSetDevice first).
+ * `device` must equal the current device. Idempotent per device. */
+fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_stream_t stream);
+
+/* ---- hashing ----------------------------------------------------------- */
+
+/* codes[r*k + i] = floor((a_i . S_i(X[r]) + b_i) / w) as int32, for r < N, i < k — Eq. 5.
+ * fp32 accumulation in a bank-conflict-free slot order (in chunks of <= 64 products), then
+ * __fadd_rn(p, b), __fdiv_rn(., w), floor toward -inf. Non-finite or out-of-int32 quotients
+ * write INT32_MIN and count in the params' flags. Requires fastlsh_params_upload. */
+fastlsh_status fastlsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
+                            fastlsh_stream_t stream);
+
+/* proj[r*k + i] = a_i . S_i(X[r]) in fp32 (the projection before +b, /w, floor). */
+fastlsh_status fastlsh_project(const fastlsh_params* p, const float* X, int64_t N, float* proj,
+                               fastlsh_stream_t stream);
+
+/* ---- dense E2LSH baseline on tcgen05 tensor cores ---------------------- */
+
+/* codes = floor((X . A^T + b) / w) with A[k][n] the dense coefficient matrix of the params
+ * (for E2LSH params, a_i itself; for FastLSH params, the duplicates-merged sampled matrix).
+ * tcgen05 kind::tf32 MMAs with a 3xTF32 split (hi*hi + hi*lo + lo*hi), fp32 accumulation in TMEM,
+ * fused +b, /w, floor epilogue. precision: 3 = 3xTF32 (parity-gated), 1 = plain TF32.
+ * Requires n % 32 == 0 and k % 16 == 0 (else EUNSUPPORTED). */
+fastlsh_status e2lsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
+                          int32_t precision, fastlsh_stream_t stream);
+
+/* proj = X . A^T in fp32 from the same GEMM (for projection parity). */
+fastlsh_status e2lsh_project(const fastlsh_params* p, const float* X, int64_t N, float* proj,
+                             int32_t precision, fastlsh_stream_t stream);
+
+/* ---- compound bucket keys (§3.2) --------------------------- */
+
+/* r[l][j] uniform in [0, 2^61-1) from Philox stream 4 (R9). L, K >= 1. */
+fastlsh_status fastlsh_keys_create(int32_t L, int32_t K, uint64_t seed, fastlsh_keys** out);
+fastlsh_status fastlsh_keys_create_from_arrays(int32_t L, int32_t K, const uint64_t* r,
+                                               fastlsh_keys** out); /* r[L*(K+1)], each < 2^61-1 */
+void fastlsh_keys_destroy(fastlsh_keys* keys);
+fastlsh_status fastlsh_keys_export(const fastlsh_keys* keys, uint64_t* r);
+
+/* keys[l*ldk + v] = (r[l][0] + sum_{j<K} r[l][j+1] * u32(codes[v*k + l*K + j])) mod (2^61-1)
+ * for l < L, v < N; exact integer arithmetic. EINVAL if L*K > k or ldk < N. */
+fastlsh_status fastlsh_build_keys(const fastlsh_keys* keys, const int32_t* codes, int64_t N,
+                                  int32_t k, uint64_t* keys_out, int64_t ldk,
+                                  fastlsh_stream_t stream);
+
+/* Fused: codes (as fastlsh_hash) and keys (as fastlsh_build_keys) for the same rows in one call
+ * sequence on `stream`; keys may be NULL (codes only). */
+fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* keys,
+                                 const float* X, int64_t N, int32_t* codes, uint64_t* keys_out,
+                                 int64_t ldk, fastlsh_stream_t stream);
+
+/* ---- host-buffer entry point (end-to-end; SURVEY.md §3 "config 4 streaming") ----------------- */
+
+/* Hash HOST rows: X_host f32[N*n] (pinned or pageable), codes_host int32[N*k], keys_host
+ * uint64[L*N] table-major (may be NULL; `keys` may be NULL). Rows are streamed in chunks of
+ * `chunk_rows` through a double-buffered device workspace owned by the params object, with H2D
+ * copies, hashing and D2H copies overlapped on two streams. Synchronous: returns when the host
+ * outputs are complete. */
+fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* keys, const float* X_host,
+                                 int64_t N, int32_t* codes_host, uint64_t* keys_host,
+                                 int64_t chunk_rows);
+
+/* ---- flags / errors --------------------------------------------------------------------------- */
+
+/* Read (and optionally reset) the per-device counters of sentinel codes written so far:
+ * nonfinite (NaN/Inf projections), saturated (finite quotient outside int32). Synchronises
+ * `stream`. */
+fastlsh_status fastlsh_read_flags(const fastlsh_params* p, uint64_t* nonfinite,
+                                  uint64_t* saturated, int32_t reset, fastlsh_stream_t stream);
+
+const char* fastlsh_status_string(fastlsh_status s);
+const char* fastlsh_last_cuda_error(void); /* thread-local text of the last ECUDA */
+int32_t fastlsh_abi_version(void);         /* 1 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTLSH_H */

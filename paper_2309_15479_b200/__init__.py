@@ -1,0 +1,363 @@
+"""paper_2309_15479_b200 — FastLSH hash evaluation on B200 (sm_100a).
+
+Thin ctypes binding over libfastlsh.so (include/fastlsh.h). Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels; torch supplies device memory and streams.
+There is no CPU fallback: if the library is missing or the device is not a B200, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfastlsh.so")
+
+OK, EINVAL, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5
+
+EXPORTED = [
+    "fastlsh_params_create", "fastlsh_params_create_from_arrays", "e2lsh_params_create",
+    "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
+    "fastlsh_params_upload",
+    "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
+    "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
+    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_host", "fastlsh_read_flags",
+    "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
+]
+
+
+class FastLSHError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        lib = _lib
+        msg = lib.fastlsh_status_string(status).decode() if lib else str(status)
+        if status == ECUDA and lib:
+            msg += f" ({lib.fastlsh_last_cuda_error().decode()})"
+        super().__init__(f"{what}: {msg} [{status}]")
+        self.status = status
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("w", ctypes.c_float), ("is_e2lsh", ctypes.c_int32), ("parts", ctypes.c_int32),
+                ("slots", ctypes.c_int32), ("units", ctypes.c_int32),
+                ("warps_per_block", ctypes.c_int32), ("hash_blocks", ctypes.c_int32),
+                ("rows_per_group", ctypes.c_int32), ("bank_efficiency", ctypes.c_double),
+                ("conflict_wavefronts", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libfastlsh.so (build it with __graft_entry__.build() or paper_2309_15479_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libfastlsh.so not built at {path}; run `python __graft_entry__.py build`")
+    lib = ctypes.CDLL(path)
+    P, i32, i64, u64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "fastlsh_params_create": [i32, i32, i32, f32, u64, PP],
+        "fastlsh_params_create_from_arrays": [i32, i32, i32, f32, P, P, P, PP],
+        "e2lsh_params_create": [i32, i32, f32, u64, PP],
+        "fastlsh_params_export": [P, P, P, P, P],
+        "fastlsh_params_info": [P, ctypes.POINTER(_Info)],
+        "fastlsh_params_upload": [P, i32, P],
+        "fastlsh_params_packing": [P, P, P, P, P, P, P],
+        "fastlsh_hash": [P, P, i64, P, P],
+        "fastlsh_project": [P, P, i64, P, P],
+        "e2lsh_hash": [P, P, i64, P, i32, P],
+        "e2lsh_project": [P, P, i64, P, i32, P],
+        "fastlsh_keys_create": [i32, i32, u64, PP],
+        "fastlsh_keys_create_from_arrays": [i32, i32, P, PP],
+        "fastlsh_keys_export": [P, P],
+        "fastlsh_build_keys": [P, P, i64, i32, P, i64, P],
+        "fastlsh_hash_keys": [P, P, P, i64, P, P, i64, P],
+        "fastlsh_hash_host": [P, P, P, i64, P, P, i64],
+        "fastlsh_read_flags": [P, P, P, i32, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.fastlsh_params_destroy.argtypes = [P]
+    lib.fastlsh_params_destroy.restype = None
+    lib.fastlsh_keys_destroy.argtypes = [P]
+    lib.fastlsh_keys_destroy.restype = None
+    lib.fastlsh_status_string.argtypes = [ctypes.c_int]
+    lib.fastlsh_status_string.restype = ctypes.c_char_p
+    lib.fastlsh_last_cuda_error.restype = ctypes.c_char_p
+    lib.fastlsh_abi_version.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise FastLSHError(status, what)
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dev_ptr(t, dtype, what: str):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA torch tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"{what} must be a contiguous {dtype} tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Params:
+    """FastLSH (or E2LSH) hash-function parameters: S_i, a_i, b_i, w."""
+
+    def __init__(self, handle: int, lib):
+        self._h = ctypes.c_void_p(handle)
+        self._lib = lib
+        info = self.info()
+        self.n, self.m, self.k, self.w = info["n"], info["m"], info["k"], info["w"]
+        self._uploaded = set()
+
+    @classmethod
+    def create(cls, n: int, m: int, k: int, w: float, seed: int):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.fastlsh_params_create(n, m, k, w, seed, ctypes.byref(h)), "fastlsh_params_create")
+        return cls(h.value, lib)
+
+    @classmethod
+    def from_arrays(cls, n: int, w: float, idx, a, b):
+        lib = load_library()
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        k, m = idx.shape
+        h = ctypes.c_void_p()
+        _check(lib.fastlsh_params_create_from_arrays(n, m, k, w, _np_ptr(idx), _np_ptr(a), _np_ptr(b),
+                                                     ctypes.byref(h)), "fastlsh_params_create_from_arrays")
+        return cls(h.value, lib)
+
+    @classmethod
+    def e2lsh(cls, n: int, k: int, w: float, seed: int):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.e2lsh_params_create(n, k, w, seed, ctypes.byref(h)), "e2lsh_params_create")
+        return cls(h.value, lib)
+
+    def info(self) -> dict:
+        inf = _Info()
+        _check(self._lib.fastlsh_params_info(self._h, ctypes.byref(inf)), "fastlsh_params_info")
+        return {f: getattr(inf, f) for f, _ in _Info._fields_}
+
+    def export(self):
+        idx = np.empty((self.k, self.m), np.int32)
+        a = np.empty((self.k, self.m), np.float32)
+        b = np.empty(self.k, np.float32)
+        w = ctypes.c_float()
+        _check(self._lib.fastlsh_params_export(self._h, _np_ptr(idx), _np_ptr(a), _np_ptr(b), ctypes.byref(w)),
+               "fastlsh_params_export")
+        return idx, a, b, w.value
+
+    def packing(self) -> dict:
+        """The bank-scheduled GPU layout (diagnostic; see fastlsh_params_packing)."""
+        sz = np.zeros(8, np.int32)
+        _check(self._lib.fastlsh_params_packing(self._h, _np_ptr(sz), None, None, None, None, None),
+               "fastlsh_params_packing")
+        P, MS, W, HB, kbm, nq, sc, lanes = (int(x) for x in sz)
+        offp = np.zeros(HB * W * (MS // 2) * 32, np.uint32)
+        coef = np.zeros(HB * W * MS * 32, np.float32)
+        unit = np.zeros(HB * kbm * P, np.uint16)
+        h0 = np.zeros(HB, np.int32)
+        kb = np.zeros(HB, np.int32)
+        _check(self._lib.fastlsh_params_packing(self._h, _np_ptr(sz), _np_ptr(offp), _np_ptr(coef), _np_ptr(unit),
+                                                _np_ptr(h0), _np_ptr(kb)), "fastlsh_params_packing")
+        return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, nq=nq, stage_chunks=sc,
+                    offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
+                    unit_lane=unit.reshape(HB, kbm, P), block_h0=h0, block_kb=kb)
+
+    def upload(self, device=None, stream=None):
+        import torch
+        dev = torch.cuda.current_device() if device is None else int(device)
+        if dev in self._uploaded:
+            return self
+        with torch.cuda.device(dev):
+            _check(self._lib.fastlsh_params_upload(self._h, dev, _stream_ptr(stream)), "fastlsh_params_upload")
+        self._uploaded.add(dev)
+        return self
+
+    def _ready(self):
+        import torch
+        if torch.cuda.current_device() not in self._uploaded:
+            self.upload()
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            self._lib.fastlsh_params_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Keys:
+    """Compound-key multipliers r[L][K+1] (reading R9)."""
+
+    def __init__(self, handle: int, lib, L: int, K: int):
+        self._h = ctypes.c_void_p(handle)
+        self._lib = lib
+        self.L, self.K = L, K
+
+    @classmethod
+    def create(cls, L: int, K: int, seed: int):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.fastlsh_keys_create(L, K, seed, ctypes.byref(h)), "fastlsh_keys_create")
+        return cls(h.value, lib, L, K)
+
+    @classmethod
+    def from_arrays(cls, r):
+        lib = load_library()
+        r = np.ascontiguousarray(r, dtype=np.uint64)
+        L, K1 = r.shape
+        h = ctypes.c_void_p()
+        _check(lib.fastlsh_keys_create_from_arrays(L, K1 - 1, _np_ptr(r), ctypes.byref(h)),
+               "fastlsh_keys_create_from_arrays")
+        return cls(h.value, lib, L, K1 - 1)
+
+    def export(self):
+        r = np.empty((self.L, self.K + 1), np.uint64)
+        _check(self._lib.fastlsh_keys_export(self._h, _np_ptr(r)), "fastlsh_keys_export")
+        return r
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            self._lib.fastlsh_keys_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fastlsh_hash(params: Params, X, out=None, stream=None):
+    """codes[N,k] int32 = floor((a_i . S_i(x) + b_i) / w) (Eq. 5) for X f32 [N,n] on the GPU."""
+    import torch
+    params._ready()
+    N = X.shape[0]
+    if out is None:
+        out = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    _check(params._lib.fastlsh_hash(params._h, _dev_ptr(X, torch.float32, "X"), N,
+                                    _dev_ptr(out, torch.int32, "codes"), _stream_ptr(stream)), "fastlsh_hash")
+    return out
+
+
+def fastlsh_project(params: Params, X, out=None, stream=None):
+    """proj[N,k] f32 = a_i . S_i(x) — the projection before +b, /w, floor."""
+    import torch
+    params._ready()
+    N = X.shape[0]
+    if out is None:
+        out = torch.empty((N, params.k), dtype=torch.float32, device=X.device)
+    _check(params._lib.fastlsh_project(params._h, _dev_ptr(X, torch.float32, "X"), N,
+                                       _dev_ptr(out, torch.float32, "proj"), _stream_ptr(stream)), "fastlsh_project")
+    return out
+
+
+def e2lsh_hash(params: Params, X, out=None, precision: int = 3, stream=None):
+    """Dense baseline codes on tcgen05 (3xTF32 by default)."""
+    import torch
+    params._ready()
+    N = X.shape[0]
+    if out is None:
+        out = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    _check(params._lib.e2lsh_hash(params._h, _dev_ptr(X, torch.float32, "X"), N,
+                                  _dev_ptr(out, torch.int32, "codes"), precision, _stream_ptr(stream)), "e2lsh_hash")
+    return out
+
+
+def e2lsh_project(params: Params, X, out=None, precision: int = 3, stream=None):
+    import torch
+    params._ready()
+    N = X.shape[0]
+    if out is None:
+        out = torch.empty((N, params.k), dtype=torch.float32, device=X.device)
+    _check(params._lib.e2lsh_project(params._h, _dev_ptr(X, torch.float32, "X"), N,
+                                     _dev_ptr(out, torch.float32, "proj"), precision, _stream_ptr(stream)),
+           "e2lsh_project")
+    return out
+
+
+def build_keys(keys: Keys, codes, out=None, ldk=None, stream=None):
+    """keys[L, N] uint64 (stored in an int64 tensor) from codes[N, k] int32."""
+    import torch
+    N, k = codes.shape
+    ldk = N if ldk is None else ldk
+    if out is None:
+        out = torch.empty((keys.L, ldk), dtype=torch.int64, device=codes.device)
+    _check(keys._lib.fastlsh_build_keys(keys._h, _dev_ptr(codes, torch.int32, "codes"), N, k,
+                                        _dev_ptr(out, torch.int64, "keys"), ldk, _stream_ptr(stream)),
+           "fastlsh_build_keys")
+    return out
+
+
+def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None):
+    """One step of the hot path: codes (Eq. 5) then compound keys, on the same stream."""
+    import torch
+    params._ready()
+    N = X.shape[0]
+    if codes is None:
+        codes = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    kp = ctypes.c_void_p(0)
+    if keys is not None:
+        if keys_out is None:
+            keys_out = torch.empty((keys.L, N), dtype=torch.int64, device=X.device)
+        kp = _dev_ptr(keys_out, torch.int64, "keys")
+    _check(params._lib.fastlsh_hash_keys(params._h, keys._h if keys is not None else None,
+                                         _dev_ptr(X, torch.float32, "X"), N, _dev_ptr(codes, torch.int32, "codes"),
+                                         kp, N, _stream_ptr(stream)), "fastlsh_hash_keys")
+    return codes, keys_out
+
+
+def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_host=None,
+              chunk_rows: int = 65536):
+    """End-to-end entry point on HOST buffers (numpy or pinned torch CPU tensors)."""
+    import torch
+    params._ready()
+    if isinstance(X_host, np.ndarray):
+        X_host = torch.from_numpy(np.ascontiguousarray(X_host, dtype=np.float32))
+    N = X_host.shape[0]
+    if codes_host is None:
+        codes_host = torch.empty((N, params.k), dtype=torch.int32, pin_memory=X_host.is_pinned())
+    kp = ctypes.c_void_p(0)
+    if keys is not None:
+        if keys_host is None:
+            keys_host = torch.empty((keys.L, N), dtype=torch.int64, pin_memory=X_host.is_pinned())
+        kp = ctypes.c_void_p(keys_host.data_ptr())
+    _check(params._lib.fastlsh_hash_host(params._h, keys._h if keys is not None else None,
+                                         ctypes.c_void_p(X_host.data_ptr()), N,
+                                         ctypes.c_void_p(codes_host.data_ptr()), kp, chunk_rows),
+           "fastlsh_hash_host")
+    return codes_host, keys_host
+
+
+def read_flags(params: Params, reset: bool = False, stream=None):
+    nf, sat = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(params._lib.fastlsh_read_flags(params._h, ctypes.byref(nf), ctypes.byref(sat), int(reset),
+                                          _stream_ptr(stream)), "fastlsh_read_flags")
+    return nf.value, sat.value

@@ -1,0 +1,511 @@
+// api.cu — the C ABI of include/fastlsh.h: validation, params/keys objects, per-device uploads,
+// dispatch to the kernels, and the pipelined host-buffer entry point.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+#include "philox.h"
+
+namespace fastlsh {
+
+static thread_local std::string g_cuda_error;
+
+fastlsh_status set_cuda_error(cudaError_t e) {
+    g_cuda_error = std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e);
+    return FASTLSH_ECUDA;
+}
+
+namespace {
+
+#define FL_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t _e = (call);                       \
+        if (_e != cudaSuccess) return set_cuda_error(_e); \
+    } while (0)
+
+fastlsh_status current_device(int* dev) {
+    FL_CUDA(cudaGetDevice(dev));
+    if (*dev < 0 || *dev >= kMaxDevices) return FASTLSH_EUNSUPPORTED;
+    return FASTLSH_OK;
+}
+
+fastlsh_status check_sm100(int dev) {
+    int major = 0, minor = 0;
+    FL_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    FL_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    if (major != 10 || minor != 0) return FASTLSH_EUNSUPPORTED;
+    return FASTLSH_OK;
+}
+
+bool valid_w(float w) { return std::isfinite(w) && w > 0.0f; }
+
+template <typename T>
+fastlsh_status upload_vec(T** dst, const std::vector<T>& src, cudaStream_t s) {
+    if (src.empty()) { *dst = nullptr; return FASTLSH_OK; }
+    FL_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), src.size() * sizeof(T)));
+    FL_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return FASTLSH_OK;
+}
+
+fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_params** out) {
+    if (!out) return FASTLSH_EINVAL;
+    *out = nullptr;
+    if (n <= 0 || m <= 0 || k <= 0 || !valid_w(w)) return FASTLSH_EINVAL;
+    if (n > 16352) return FASTLSH_EUNSUPPORTED;       // 16-bit smem byte offsets
+    if ((int64_t)m > (int64_t)kMaxSlots * 256) return FASTLSH_EUNSUPPORTED;
+    fastlsh_params* p = new (std::nothrow) fastlsh_params();
+    if (!p) return FASTLSH_ENOMEM;
+    p->n = n; p->m = m; p->k = k; p->w = w;
+    try {
+        p->idx.resize((size_t)k * m);
+        p->a.resize((size_t)k * m);
+        p->b.resize(k);
+    } catch (...) {
+        delete p;
+        return FASTLSH_ENOMEM;
+    }
+    *out = p;
+    return FASTLSH_OK;
+}
+
+fastlsh_status ensure_packed(fastlsh_params* p) {
+    if (p->packed) return FASTLSH_OK;
+    try {
+        build_packing(*p, p->pack);
+    } catch (...) {
+        return FASTLSH_ENOMEM;
+    }
+    if (p->pack.slots <= 0) return FASTLSH_EUNSUPPORTED;
+    p->packed = true;
+    return FASTLSH_OK;
+}
+
+fastlsh_status ready_params(const fastlsh_params* p, int* dev_out) {
+    if (!p) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    if (!p->dev[dev].ready) return FASTLSH_ESTATE;
+    *dev_out = dev;
+    return FASTLSH_OK;
+}
+
+void free_device_copy(DeviceCopy& d) {
+    cudaFree(d.offp); cudaFree(d.coef); cudaFree(d.unit_lane); cudaFree(d.b);
+    cudaFree(d.block_h0); cudaFree(d.block_kb); cudaFree(d.flags);
+    cudaFree(d.dense_hi); cudaFree(d.dense_lo);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(d.ws_x[i]); cudaFree(d.ws_codes[i]); cudaFree(d.ws_keys[i]);
+        if (d.ws_stream[i]) cudaStreamDestroy(d.ws_stream[i]);
+    }
+    for (int i = 0; i < 4; ++i) if (d.ws_event[i]) cudaEventDestroy(d.ws_event[i]);
+    d = DeviceCopy();
+}
+
+}  // namespace
+}  // namespace fastlsh
+
+using namespace fastlsh;
+
+extern "C" {
+
+int32_t fastlsh_abi_version(void) { return 1; }
+
+const char* fastlsh_status_string(fastlsh_status s) {
+    switch (s) {
+        case FASTLSH_OK: return "ok";
+        case FASTLSH_EINVAL: return "invalid argument";
+        case FASTLSH_ENOMEM: return "out of memory";
+        case FASTLSH_ECUDA: return "CUDA error";
+        case FASTLSH_EUNSUPPORTED: return "unsupported device or shape";
+        case FASTLSH_ESTATE: return "params/keys not uploaded to the current device";
+    }
+    return "unknown status";
+}
+
+const char* fastlsh_last_cuda_error(void) { return g_cuda_error.c_str(); }
+
+fastlsh_status fastlsh_params_create(int32_t n, int32_t m, int32_t k, float w, uint64_t seed,
+                                     fastlsh_params** out) {
+    fastlsh_status st = new_params(n, m, k, w, out);
+    if (st != FASTLSH_OK) return st;
+    fastlsh_params* p = *out;
+    for (int32_t i = 0; i < k; ++i) {
+        for (int32_t j = 0; j < m; ++j) {
+            p->idx[(size_t)i * m + j] = draw_index(seed, (uint32_t)i, (uint32_t)j, (uint32_t)n);
+            p->a[(size_t)i * m + j] = draw_gaussian(seed, (uint32_t)i, (uint32_t)j);
+        }
+        p->b[i] = draw_offset(seed, (uint32_t)i, w);
+    }
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_create_from_arrays(int32_t n, int32_t m, int32_t k, float w,
+                                                 const int32_t* idx, const float* a,
+                                                 const float* b, fastlsh_params** out) {
+    if (!idx || !a || !b) return FASTLSH_EINVAL;
+    for (int64_t t = 0; t < (int64_t)k * m; ++t) {
+        if (k > 0 && m > 0 && (idx[t] < 0 || idx[t] >= n)) return FASTLSH_EINVAL;
+        if (!std::isfinite(a[t])) return FASTLSH_EINVAL;
+    }
+    for (int32_t i = 0; i < k; ++i) if (!std::isfinite(b[i])) return FASTLSH_EINVAL;
+    fastlsh_status st = new_params(n, m, k, w, out);
+    if (st != FASTLSH_OK) return st;
+    fastlsh_params* p = *out;
+    std::memcpy(p->idx.data(), idx, sizeof(int32_t) * (size_t)k * m);
+    std::memcpy(p->a.data(), a, sizeof(float) * (size_t)k * m);
+    std::memcpy(p->b.data(), b, sizeof(float) * (size_t)k);
+    return FASTLSH_OK;
+}
+
+fastlsh_status e2lsh_params_create(int32_t n, int32_t k, float w, uint64_t seed,
+                                   fastlsh_params** out) {
+    fastlsh_status st = new_params(n, n, k, w, out);
+    if (st != FASTLSH_OK) return st;
+    fastlsh_params* p = *out;
+    p->is_e2lsh = true;
+    for (int32_t i = 0; i < k; ++i) {
+        for (int32_t j = 0; j < n; ++j) {
+            p->idx[(size_t)i * n + j] = j;
+            p->a[(size_t)i * n + j] = draw_gaussian(seed, (uint32_t)i, (uint32_t)j);
+        }
+        p->b[i] = draw_offset(seed, (uint32_t)i, w);
+    }
+    return FASTLSH_OK;
+}
+
+void fastlsh_params_destroy(fastlsh_params* p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int d = 0; d < kMaxDevices; ++d) {
+        DeviceCopy& dc = p->dev[d];
+        bool any = dc.offp || dc.flags || dc.dense_hi || dc.ws_x[0];
+        if (!any) continue;
+        cudaSetDevice(d);
+        free_device_copy(dc);
+    }
+    cudaSetDevice(cur);
+    delete p;
+}
+
+fastlsh_status fastlsh_params_export(const fastlsh_params* p, int32_t* idx, float* a, float* b,
+                                     float* w) {
+    if (!p) return FASTLSH_EINVAL;
+    if (idx) std::memcpy(idx, p->idx.data(), p->idx.size() * sizeof(int32_t));
+    if (a) std::memcpy(a, p->a.data(), p->a.size() * sizeof(float));
+    if (b) std::memcpy(b, p->b.data(), p->b.size() * sizeof(float));
+    if (w) *w = p->w;
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info_t* info) {
+    if (!cp || !info) return FASTLSH_EINVAL;
+    fastlsh_params* p = const_cast<fastlsh_params*>(cp);
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        fastlsh_status st = ensure_packed(p);
+        if (st != FASTLSH_OK) return st;
+    }
+    const Packing& pk = p->pack;
+    info->n = p->n; info->m = p->m; info->k = p->k; info->w = p->w;
+    info->is_e2lsh = p->is_e2lsh ? 1 : 0;
+    info->parts = pk.parts;
+    info->slots = pk.slots;
+    info->units = p->k * pk.parts;
+    info->warps_per_block = pk.warps;
+    info->hash_blocks = pk.hash_blocks;
+    info->rows_per_group = kRows;
+    info->bank_efficiency = pk.efficiency;
+    info->conflict_wavefronts = pk.conflict_wavefronts;
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_packing(const fastlsh_params* cp, int32_t* sizes, uint32_t* offp,
+                                      float* coef, uint16_t* unit_lane, int32_t* block_h0,
+                                      int32_t* block_kb) {
+    if (!cp) return FASTLSH_EINVAL;
+    fastlsh_params* p = const_cast<fastlsh_params*>(cp);
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        fastlsh_status st = ensure_packed(p);
+        if (st != FASTLSH_OK) return st;
+    }
+    const Packing& pk = p->pack;
+    if (sizes) {
+        sizes[0] = pk.parts; sizes[1] = pk.slots; sizes[2] = pk.warps; sizes[3] = pk.hash_blocks;
+        sizes[4] = pk.kb_max; sizes[5] = pk.nq; sizes[6] = pk.stage_chunks;
+        sizes[7] = pk.hash_blocks * pk.warps * 32;
+    }
+    if (offp) std::memcpy(offp, pk.offp.data(), pk.offp.size() * sizeof(uint32_t));
+    if (coef) std::memcpy(coef, pk.coef.data(), pk.coef.size() * sizeof(float));
+    if (unit_lane) std::memcpy(unit_lane, pk.unit_lane.data(), pk.unit_lane.size() * sizeof(uint16_t));
+    if (block_h0) for (size_t i = 0; i < pk.block_h0.size(); ++i) block_h0[i] = pk.block_h0[i];
+    if (block_kb) for (size_t i = 0; i < pk.block_kb.size(); ++i) block_kb[i] = pk.block_kb[i];
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_stream_t stream) {
+    if (!p) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    if (device != dev) return FASTLSH_EINVAL;
+    st = check_sm100(dev);
+    if (st != FASTLSH_OK) return st;
+    std::lock_guard<std::mutex> g(p->mu);
+    if (p->dev[dev].ready) return FASTLSH_OK;
+    st = ensure_packed(p);
+    if (st != FASTLSH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    DeviceCopy& d = p->dev[dev];
+    const Packing& pk = p->pack;
+    std::vector<int32_t> h0(pk.block_h0.begin(), pk.block_h0.end());
+    std::vector<int32_t> kb(pk.block_kb.begin(), pk.block_kb.end());
+    if ((st = upload_vec(&d.offp, pk.offp, s)) != FASTLSH_OK ||
+        (st = upload_vec(&d.coef, pk.coef, s)) != FASTLSH_OK ||
+        (st = upload_vec(&d.unit_lane, pk.unit_lane, s)) != FASTLSH_OK ||
+        (st = upload_vec(&d.b, p->b, s)) != FASTLSH_OK ||
+        (st = upload_vec(&d.block_h0, h0, s)) != FASTLSH_OK ||
+        (st = upload_vec(&d.block_kb, kb, s)) != FASTLSH_OK) {
+        free_device_copy(d);
+        return st;
+    }
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d.flags), 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(d.flags, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors may be reused right away
+    if (e != cudaSuccess) {
+        free_device_copy(d);
+        return set_cuda_error(e);
+    }
+    d.ready = true;
+    return FASTLSH_OK;
+}
+
+static fastlsh_status hash_common(const fastlsh_params* p, const float* X, int64_t N,
+                                  int32_t* codes, float* proj, fastlsh_stream_t stream) {
+    if (!p || N < 0) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X || (!codes && !proj)) return FASTLSH_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(X) & 3) || (reinterpret_cast<uintptr_t>(codes) & 3) ||
+        (reinterpret_cast<uintptr_t>(proj) & 3))
+        return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    return launch_gather(p, p->dev[dev], X, N, codes, proj, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status fastlsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
+                            fastlsh_stream_t stream) {
+    if (!codes && N > 0) return FASTLSH_EINVAL;
+    return hash_common(p, X, N, codes, nullptr, stream);
+}
+
+fastlsh_status fastlsh_project(const fastlsh_params* p, const float* X, int64_t N, float* proj,
+                               fastlsh_stream_t stream) {
+    if (!proj && N > 0) return FASTLSH_EINVAL;
+    return hash_common(p, X, N, nullptr, proj, stream);
+}
+
+fastlsh_status e2lsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
+                          int32_t precision, fastlsh_stream_t stream) {
+    if (!p || N < 0 || (precision != 1 && precision != 3)) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X || !codes) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    fastlsh_params* mp = const_cast<fastlsh_params*>(p);
+    return launch_e2lsh(mp, mp->dev[dev], X, N, codes, nullptr, precision,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status e2lsh_project(const fastlsh_params* p, const float* X, int64_t N, float* proj,
+                             int32_t precision, fastlsh_stream_t stream) {
+    if (!p || N < 0 || (precision != 1 && precision != 3)) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X || !proj) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    fastlsh_params* mp = const_cast<fastlsh_params*>(p);
+    return launch_e2lsh(mp, mp->dev[dev], X, N, nullptr, proj, precision,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status fastlsh_keys_create(int32_t L, int32_t K, uint64_t seed, fastlsh_keys** out) {
+    if (!out) return FASTLSH_EINVAL;
+    *out = nullptr;
+    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 16384) return FASTLSH_EINVAL;
+    fastlsh_keys* ks = new (std::nothrow) fastlsh_keys();
+    if (!ks) return FASTLSH_ENOMEM;
+    ks->L = L; ks->K = K;
+    ks->r.resize((size_t)L * (K + 1));
+    for (int32_t l = 0; l < L; ++l)
+        for (int32_t j = 0; j <= K; ++j)
+            ks->r[(size_t)l * (K + 1) + j] = draw_key_multiplier(seed, (uint32_t)l, (uint32_t)j);
+    *out = ks;
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_keys_create_from_arrays(int32_t L, int32_t K, const uint64_t* r,
+                                               fastlsh_keys** out) {
+    if (!out || !r) return FASTLSH_EINVAL;
+    *out = nullptr;
+    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 16384) return FASTLSH_EINVAL;
+    for (int64_t t = 0; t < (int64_t)L * (K + 1); ++t) if (r[t] >= kP61) return FASTLSH_EINVAL;
+    fastlsh_keys* ks = new (std::nothrow) fastlsh_keys();
+    if (!ks) return FASTLSH_ENOMEM;
+    ks->L = L; ks->K = K;
+    ks->r.assign(r, r + (size_t)L * (K + 1));
+    *out = ks;
+    return FASTLSH_OK;
+}
+
+void fastlsh_keys_destroy(fastlsh_keys* ks) {
+    if (!ks) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int d = 0; d < kMaxDevices; ++d) {
+        if (!ks->dev_r[d]) continue;
+        cudaSetDevice(d);
+        cudaFree(ks->dev_r[d]);
+    }
+    cudaSetDevice(cur);
+    delete ks;
+}
+
+fastlsh_status fastlsh_keys_export(const fastlsh_keys* ks, uint64_t* r) {
+    if (!ks || !r) return FASTLSH_EINVAL;
+    std::memcpy(r, ks->r.data(), ks->r.size() * sizeof(uint64_t));
+    return FASTLSH_OK;
+}
+
+static fastlsh_status keys_device(const fastlsh_keys* cks, int dev, const uint64_t** out) {
+    fastlsh_keys* ks = const_cast<fastlsh_keys*>(cks);
+    std::lock_guard<std::mutex> g(ks->mu);
+    if (!ks->dev_r[dev]) {
+        uint64_t* d = nullptr;
+        FL_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), ks->r.size() * sizeof(uint64_t)));
+        cudaError_t e = cudaMemcpy(d, ks->r.data(), ks->r.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { cudaFree(d); return set_cuda_error(e); }
+        ks->dev_r[dev] = d;
+    }
+    *out = ks->dev_r[dev];
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_build_keys(const fastlsh_keys* ks, const int32_t* codes, int64_t N,
+                                  int32_t k, uint64_t* keys_out, int64_t ldk,
+                                  fastlsh_stream_t stream) {
+    if (!ks || N < 0 || k <= 0) return FASTLSH_EINVAL;
+    if ((int64_t)ks->L * ks->K > k) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!codes || !keys_out || ldk < N) return FASTLSH_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(codes) & 3) || (reinterpret_cast<uintptr_t>(keys_out) & 7))
+        return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    st = check_sm100(dev);
+    if (st != FASTLSH_OK) return st;
+    const uint64_t* dr = nullptr;
+    st = keys_device(ks, dev, &dr);
+    if (st != FASTLSH_OK) return st;
+    return launch_build_keys(ks, dr, codes, N, k, keys_out, ldk, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
+                                 int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
+                                 fastlsh_stream_t stream) {
+    fastlsh_status st = fastlsh_hash(p, X, N, codes, stream);
+    if (st != FASTLSH_OK || !ks || !keys_out) return st;
+    return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
+}
+
+fastlsh_status fastlsh_read_flags(const fastlsh_params* p, uint64_t* nonfinite,
+                                  uint64_t* saturated, int32_t reset, fastlsh_stream_t stream) {
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long h[2] = {0, 0};
+    FL_CUDA(cudaMemcpyAsync(h, p->dev[dev].flags, sizeof(h), cudaMemcpyDeviceToHost, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    if (reset) {
+        FL_CUDA(cudaMemsetAsync(p->dev[dev].flags, 0, sizeof(h), s));
+        FL_CUDA(cudaStreamSynchronize(s));
+    }
+    if (nonfinite) *nonfinite = h[0];
+    if (saturated) *saturated = h[1];
+    return FASTLSH_OK;
+}
+
+// Host-buffer pipeline: chunk i is copied H2D on stream s[i%2], hashed (+keys) there, and its
+// results copied D2H on the same stream; the two streams overlap copy with compute. The host
+// buffers are used in place (pinned memory gives true async copies; pageable memory still works).
+fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, const float* X_host,
+                                 int64_t N, int32_t* codes_host, uint64_t* keys_host,
+                                 int64_t chunk_rows) {
+    if (!p || N < 0 || chunk_rows <= 0) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X_host || !codes_host) return FASTLSH_EINVAL;
+    if (ks && keys_host && (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    DeviceCopy& d = p->dev[dev];
+    const bool want_keys = ks && keys_host;
+    const int L = want_keys ? ks->L : 0;
+    std::lock_guard<std::mutex> g(p->mu);
+    if (d.ws_rows < chunk_rows || d.ws_L < L) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(d.ws_x[i]); cudaFree(d.ws_codes[i]); cudaFree(d.ws_keys[i]);
+            d.ws_x[i] = nullptr; d.ws_codes[i] = nullptr; d.ws_keys[i] = nullptr;
+        }
+        for (int i = 0; i < 2; ++i) {
+            FL_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.ws_x[i]), (size_t)chunk_rows * p->n * sizeof(float)));
+            FL_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.ws_codes[i]), (size_t)chunk_rows * p->k * sizeof(int32_t)));
+            if (L > 0) FL_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.ws_keys[i]), (size_t)chunk_rows * L * sizeof(uint64_t)));
+            if (!d.ws_stream[i]) FL_CUDA(cudaStreamCreateWithFlags(&d.ws_stream[i], cudaStreamNonBlocking));
+        }
+        d.ws_rows = chunk_rows;
+        d.ws_L = L;
+    }
+    const uint64_t* dr = nullptr;
+    if (want_keys) {
+        st = keys_device(ks, dev, &dr);
+        if (st != FASTLSH_OK) return st;
+    }
+    const int64_t nchunks = (N + chunk_rows - 1) / chunk_rows;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int b = (int)(c & 1);
+        cudaStream_t s = d.ws_stream[b];
+        const int64_t r0 = c * chunk_rows;
+        const int64_t rows = (N - r0 < chunk_rows) ? N - r0 : chunk_rows;
+        FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
+                                cudaMemcpyHostToDevice, s));
+        st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
+        if (st != FASTLSH_OK) return st;
+        FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s));
+        if (want_keys) {
+            st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
+            if (st != FASTLSH_OK) return st;
+            // keys of this chunk: [L][rows] on device -> columns r0.. of the [L][N] host matrix
+            FL_CUDA(cudaMemcpy2DAsync(keys_host + r0, (size_t)N * sizeof(uint64_t), d.ws_keys[b],
+                                      (size_t)rows * sizeof(uint64_t), (size_t)rows * sizeof(uint64_t), L,
+                                      cudaMemcpyDeviceToHost, s));
+        }
+    }
+    FL_CUDA(cudaStreamSynchronize(d.ws_stream[0]));
+    FL_CUDA(cudaStreamSynchronize(d.ws_stream[1]));
+    return FASTLSH_OK;
+}
+
+}  // extern "C"

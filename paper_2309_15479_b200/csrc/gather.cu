@@ -1,0 +1,294 @@
+// gather.cu — K1/K2: FastLSH sampled-projection hashing on sm_100a.
+//
+// For every row v and hash i: h_i(v) = floor((a_i . S_i(v) + b_i) / w)   (Eq. 5).
+//
+// Design:
+//  * One CTA owns a block of hashes; its lanes hold their hash part's slots in registers for the
+//    whole kernel: MS 16-bit smem byte offsets (two per register) and MS f32 coefficients, in
+//    the bank-scheduled order produced by packer.cpp.
+//  * Rows are processed 4 at a time. A stage holds 4 rows column-interleaved: the 16-byte chunk
+//    at position pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per slot
+//    therefore gathers the sampled coordinate of 4 rows, and one FFMA per row accumulates it.
+//    The packer guarantees the 8 lanes of each quarter-warp hit 8 distinct bank groups at every
+//    slot position, so each LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
+//  * Stages are double buffered: while a CTA gathers from stage j it has already issued the
+//    coalesced 128-bit global loads of group j+1 (held in registers), stored transposed into the
+//    other stage after the gather loop.
+//  * Epilogue (fused): lanes deposit their 4 partial projections; after one CTA barrier the
+//    threads sum the parts of each hash in fixed order, add b (__fadd_rn), divide by w
+//    (__fdiv_rn), floor toward -inf, and write int32 codes with coalesced stores.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace fastlsh {
+namespace {
+
+constexpr int kBatch = 4;  // float4 staging loads held in registers per thread
+
+struct GatherArgs {
+    const float* X;
+    long long N;
+    int n, nq, stage_chunks;
+    const uint32_t* offp;
+    const float* coef;
+    const uint16_t* unit_lane;
+    const float* b;
+    const int* block_h0;
+    const int* block_kb;
+    float w;
+    int k, P, W, HB, kb_max;
+    long long groups;
+    int32_t* codes;
+    float* proj;
+    unsigned long long* flags;
+    int vec4;
+};
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Load up to kBatch float4 items of group g starting at item `first` into registers.
+__device__ __forceinline__ void stage_load(const GatherArgs& a, long long g, int first, float4 (&buf)[kBatch]) {
+    const int items = 4 * a.nq;
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+        const int it = first + i * blockDim.x;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (it < items) {
+            const int r = it & 3, q = it >> 2;
+            const long long row = g * 4 + r;
+            if (row < a.N) {
+                if (a.vec4) {
+                    v = __ldg(reinterpret_cast<const float4*>(a.X + row * a.n) + q);
+                } else {
+                    const float* src = a.X + row * a.n;
+                    const int c = 4 * q;
+                    v.x = (c + 0 < a.n) ? __ldg(src + c + 0) : 0.f;
+                    v.y = (c + 1 < a.n) ? __ldg(src + c + 1) : 0.f;
+                    v.z = (c + 2 < a.n) ? __ldg(src + c + 2) : 0.f;
+                    v.w = (c + 3 < a.n) ? __ldg(src + c + 3) : 0.f;
+                }
+            }
+        }
+        buf[i] = v;
+    }
+}
+
+// Store the batch transposed: column 4q+i of row r goes to chunk i*nq+q, lane r.
+__device__ __forceinline__ void stage_store(const GatherArgs& a, float* stage, int first, const float4 (&buf)[kBatch]) {
+    const int items = 4 * a.nq;
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+        const int it = first + i * blockDim.x;
+        if (it < items) {
+            const int r = it & 3, q = it >> 2;
+            stage[(0 * a.nq + q) * 4 + r] = buf[i].x;
+            stage[(1 * a.nq + q) * 4 + r] = buf[i].y;
+            stage[(2 * a.nq + q) * 4 + r] = buf[i].z;
+            stage[(3 * a.nq + q) * 4 + r] = buf[i].w;
+        }
+    }
+}
+
+__device__ __forceinline__ void stage_fill(const GatherArgs& a, long long g, float* stage, int from_item) {
+    const int items = 4 * a.nq;
+    for (int first = from_item; first < items; first += kBatch * blockDim.x) {
+        float4 buf[kBatch];
+        stage_load(a, g, first, buf);
+        stage_store(a, stage, first, buf);
+    }
+}
+
+template <int MS>
+__global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
+    extern __shared__ __align__(128) float4 smem[];
+    const int SC = a.stage_chunks;
+    float4* stage[2] = {smem, smem + SC};
+    float4* part = smem + 2 * SC;  // [2][W*32]
+    uint16_t* s_unit = reinterpret_cast<uint16_t*>(part + 2 * a.W * 32);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthreads = blockDim.x;
+    const int hb = blockIdx.x % a.HB;
+    const long long gpr = gridDim.x / a.HB;
+    const long long rs = blockIdx.x / a.HB;
+    const int kb = a.block_kb[hb];
+    const int h0 = a.block_h0[hb];
+    float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * a.P + 1) & ~1));
+
+    // zero chunks (padding slots read these), hash metadata
+    for (int i = tid; i < 2 * kPadChunks; i += nthreads)
+        stage[i / kPadChunks][4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = tid; i < kb * a.P; i += nthreads)
+        s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * a.P + i];
+    for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
+
+    // this lane's slots: offsets (two u16 per register) and coefficients
+    uint32_t op[MS / 2];
+    float cf[MS];
+    {
+        const size_t wl = (size_t)hb * a.W + warp;
+        const uint32_t* po = a.offp + wl * (MS / 2) * 32 + lane;
+        const float* pc = a.coef + wl * MS * 32 + lane;
+#pragma unroll
+        for (int t = 0; t < MS / 2; ++t) op[t] = __ldg(po + t * 32);
+#pragma unroll
+        for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
+    }
+
+    long long g = rs;
+    if (g < a.groups) stage_fill(a, g, reinterpret_cast<float*>(stage[0]), tid);
+    __syncthreads();
+
+    const float w = a.w;
+    int j = 0;
+    for (; g < a.groups; g += gpr, ++j) {
+        const long long gn = g + gpr;
+        const bool has_next = gn < a.groups;
+        float4 buf[kBatch];
+        if (has_next) stage_load(a, gn, tid, buf);
+
+        // gather-FMA over the scheduled slots: 4 rows per LDS.128
+        const uint32_t base = smem_u32(stage[j & 1]);
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+        for (int t = 0; t < MS; t += 2) {
+            const uint32_t pr = op[t >> 1];
+            const float4 v0 = lds128(base + (pr & 0xffffu));
+            const float4 v1 = lds128(base + (pr >> 16));
+            acc0 = fmaf(v0.x, cf[t], acc0);
+            acc1 = fmaf(v0.y, cf[t], acc1);
+            acc2 = fmaf(v0.z, cf[t], acc2);
+            acc3 = fmaf(v0.w, cf[t], acc3);
+            acc0 = fmaf(v1.x, cf[t + 1], acc0);
+            acc1 = fmaf(v1.y, cf[t + 1], acc1);
+            acc2 = fmaf(v1.z, cf[t + 1], acc2);
+            acc3 = fmaf(v1.w, cf[t + 1], acc3);
+        }
+        part[(j & 1) * a.W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
+
+        if (has_next) {
+            float* nst = reinterpret_cast<float*>(stage[(j + 1) & 1]);
+            stage_store(a, nst, tid, buf);
+            if (4 * a.nq > kBatch * nthreads) stage_fill(a, gn, nst, tid + kBatch * nthreads);
+        }
+        __syncthreads();
+
+        // epilogue: sum parts in fixed order, +b, /w, floor, coalesced int32 stores
+        const float* pf = reinterpret_cast<const float*>(part + (j & 1) * a.W * 32);
+        for (int it = tid; it < 4 * kb; it += nthreads) {
+            const int r = it / kb, h = it - r * kb;
+            const long long row = g * 4 + r;
+            if (row >= a.N) continue;
+            float p = 0.f;
+            for (int q = 0; q < a.P; ++q) p += pf[(int)s_unit[h * a.P + q] * 4 + r];
+            const long long o = row * a.k + h0 + h;
+            if (a.proj) {
+                a.proj[o] = p;
+            } else {
+                const float qv = __fdiv_rn(__fadd_rn(p, s_b[h]), w);
+                int code;
+                if (!isfinite(qv)) {
+                    code = INT_MIN;
+                    atomicAdd(a.flags + 0, 1ull);
+                } else {
+                    const float f = floorf(qv);
+                    if (f <= -2147483648.0f || f >= 2147483648.0f) {
+                        code = INT_MIN;
+                        atomicAdd(a.flags + 1, 1ull);
+                    } else {
+                        code = (int)f;
+                    }
+                }
+                a.codes[o] = code;
+            }
+        }
+    }
+}
+
+typedef void (*KernelFn)(GatherArgs);
+
+template <int MS>
+KernelFn kernel_for() { return gather_kernel<MS>; }
+
+KernelFn select_kernel(int MS) {
+    switch (MS) {
+#define FASTLSH_CASE(X) case X: return kernel_for<X>();
+        FASTLSH_CASE(2) FASTLSH_CASE(4) FASTLSH_CASE(6) FASTLSH_CASE(8) FASTLSH_CASE(10)
+        FASTLSH_CASE(12) FASTLSH_CASE(14) FASTLSH_CASE(16) FASTLSH_CASE(18) FASTLSH_CASE(20)
+        FASTLSH_CASE(22) FASTLSH_CASE(24) FASTLSH_CASE(26) FASTLSH_CASE(28) FASTLSH_CASE(30)
+        FASTLSH_CASE(32) FASTLSH_CASE(34) FASTLSH_CASE(36) FASTLSH_CASE(38) FASTLSH_CASE(40)
+        FASTLSH_CASE(42) FASTLSH_CASE(44) FASTLSH_CASE(46) FASTLSH_CASE(48) FASTLSH_CASE(50)
+        FASTLSH_CASE(52) FASTLSH_CASE(54) FASTLSH_CASE(56) FASTLSH_CASE(58) FASTLSH_CASE(60)
+        FASTLSH_CASE(62) FASTLSH_CASE(64)
+#undef FASTLSH_CASE
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
+                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream) {
+    const Packing& pk = p->pack;
+    KernelFn fn = select_kernel(pk.slots);
+    if (!fn) return FASTLSH_EUNSUPPORTED;
+    GatherArgs a;
+    a.X = X;
+    a.N = N;
+    a.n = p->n;
+    a.nq = pk.nq;
+    a.stage_chunks = pk.stage_chunks;
+    a.offp = d.offp;
+    a.coef = d.coef;
+    a.unit_lane = d.unit_lane;
+    a.b = d.b;
+    a.block_h0 = d.block_h0;
+    a.block_kb = d.block_kb;
+    a.w = p->w;
+    a.k = p->k;
+    a.P = pk.parts;
+    a.W = pk.warps;
+    a.HB = pk.hash_blocks;
+    a.kb_max = pk.kb_max;
+    a.groups = (N + 3) / 4;
+    a.codes = codes;
+    a.proj = proj;
+    a.flags = d.flags;
+    a.vec4 = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+
+    const int threads = pk.warps * 32;
+    const size_t smem = (size_t)2 * pk.stage_chunks * 16 + (size_t)2 * pk.warps * 32 * 16 +
+                        (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+    const long long resident = (long long)sms * per_sm;
+    long long gpr = resident / pk.hash_blocks;
+    if (gpr > a.groups) gpr = a.groups;
+    if (gpr < 1) gpr = 1;
+    const long long grid = gpr * pk.hash_blocks;
+    fn<<<(unsigned)grid, threads, smem, stream>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e);
+    return FASTLSH_OK;
+}
+
+}  // namespace fastlsh

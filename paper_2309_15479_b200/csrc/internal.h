@@ -1,0 +1,108 @@
+// internal.h — host-side structures shared by the C ABI, the packer and the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fastlsh.h"
+
+namespace fastlsh {
+
+constexpr int kMaxDevices = 16;
+constexpr int kRows = 4;          // rows per stage: one LDS.128 gathers the same column of 4 rows
+constexpr int kMaxSlots = 64;     // slot positions per lane held in registers
+constexpr int kPadChunks = 8;     // zero chunks after the data: one per 16-B bank group
+
+// GPU packing of a params object.
+//
+// Shared-memory stage layout (one stage = kRows rows): the 16-byte chunk at position pos holds
+// column c of all 4 rows, pos(c) = (c % 4) * nq + c / 4 with nq = ceil(n/4); chunks
+// [4*nq, 4*nq + 8) are zero (targets of padding slots). A lane's slot is a byte offset 16*pos into
+// the stage and a coefficient; one LDS.128 returns x[0..3][c].
+//
+// Lanes: each hash is split into `parts` lane units of <= ceil(m/parts) slots. Units of one CTA
+// hash block are grouped into quarter-warps (8 lanes = one LDS.128 wavefront) whose slots are
+// edge-coloured (König) so that at every slot position the 8 lanes touch distinct bank groups
+// (pos mod 8).
+struct Packing {
+    int parts = 1;
+    int slots = 0;            // MS: slot positions per lane (even)
+    int warps = 0;            // W: warps per CTA
+    int hash_blocks = 0;      // HB
+    int kb_max = 0;           // max hashes per block
+    int nq = 0;               // chunk columns per row-quarter
+    int stage_chunks = 0;     // 4*nq + kPadChunks
+    std::vector<int> block_h0, block_kb;       // hash range per block
+    std::vector<uint32_t> offp;  // [HB][W][MS/2][32]: two u16 byte offsets (slot t low, t+1 high)
+    std::vector<float> coef;     // [HB][W][MS][32]
+    std::vector<uint16_t> unit_lane;  // [HB][kb_max][parts]: lane id (warp*32+lane) of each part
+    double efficiency = 0;       // useful slots / (lanes * MS) over all warps
+    int64_t conflict_wavefronts = 0;  // extra wavefronts per stage (all blocks) beyond 4 per LDS
+};
+
+struct DeviceCopy {
+    bool ready = false;
+    uint32_t* offp = nullptr;
+    float* coef = nullptr;
+    uint16_t* unit_lane = nullptr;
+    float* b = nullptr;
+    int32_t* block_h0 = nullptr;
+    int32_t* block_kb = nullptr;
+    unsigned long long* flags = nullptr;  // [0] nonfinite, [1] saturated
+    float* dense_hi = nullptr;            // dense E2LSH operand A (tf32 hi) [kpad][n]
+    float* dense_lo = nullptr;            // A - hi (tf32 lo)
+    int dense_kpad = 0;
+    // host-pipeline workspace (fastlsh_hash_host)
+    float* ws_x[2] = {nullptr, nullptr};
+    int32_t* ws_codes[2] = {nullptr, nullptr};
+    uint64_t* ws_keys[2] = {nullptr, nullptr};
+    int64_t ws_rows = 0;
+    int ws_L = 0;
+    cudaStream_t ws_stream[2] = {nullptr, nullptr};
+    cudaEvent_t ws_event[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+}  // namespace fastlsh
+
+struct fastlsh_params {
+    int32_t n = 0, m = 0, k = 0;
+    float w = 1.0f;
+    bool is_e2lsh = false;
+    std::vector<int32_t> idx;  // [k][m] canonical (paper) order
+    std::vector<float> a;      // [k][m]
+    std::vector<float> b;      // [k]
+    fastlsh::Packing pack;
+    bool packed = false;
+    fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
+    std::mutex mu;
+};
+
+struct fastlsh_keys {
+    int32_t L = 0, K = 0;
+    std::vector<uint64_t> r;  // [L][K+1]
+    uint64_t* dev_r[fastlsh::kMaxDevices] = {};
+    std::mutex mu;
+};
+
+namespace fastlsh {
+
+// packer.cpp
+void build_packing(const fastlsh_params& p, Packing& out);
+
+// gather.cu
+fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
+                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+// keys.cu
+fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r,
+                                 const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
+                                 int64_t ldk, cudaStream_t stream);
+// e2lsh_tcgen05.cu
+fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N,
+                            int32_t* codes, float* proj, int precision, cudaStream_t stream);
+
+fastlsh_status set_cuda_error(cudaError_t e);
+
+}  // namespace fastlsh

@@ -1,0 +1,371 @@
+// packer.cpp — offline bank scheduling of the sampled slots.
+//
+// Addition commutes, so the order in which a hash's m products are accumulated is free
+// (Eq. 5 fixes the value, not the order). The packer uses that freedom so that the
+// gather kernel's shared-memory loads are conflict-free:
+//
+//  1. Each hash's m slots (in paper order) are split into `parts` contiguous lane units.
+//  2. The units of a CTA hash block are grouped 8 at a time into quarter-warps. One LDS.128
+//     wavefront serves 8 lanes; two lanes conflict when their 16-B chunk positions differ but
+//     fall in the same bank group (pos mod 8). Grouping balances the per-class load of each
+//     quarter (greedy, then swap local search).
+//  3. Each quarter's bipartite multigraph (lanes x 8 bank groups, one edge per slot) is edge
+//     coloured with Delta colours by König's alternating-path method; a colour is a slot
+//     position at which every lane and every bank group is used at most once.
+//  4. Free (lane, position) pairs become padding slots: coefficient 0 reading a zero chunk of a
+//     bank group unused at that position.
+//
+// Everything is deterministic, so every rank derives the identical packing (and hence the
+// identical fp32 summation order) from the same params.
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+
+#include "internal.h"
+
+namespace fastlsh {
+namespace {
+
+struct Edge {
+    int lane;   // lane within quarter
+    int cls;    // bank group (pos mod 8)
+    int pos;    // chunk position
+    float coef;
+    int color = -1;
+};
+
+struct Unit {
+    int hash, part;
+    std::vector<std::pair<int, float>> slots;  // (pos, coef)
+    std::array<int, 8> cnt{};
+    int deg = 0;
+};
+
+inline int chunk_pos(int c, int nq) { return (c & 3) * nq + (c >> 2); }
+
+struct QuarterState {
+    std::vector<int> members;  // unit ids
+    std::array<int, 8> load{};
+    int maxload() const { return *std::max_element(load.begin(), load.end()); }
+    long sumsq() const {
+        long s = 0;
+        for (int v : load) s += (long)v * v;
+        return s;
+    }
+};
+
+// Group the units of one block into Q quarters of <= 8 lanes with balanced class loads.
+std::vector<QuarterState> group_units(const std::vector<Unit>& units, int Q, int dmax) {
+    std::vector<QuarterState> qs(Q);
+    std::vector<int> order(units.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        int ma = *std::max_element(units[a].cnt.begin(), units[a].cnt.end());
+        int mb = *std::max_element(units[b].cnt.begin(), units[b].cnt.end());
+        return ma > mb;
+    });
+    // even fill: quarter capacity is ceil(U / Q) (<= 8) so empty lanes are spread out
+    const int cap = std::min<int>(8, (int)((units.size() + Q - 1) / Q));
+    for (int u : order) {
+        int best = -1;
+        long best_key0 = 0, best_key1 = 0;
+        for (int q = 0; q < Q; ++q) {
+            if ((int)qs[q].members.size() >= cap) continue;
+            int ml = 0;
+            long ss = 0;
+            for (int c = 0; c < 8; ++c) {
+                int v = qs[q].load[c] + units[u].cnt[c];
+                ml = std::max(ml, v);
+                ss += (long)v * v;
+            }
+            long k0 = ml, k1 = ss * 16 + (long)qs[q].members.size();
+            if (best < 0 || k0 < best_key0 || (k0 == best_key0 && k1 < best_key1)) {
+                best = q; best_key0 = k0; best_key1 = k1;
+            }
+        }
+        qs[best].members.push_back(u);
+        for (int c = 0; c < 8; ++c) qs[best].load[c] += units[u].cnt[c];
+    }
+    // local search on the excess over a target T: F = sum_q sum_c max(0, load - T)^2.
+    // Start at T = dmax (perfect balance); if no swap/move lowers F any more, relax T by one.
+    auto excess = [](const std::array<int, 8>& l, int T) {
+        long e = 0;
+        for (int v : l) if (v > T) e += (long)(v - T) * (v - T);
+        return e;
+    };
+    int T = dmax;
+    for (int guard = 0; guard < 64; ++guard, ++T) {
+        bool any_excess = false;
+        for (int sweep = 0; sweep < 200; ++sweep) {
+            bool improved = false;
+            any_excess = false;
+            for (int q = 0; q < Q; ++q) {
+                const long eq = excess(qs[q].load, T);
+                if (eq == 0) continue;
+                any_excess = true;
+                long best = 0;
+                int bi = -1, bq = -1, bj = -1;
+                const auto& A = qs[q];
+                for (int ii = 0; ii < (int)A.members.size(); ++ii) {
+                    const Unit& u = units[A.members[ii]];
+                    for (int q2 = 0; q2 < Q; ++q2) {
+                        if (q2 == q) continue;
+                        const auto& B = qs[q2];
+                        const int n2 = (int)B.members.size();
+                        const long e2 = excess(B.load, T);
+                        for (int jj = -1; jj < n2; ++jj) {
+                            if (jj < 0 && n2 >= 8) continue;
+                            std::array<int, 8> a = A.load, b = B.load;
+                            for (int c = 0; c < 8; ++c) { a[c] -= u.cnt[c]; b[c] += u.cnt[c]; }
+                            if (jj >= 0) {
+                                const Unit& v = units[B.members[jj]];
+                                for (int c = 0; c < 8; ++c) { a[c] += v.cnt[c]; b[c] -= v.cnt[c]; }
+                            }
+                            const long d = excess(a, T) + excess(b, T) - eq - e2;
+                            if (d < best) { best = d; bi = ii; bq = q2; bj = jj; }
+                        }
+                    }
+                }
+                if (bi < 0) continue;
+                improved = true;
+                auto& Am = qs[q];
+                auto& Bm = qs[bq];
+                const int u = Am.members[bi];
+                for (int c = 0; c < 8; ++c) { Am.load[c] -= units[u].cnt[c]; Bm.load[c] += units[u].cnt[c]; }
+                if (bj >= 0) {
+                    const int v = Bm.members[bj];
+                    for (int c = 0; c < 8; ++c) { Am.load[c] += units[v].cnt[c]; Bm.load[c] -= units[v].cnt[c]; }
+                    Am.members[bi] = v;
+                    Bm.members[bj] = u;
+                } else {
+                    Am.members.erase(Am.members.begin() + bi);
+                    Bm.members.push_back(u);
+                }
+            }
+            if (!any_excess || !improved) break;
+        }
+        if (!any_excess) break;
+    }
+    return qs;
+}
+
+// König edge colouring of a bipartite multigraph (lanes x 8 classes) with `ncol` colours,
+// ncol >= max degree. Returns false if some edge could not be coloured (never for a valid ncol).
+bool color_quarter(std::vector<Edge>& edges, int nlanes, int ncol) {
+    std::vector<int> lane_col((size_t)nlanes * ncol, -1), cls_col((size_t)8 * ncol, -1);
+    auto L = [&](int l, int t) -> int& { return lane_col[(size_t)l * ncol + t]; };
+    auto C = [&](int c, int t) -> int& { return cls_col[(size_t)c * ncol + t]; };
+    for (int e = 0; e < (int)edges.size(); ++e) {
+        const int l = edges[e].lane, c = edges[e].cls;
+        int alpha = -1, beta = -1;
+        for (int t = 0; t < ncol && alpha < 0; ++t) if (L(l, t) < 0) alpha = t;
+        for (int t = 0; t < ncol && beta < 0; ++t) if (C(c, t) < 0) beta = t;
+        if (alpha < 0 || beta < 0) return false;
+        if (C(c, alpha) >= 0) {
+            // flip the alpha/beta alternating path that starts at class c
+            std::vector<int> path;
+            bool at_class = true;
+            int v = c, col = alpha;
+            for (;;) {
+                int e2 = at_class ? C(v, col) : L(v, col);
+                if (e2 < 0) break;
+                path.push_back(e2);
+                v = at_class ? edges[e2].lane : edges[e2].cls;
+                at_class = !at_class;
+                col = (col == alpha) ? beta : alpha;
+            }
+            for (int e2 : path) {
+                L(edges[e2].lane, edges[e2].color) = -1;
+                C(edges[e2].cls, edges[e2].color) = -1;
+            }
+            for (int e2 : path) {
+                edges[e2].color = (edges[e2].color == alpha) ? beta : alpha;
+                L(edges[e2].lane, edges[e2].color) = e2;
+                C(edges[e2].cls, edges[e2].color) = e2;
+            }
+        }
+        edges[e].color = alpha;
+        L(l, alpha) = e;
+        C(c, alpha) = e;
+    }
+    return true;
+}
+
+struct Trial {
+    Packing pk;
+    double cost = 1e300;
+};
+
+void try_parts(const fastlsh_params& p, int P, Trial& out) {
+    const int n = p.n, m = p.m, k = p.k;
+    Packing pk;
+    pk.parts = P;
+    pk.nq = (n + 3) / 4;
+    pk.stage_chunks = 4 * pk.nq + kPadChunks;
+    const int dmax = (m + P - 1) / P;
+    const int lanes_cap = 256;                  // 8 warps per CTA
+    const int kb_cap = std::max(1, lanes_cap / P);
+    const int HB = (k + kb_cap - 1) / kb_cap;
+    pk.hash_blocks = HB;
+    pk.block_h0.resize(HB);
+    pk.block_kb.resize(HB);
+    int h0 = 0;
+    for (int bl = 0; bl < HB; ++bl) {
+        pk.block_kb[bl] = k / HB + (bl < k % HB ? 1 : 0);
+        pk.block_h0[bl] = h0;
+        h0 += pk.block_kb[bl];
+    }
+    pk.kb_max = *std::max_element(pk.block_kb.begin(), pk.block_kb.end());
+    pk.warps = (pk.kb_max * P + 31) / 32;
+    const int Wn = pk.warps, Q = 4 * Wn;
+
+    struct QuarterPlan {
+        std::vector<int> members;
+        std::vector<Edge> edges;
+        int delta;
+    };
+    std::vector<std::vector<QuarterPlan>> plans(HB);
+    std::vector<std::vector<Unit>> block_units(HB);
+    int MS = 2;
+    for (int bl = 0; bl < HB; ++bl) {
+        auto& units = block_units[bl];
+        for (int hh = 0; hh < pk.block_kb[bl]; ++hh) {
+            const int h = pk.block_h0[bl] + hh;
+            for (int q = 0; q < P; ++q) {
+                Unit u;
+                u.hash = hh;
+                u.part = q;
+                const int j0 = (int)((long)q * m / P), j1 = (int)((long)(q + 1) * m / P);
+                for (int j = j0; j < j1; ++j) {
+                    int pos = chunk_pos(p.idx[(size_t)h * m + j], pk.nq);
+                    u.slots.push_back({pos, p.a[(size_t)h * m + j]});
+                    u.cnt[pos & 7]++;
+                }
+                u.deg = j1 - j0;
+                units.push_back(std::move(u));
+            }
+        }
+        auto qs = group_units(units, Q, dmax);
+        plans[bl].resize(Q);
+        for (int q = 0; q < Q; ++q) {
+            auto& qp = plans[bl][q];
+            qp.members = qs[q].members;
+            int d = 0;
+            for (int li = 0; li < (int)qp.members.size(); ++li) {
+                const Unit& u = units[qp.members[li]];
+                d = std::max(d, u.deg);
+                for (auto& s : u.slots) qp.edges.push_back(Edge{li, s.first & 7, s.first, s.second});
+            }
+            d = std::max(d, qs[q].maxload());
+            qp.delta = d;
+            if (!color_quarter(qp.edges, std::max<int>(1, qp.members.size()), std::max(1, d))) {
+                qp.delta = -1;  // cannot happen for a valid Delta
+            }
+            MS = std::max(MS, d);
+        }
+    }
+    if (std::getenv("FASTLSH_PACK_DEBUG")) {
+        std::vector<int> hist(4 * kMaxSlots + 8, 0);
+        for (int bl = 0; bl < HB; ++bl)
+            for (auto& qp : plans[bl]) hist[std::min<int>(qp.delta, hist.size() - 1)]++;
+        std::fprintf(stderr, "[pack] P=%d dmax=%d HB=%d W=%d delta histogram:", P, dmax, HB, Wn);
+        for (size_t d = 0; d < hist.size(); ++d) if (hist[d]) std::fprintf(stderr, " %zu:%d", d, hist[d]);
+        std::fprintf(stderr, "\n");
+    }
+    // fold colours beyond kMaxSlots into existing positions (creates bank conflicts)
+    int64_t conflicts = 0;
+    if (MS > kMaxSlots) MS = kMaxSlots;
+    MS = (MS + 1) & ~1;
+    pk.slots = MS;
+
+    const size_t lanes_total = (size_t)HB * Wn * 32;
+    pk.offp.assign(lanes_total * (MS / 2), 0);
+    pk.coef.assign(lanes_total * MS, 0.0f);
+    pk.unit_lane.assign((size_t)HB * pk.kb_max * P, 0);
+    int64_t useful = 0;
+    for (int bl = 0; bl < HB; ++bl) {
+        const auto& units = block_units[bl];
+        for (int q = 0; q < Q; ++q) {
+            auto& qp = plans[bl][q];
+            const int w = q / 4, qi = q % 4;
+            // slot table: pos[t][lane], coef[t][lane], -1 = free
+            std::vector<int> tpos((size_t)MS * 8, -1);
+            std::vector<float> tcoef((size_t)MS * 8, 0.0f);
+            std::vector<int> used_cls((size_t)MS * 8, 0);  // #lanes per (t, class)
+            std::vector<Edge*> overflow;
+            for (auto& e : qp.edges) {
+                if (e.color >= 0 && e.color < MS) {
+                    tpos[(size_t)e.color * 8 + e.lane] = e.pos;
+                    tcoef[(size_t)e.color * 8 + e.lane] = e.coef;
+                    used_cls[(size_t)e.color * 8 + e.cls]++;
+                } else {
+                    overflow.push_back(&e);
+                }
+            }
+            for (Edge* e : overflow) {
+                int bt = -1, bu = 1 << 30;
+                for (int t = 0; t < MS; ++t) {
+                    if (tpos[(size_t)t * 8 + e->lane] >= 0) continue;
+                    int u = used_cls[(size_t)t * 8 + e->cls];
+                    if (u < bu) { bu = u; bt = t; }
+                }
+                tpos[(size_t)bt * 8 + e->lane] = e->pos;
+                tcoef[(size_t)bt * 8 + e->lane] = e->coef;
+                used_cls[(size_t)bt * 8 + e->cls]++;
+            }
+            for (int t = 0; t < MS; ++t) {
+                int mx = 0;
+                for (int c = 0; c < 8; ++c) mx = std::max(mx, used_cls[(size_t)t * 8 + c]);
+                if (mx > 1) conflicts += mx - 1;
+                // padding: every free lane reads the zero chunk of one unused bank group
+                int freec = -1;
+                for (int c = 0; c < 8 && freec < 0; ++c) if (used_cls[(size_t)t * 8 + c] == 0) freec = c;
+                if (freec < 0) freec = 0;
+                const int padpos = 4 * pk.nq + (((freec - 4 * pk.nq) % 8) + 8) % 8;
+                for (int l = 0; l < 8; ++l) {
+                    if (tpos[(size_t)t * 8 + l] < 0) { tpos[(size_t)t * 8 + l] = padpos; tcoef[(size_t)t * 8 + l] = 0.0f; }
+                }
+            }
+            for (int l = 0; l < 8; ++l) {
+                const int lane = qi * 8 + l;
+                const size_t wl = ((size_t)bl * Wn + w);
+                for (int t = 0; t < MS; ++t) {
+                    const uint32_t off = (uint32_t)tpos[(size_t)t * 8 + l] * 16u;
+                    uint32_t& word = pk.offp[(wl * (MS / 2) + t / 2) * 32 + lane];
+                    word |= (t & 1) ? (off << 16) : off;
+                    pk.coef[(wl * MS + t) * 32 + lane] = tcoef[(size_t)t * 8 + l];
+                }
+                if (l < (int)qp.members.size()) {
+                    const Unit& u = units[qp.members[l]];
+                    pk.unit_lane[((size_t)bl * pk.kb_max + u.hash) * P + u.part] = (uint16_t)(w * 32 + lane);
+                    useful += u.deg;
+                }
+            }
+        }
+    }
+    pk.conflict_wavefronts = conflicts;
+    pk.efficiency = (double)useful / ((double)lanes_total * MS);
+    // cost in smem wavefronts per row: 4 per LDS.128 per warp per slot (one per quarter) + conflicts
+    out.cost = (double)HB * Wn * MS + (double)conflicts / 4.0;
+    out.pk = std::move(pk);
+}
+
+}  // namespace
+
+void build_packing(const fastlsh_params& p, Packing& out) {
+    const int pmin = (p.m + kMaxSlots - 1) / kMaxSlots;
+    Trial best;
+    for (int P = pmin; P <= std::min(p.m, pmin + 2); ++P) {
+        // beyond 256 lanes per hash the block holds a single hash; keep P <= 256
+        if (P > 256) break;
+        Trial t;
+        try_parts(p, P, t);
+        if (t.cost < best.cost) best = std::move(t);
+    }
+    out = std::move(best.pk);
+}
+
+}  // namespace fastlsh

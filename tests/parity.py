@@ -1,0 +1,50 @@
+"""The parity rule of north_star / SURVEY.md §8(c), applied to GPU results vs the CPU oracle.
+
+  projections: |p_gpu - p| <= 1e-5 * ||a_i|| * ||S_i(v)||               (north_star tolerance)
+  codes:       equal wherever floor((p - tau + b)/w) == floor((p + tau + b)/w);
+               inside that band, one of the two values,
+               with tau = 1e-5 * scale + 2^-22 * (|p| + |b|)            (reading R5:
+               the fp32 +b and /w roundings add at most ~1.5 ulp of |p + b|)
+  sentinel:    INT32_MIN where the oracle's quotient is non-finite or outside (-2^31, 2^31).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+INT32_MIN = -(2 ** 31)
+
+
+def check_projections(p_gpu, p, scale, tol=1e-5):
+    p_gpu = np.asarray(p_gpu, np.float64)
+    err = np.abs(p_gpu - p)
+    bound = tol * scale
+    bad = ~(err <= bound)
+    assert not bad.any(), (f"{int(bad.sum())} projections outside 1e-5*scale; worst rel "
+                           f"{float(np.max(err / np.maximum(scale, 1e-300)))}")
+    rel = err / np.maximum(scale, 1e-300)
+    return float(rel.max()) if rel.size else 0.0
+
+
+def expected_code_band(p, scale, b, w):
+    tau = 1e-5 * scale + 2.0 ** -22 * (np.abs(p) + np.abs(b)[None, :])
+    lo = np.floor((p - tau + b[None, :]) / w)
+    hi = np.floor((p + tau + b[None, :]) / w)
+    return lo, hi
+
+
+def check_codes(codes_gpu, p, scale, code_oracle, b, w):
+    """Returns the fraction of (row, hash) pairs whose oracle projection lies in the ambiguity band."""
+    codes_gpu = np.asarray(codes_gpu, np.int64)
+    b = np.asarray(b, np.float64)
+    lo, hi = expected_code_band(p, scale, b, w)
+    out_of_range = (code_oracle <= INT32_MIN) | (code_oracle > 2 ** 31 - 1)
+    ambig = (lo != hi) & ~out_of_range
+    exact = ~ambig & ~out_of_range
+    mism = exact & (codes_gpu != code_oracle)
+    assert not mism.any(), (f"{int(mism.sum())} code mismatches outside the band, e.g. at "
+                            f"{np.argwhere(mism)[:5].tolist()}")
+    inb = ambig & ((codes_gpu < lo) | (codes_gpu > hi))
+    assert not inb.any(), f"{int(inb.sum())} codes outside their band"
+    if out_of_range.any():
+        assert (codes_gpu[out_of_range] == INT32_MIN).all()
+    return float(ambig.mean()) if ambig.size else 0.0

@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Inputs (S_i, a_i, b_i, X) come from fastlsh_inputs only; the oracle never sees a value produced
+by the CUDA path. X is generated on the device by torch (plumbing) and the exact bytes hashed are
+copied to the host for the oracle.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2309_15479_b200 as fl
+from fastlsh_inputs import configs, data, fastlsh_arrays, e2lsh_arrays, philox
+from oracle import keys as okeys
+from parity import check_codes, check_projections
+
+pytestmark = pytest.mark.gpu
+THREADS = max(1, min(16, len(os.sched_getaffinity(0))))
+
+
+def _params(n, m, k, w, seed=1):
+    idx, a, b = fastlsh_arrays(n, m, k, w, seed)
+    return fl.Params.from_arrays(n, w, idx, a, b), idx, a, b
+
+
+def _run_and_check(P, idx, a, b, w, X_dev, rows=None):
+    """Hash X_dev on the GPU; compare all rows (rows=None) or the given row sample with the oracle."""
+    codes = fl.fastlsh_hash(P, X_dev)
+    proj = fl.fastlsh_project(P, X_dev)
+    torch.cuda.synchronize()
+    if rows is None:
+        Xh = X_dev.cpu().numpy()
+        cg, pg = codes.cpu().numpy(), proj.cpu().numpy()
+    else:
+        ri = torch.as_tensor(rows, device=X_dev.device)
+        Xh = X_dev[ri].cpu().numpy()
+        cg, pg = codes[ri].cpu().numpy(), proj[ri].cpu().numpy()
+    p, scale, code = oracle.fastlsh(Xh, idx, a, b, w, threads=THREADS)
+    rel = check_projections(pg, p, scale)
+    amb = check_codes(cg, p, scale, code, b, w)
+    return rel, amb, codes
+
+
+def _sample_rows(N, count, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    r = set(rng.choice(N, size=min(count, N), replace=False).tolist())
+    r.update([0, N - 1, *[x for x in extra if 0 <= x < N]])
+    return np.array(sorted(r), dtype=np.int64)
+
+
+# ---- C0: full parity ----------------------------------------------------------------------------
+
+def test_c0_full_parity():
+    c = configs.get("C0")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w, c.seed)
+    X = data.generate(c.data, c.n, 0, c.N, seed=c.seed, device="cuda")
+    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X)
+    assert rel < 1e-6
+    assert amb < 5e-3
+
+
+# ---- C1-C4 at small N (all rows, several tiles + ragged tail) and full N (sampled rows) ----------
+
+SMALL = [("C1", None, 2003), ("C2", 32, 517), ("C2", 128, 261), ("C2", 512, 131), ("C2", 4096, 21),
+         ("C3", None, 4099), ("C4", None, 1001)]
+
+
+@pytest.mark.parametrize("name,m,N", SMALL)
+def test_small_full_parity(name, m, N):
+    c = configs.get(name)
+    m = m or c.m
+    P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
+    X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
+    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X)
+    assert amb < 1e-2
+
+
+FULL = [("C1", None, None, 2048), ("C2", 32, None, 1024), ("C2", 4096, None, 64), ("C3", None, 4_000_000, 2048),
+        ("C4", None, None, 2048)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,m,N,sample", FULL)
+def test_full_size_sampled_parity(name, m, N, sample):
+    """At BASELINE sizes in the bench launch configuration, sampled rows vs the oracle."""
+    c = configs.get(name)
+    m = m or c.m
+    N = N or c.N
+    P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
+    X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
+    rows = _sample_rows(N, sample, seed=7, extra=[N // 2, N - 2, 4 * (N // 8) - 1])
+    _run_and_check(P, idx, a, b, c.w, X, rows=rows)
+    del X
+    torch.cuda.empty_cache()
+
+
+# ---- params drawn by the library from the seed == inputs-module arrays ---------------------------
+
+def test_seeded_params_path_matches_oracle():
+    c = configs.get("C0")
+    P = fl.Params.create(c.n, c.m, c.k, c.w, seed=c.seed)
+    idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, c.seed)
+    X = data.generate(c.data, c.n, 0, 3000, seed=c.seed, device="cuda")
+    _run_and_check(P, idx, a, b, c.w, X)
+
+
+# ---- edge cases -----------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("N,n,m,k", [(1, 128, 16, 64), (5, 130, 7, 33), (77, 37, 50, 9), (64, 1, 5, 3),
+                                     (33, 8, 1, 1), (130, 256, 200, 20), (9, 96, 64, 257), (300, 4, 4, 100)])
+def test_edge_shapes(N, n, m, k):
+    P, idx, a, b = _params(n, m, k, 1.5, seed=N + n)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(N * 31 + n)
+    X = torch.randn((N, n), generator=g, device="cuda")
+    _run_and_check(P, idx, a, b, 1.5, X)
+
+
+def test_empty_input_is_noop():
+    P, *_ = _params(16, 4, 8, 1.0)
+    X = torch.zeros((0, 16), device="cuda")
+    out = fl.fastlsh_hash(P, X)
+    assert out.shape == (0, 8)
+
+
+def test_misaligned_rows_take_scalar_path():
+    P, idx, a, b = _params(64, 16, 40, 1.0)
+    base = torch.randn(100 * 64 + 1, device="cuda")
+    X = base[1:].view(100, 64)  # 4-byte aligned, not 16-byte aligned
+    assert X.data_ptr() % 16 != 0
+    _run_and_check(P, idx, a, b, 1.0, X)
+
+
+def test_zero_rows_give_floor_b_over_w():
+    P, idx, a, b = _params(96, 16, 64, 2.0)
+    X = torch.zeros((10, 96), device="cuda")
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    assert (codes == 0).all()  # b in [0, w): floor(b/w) = 0 exactly (R5)
+
+
+def test_nonfinite_and_saturation_flags():
+    n, m, k = 32, 8, 16
+    idx = np.tile(np.arange(m, dtype=np.int32), (k, 1))
+    a = np.ones((k, m), np.float32)
+    b = np.zeros(k, np.float32)
+    P = fl.Params.from_arrays(n, 1e-3, idx, a, b)
+    X = torch.zeros((4, n), device="cuda")
+    X[1, 0] = float("nan")
+    X[2, 0] = float("inf")
+    X[3, 0] = 1e30
+    fl.read_flags(P, reset=True)
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    assert (codes[0] == 0).all()
+    assert (codes[1:] == -(2 ** 31)).all()
+    nf, sat = fl.read_flags(P, reset=True)
+    assert nf == 2 * k and sat == k
+
+
+# ---- structure: determinism, chunking, identity plan, host path -------------------------------------
+
+def test_determinism_and_chunk_invariance():
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    X = data.generate(c.data, c.n, 0, 5000, seed=1, device="cuda")
+    c1 = fl.fastlsh_hash(P, X)
+    c2 = fl.fastlsh_hash(P, X)
+    parts = [fl.fastlsh_hash(P, X[i:j].contiguous()) for i, j in [(0, 1234), (1234, 1235), (1235, 5000)]]
+    assert torch.equal(c1, c2)
+    assert torch.equal(c1, torch.cat(parts))
+    pr1 = fl.fastlsh_project(P, X)
+    pr2 = torch.cat([fl.fastlsh_project(P, X[i:j].contiguous()) for i, j in [(0, 777), (777, 5000)]])
+    assert torch.equal(pr1, pr2)
+
+
+def test_identity_plan_matches_e2lsh_oracle():
+    n, k, w = 64, 96, 1.0
+    idx, A, b = e2lsh_arrays(n, k, w, seed=4)
+    P = fl.Params.from_arrays(n, w, idx, A, b)
+    X = torch.randn((500, n), device="cuda")
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    proj = fl.fastlsh_project(P, X).cpu().numpy()
+    p, s, code = oracle.e2lsh(X.cpu().numpy(), A, b, w)
+    check_projections(proj, p, s)
+    check_codes(codes, p, s, code, b, w)
+
+
+def test_host_entry_point_matches_device_path():
+    c = configs.get("C4")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    K = fl.Keys.create(c.L, c.K, seed=1)
+    X = data.generate(c.data, c.n, 0, 10_000, seed=1, device="cuda")
+    codes_d, keys_d = fl.hash_keys(P, K, X)
+    Xh = X.cpu().pin_memory()
+    codes_h, keys_h = fl.hash_host(P, K, Xh, chunk_rows=3000)
+    assert torch.equal(codes_d.cpu(), codes_h)
+    assert torch.equal(keys_d.cpu(), keys_h)
+
+
+# ---- compound keys: bit-exact vs Python big integers, on seeded code matrices ------------------------
+
+@pytest.mark.parametrize("L,K,N,ldk_pad", [(50, 10, 1000, 0), (16, 16, 333, 5), (200, 10, 257, 0), (1, 1, 7, 0)])
+def test_keys_bit_exact(L, K, N, ldk_pad):
+    r = philox.key_multipliers(L, K, seed=3)
+    Kobj = fl.Keys.from_arrays(r)
+    codes = data.random_codes(N, L * K + 3, seed=L + K, lo=-(2 ** 31), hi=2 ** 31 - 1)
+    keys_gpu = fl.build_keys(Kobj, codes.cuda(), ldk=N + ldk_pad)[:, :N].cpu().numpy().view(np.uint64)
+    ref = okeys.build_keys(codes.numpy(), r, L, K)
+    assert np.array_equal(keys_gpu, ref)
+
+
+def test_keys_from_oracle_codes_c1():
+    c = configs.get("C1")
+    idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 1)
+    X = data.generate(c.data, c.n, 0, 200, seed=1).numpy()
+    _, _, code = oracle.fastlsh(X, idx, a, b, c.w, threads=THREADS)
+    r = philox.key_multipliers(c.L, c.K, seed=1)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1)
+    keys_gpu = fl.build_keys(Kobj, torch.as_tensor(code.astype(np.int32)).cuda()).cpu().numpy().view(np.uint64)
+    assert np.array_equal(keys_gpu, okeys.build_keys(code, r, c.L, c.K))

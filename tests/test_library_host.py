@@ -1,0 +1,156 @@
+"""Host-side checks of libfastlsh (no GPU needed): ABI surface, params generation, packer."""
+import ctypes
+import os
+import re
+from collections import Counter
+
+import numpy as np
+import pytest
+
+import paper_2309_15479_b200 as fl
+from fastlsh_inputs import fastlsh_arrays, e2lsh_arrays, philox, configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2309_15479_b200 import build
+    build.build()
+    return fl.load_library()
+
+
+def _declared_functions():
+    with open(os.path.join(ROOT, "include", "fastlsh.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fastlsh_\w+|e2lsh_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    decl = _declared_functions()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), f"missing export {name}"
+    assert set(decl) == set(fl.EXPORTED)
+    assert lib.fastlsh_abi_version() == 1
+
+
+def test_params_from_seed_match_independent_generator(lib):
+    """The library's C++ Philox and fastlsh_inputs' numpy Philox implement the same spec."""
+    for (n, m, k, w) in [(128, 16, 64, 4.0), (960, 60, 500, 1.0), (37, 50, 9, 0.5)]:
+        p = fl.Params.create(n, m, k, w, seed=1)
+        idx, a, b, ww = p.export()
+        i2, a2, b2 = fastlsh_arrays(n, m, k, w, seed=1)
+        assert np.array_equal(idx, i2) and np.array_equal(a, a2) and np.array_equal(b, b2)
+        assert ww == np.float32(w)
+
+
+def test_e2lsh_params_share_coefficient_stream(lib):
+    p = fl.Params.e2lsh(24, 7, 1.0, seed=3)
+    idx, a, b, _ = p.export()
+    i2, a2, b2 = e2lsh_arrays(24, 7, 1.0, seed=3)
+    assert np.array_equal(idx, i2) and np.array_equal(a, a2) and np.array_equal(b, b2)
+    assert p.info()["is_e2lsh"] == 1
+
+
+def test_keys_from_seed_match_independent_generator(lib):
+    k = fl.Keys.create(50, 10, seed=1)
+    assert np.array_equal(k.export(), philox.key_multipliers(50, 10, seed=1))
+
+
+@pytest.mark.parametrize("args", [(0, 4, 4, 1.0), (8, 0, 4, 1.0), (8, 4, 0, 1.0), (8, 4, 4, 0.0),
+                                  (8, 4, 4, -1.0), (8, 4, 4, float("nan")), (8, 4, 4, float("inf"))])
+def test_invalid_params_rejected(lib, args):
+    h = ctypes.c_void_p()
+    assert lib.fastlsh_params_create(*args, 1, ctypes.byref(h)) == fl.EINVAL
+    assert not h.value
+
+
+def test_from_arrays_rejects_out_of_range_index(lib):
+    idx = np.array([[0, 5]], np.int32)
+    a = np.ones((1, 2), np.float32)
+    b = np.zeros(1, np.float32)
+    with pytest.raises(fl.FastLSHError):
+        fl.Params.from_arrays(5, 1.0, idx, a, b)
+    idx[0, 1] = -1
+    with pytest.raises(fl.FastLSHError):
+        fl.Params.from_arrays(5, 1.0, idx, a, b)
+
+
+def test_keys_invalid(lib):
+    h = ctypes.c_void_p()
+    assert lib.fastlsh_keys_create(0, 3, 1, ctypes.byref(h)) == fl.EINVAL
+    r = np.full((1, 2), (1 << 61) - 1, np.uint64)  # not reduced mod p
+    assert lib.fastlsh_keys_create_from_arrays(1, 1, r.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h)) == fl.EINVAL
+
+
+def test_gpu_calls_without_device_fail_loudly(lib):
+    """No CPU fallback: hashing needs an uploaded params object on a B200."""
+    p = fl.Params.create(16, 4, 8, 1.0, seed=1)
+    rc = lib.fastlsh_hash(p._h, ctypes.c_void_p(16), 1, ctypes.c_void_p(16), None)
+    assert rc in (fl.ESTATE, fl.ECUDA, fl.EUNSUPPORTED)
+
+
+def _unpack(p):
+    """Decode the packing into per-(hash, part) slot multisets and check its invariants."""
+    pk = p.packing()
+    idx, a, b, _ = p.export()
+    nq, MS, W, HB, P = pk["nq"], pk["slots"], pk["warps"], pk["hash_blocks"], pk["parts"]
+    offs = np.empty((HB, W, MS, 32), np.int64)
+    offs[:, :, 0::2, :] = pk["offp"] & 0xFFFF
+    offs[:, :, 1::2, :] = pk["offp"] >> 16
+    assert (offs % 16 == 0).all()
+    pos = offs // 16
+    assert (pos < 4 * nq + 8).all()
+    coef = pk["coef"]
+    # bank groups: at every slot, the 8 lanes of a quarter touch distinct groups (or equal chunks)
+    conflicts = 0
+    for bl in range(HB):
+        for w in range(W):
+            for t in range(MS):
+                for q in range(4):
+                    ps = set(int(x) for x in pos[bl, w, t, 8 * q:8 * q + 8])
+                    groups = Counter(x % 8 for x in ps)
+                    conflicts += max(groups.values()) - 1
+    # padding slots: zero coefficient on a zero chunk
+    pad = pos >= 4 * nq
+    assert (coef[pad] == 0).all()
+    # every hash's multiset {(column, coefficient)} is preserved across its parts
+    for bl in range(HB):
+        h0, kb = int(pk["block_h0"][bl]), int(pk["block_kb"][bl])
+        for hh in range(kb):
+            got = Counter()
+            for part in range(P):
+                lane = int(pk["unit_lane"][bl, hh, part])
+                w, l = divmod(lane, 32)
+                for t in range(MS):
+                    ps = int(pos[bl, w, t, l])
+                    if ps < 4 * nq:
+                        i, qd = divmod(ps, nq)
+                        got[(4 * qd + i, float(coef[bl, w, t, l]))] += 1
+            want = Counter((int(c), float(x)) for c, x in zip(idx[h0 + hh], a[h0 + hh]))
+            assert got == want, f"hash {h0 + hh}"
+    assert sum(int(x) for x in pk["block_kb"]) == p.k
+    return pk, conflicts
+
+
+@pytest.mark.parametrize("n,m,k", [(128, 16, 64), (960, 60, 500), (37, 50, 9), (130, 7, 33), (1, 5, 3),
+                                   (784, 64, 200), (256, 200, 20)])
+def test_packer_preserves_slots_and_avoids_conflicts(lib, n, m, k):
+    p = fl.Params.create(n, m, k, 1.0, seed=5)
+    pk, conflicts = _unpack(p)
+    info = p.info()
+    assert info["slots"] == pk["slots"] and info["slots"] <= 64 and info["slots"] % 2 == 0
+    if info["conflict_wavefronts"] == 0:
+        assert conflicts == 0
+    if n >= 64 and 16 <= m <= 64 and k >= 64:
+        assert info["bank_efficiency"] > 0.75
+
+
+def test_bench_config_packing_quality(lib):
+    c = configs.get("C1")
+    p = fl.Params.create(c.n, c.m, c.k, c.w, seed=1)
+    info = p.info()
+    assert info["conflict_wavefronts"] == 0
+    assert info["bank_efficiency"] >= 0.93
