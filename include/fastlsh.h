@@ -64,8 +64,8 @@ typedef struct {
  *   idx[i][j] = hi64(u64(philox(j,i,1)) * n),  a[i][j] = BoxMuller(philox(j,i,2)) as f32,
  *   b[i] = f32(w * u53(philox(0,i,3))) clamped to [0, w).
  * n, m, k >= 1; w finite and > 0; m > n is legal (sampling with replacement).
- * EINVAL otherwise. EUNSUPPORTED if n > 16352 (offsets are packed as 16-bit smem byte offsets)
- * or m > 16384. */
+ * EINVAL otherwise. EUNSUPPORTED if n > 6400 (two 4-row stages of X must fit in 227 KB of
+ * shared memory) or m > 16384. */
 fastlsh_status fastlsh_params_create(int32_t n, int32_t m, int32_t k, float w, uint64_t seed,
                                      fastlsh_params** out);
 
@@ -91,7 +91,7 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* p, fastlsh_params_info_
 
 /* Diagnostic: copy the GPU packing out (for host-side verification of the bank scheduler).
  * sizes[0..7] = {parts, slots, warps, hash_blocks, kb_max, nq, stage_chunks, n_lanes_total}.
- * Arrays (any may be NULL): offp u32[HB*W*slots/2*32], coef f32[HB*W*slots*32],
+ * Arrays (any may be NULL): offp u32[HB*W*slots*32] (smem byte offsets), coef f32[HB*W*slots*32],
  * unit_lane u16[HB*kb_max*parts], block_h0 int32[HB], block_kb int32[HB]. */
 fastlsh_status fastlsh_params_packing(const fastlsh_params* p, int32_t* sizes, uint32_t* offp,
                                       float* coef, uint16_t* unit_lane, int32_t* block_h0,

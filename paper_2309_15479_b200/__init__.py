@@ -175,7 +175,7 @@ class Params:
         _check(self._lib.fastlsh_params_packing(self._h, _np_ptr(sz), None, None, None, None, None),
                "fastlsh_params_packing")
         P, MS, W, HB, kbm, nq, sc, lanes = (int(x) for x in sz)
-        offp = np.zeros(HB * W * (MS // 2) * 32, np.uint32)
+        offp = np.zeros(HB * W * MS * 32, np.uint32)
         coef = np.zeros(HB * W * MS * 32, np.float32)
         unit = np.zeros(HB * kbm * P, np.uint16)
         h0 = np.zeros(HB, np.int32)
@@ -183,7 +183,7 @@ class Params:
         _check(self._lib.fastlsh_params_packing(self._h, _np_ptr(sz), _np_ptr(offp), _np_ptr(coef), _np_ptr(unit),
                                                 _np_ptr(h0), _np_ptr(kb)), "fastlsh_params_packing")
         return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, nq=nq, stage_chunks=sc,
-                    offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
+                    offp=offp.reshape(HB, W, MS, 32), coef=coef.reshape(HB, W, MS, 32),
                     unit_lane=unit.reshape(HB, kbm, P), block_h0=h0, block_kb=kb)
 
     def upload(self, device=None, stream=None):
@@ -357,6 +357,7 @@ def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_h
 
 
 def read_flags(params: Params, reset: bool = False, stream=None):
+    params._ready()
     nf, sat = ctypes.c_uint64(), ctypes.c_uint64()
     _check(params._lib.fastlsh_read_flags(params._h, ctypes.byref(nf), ctypes.byref(sat), int(reset),
                                           _stream_ptr(stream)), "fastlsh_read_flags")

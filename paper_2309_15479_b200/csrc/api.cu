@@ -55,7 +55,7 @@ fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_para
     if (!out) return FASTLSH_EINVAL;
     *out = nullptr;
     if (n <= 0 || m <= 0 || k <= 0 || !valid_w(w)) return FASTLSH_EINVAL;
-    if (n > 16352) return FASTLSH_EUNSUPPORTED;       // 16-bit smem byte offsets
+    if (n > kMaxN) return FASTLSH_EUNSUPPORTED;       // two 4-row stages must fit in shared memory
     if ((int64_t)m > (int64_t)kMaxSlots * 256) return FASTLSH_EUNSUPPORTED;
     fastlsh_params* p = new (std::nothrow) fastlsh_params();
     if (!p) return FASTLSH_ENOMEM;

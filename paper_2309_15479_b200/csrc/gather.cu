@@ -4,7 +4,7 @@
 //
 // Design:
 //  * One CTA owns a block of hashes; its lanes hold their hash part's slots in registers for the
-//    whole kernel: MS 16-bit smem byte offsets (two per register) and MS f32 coefficients, in
+//    whole kernel: MS 32-bit smem byte offsets and MS f32 coefficients, in
 //    the bank-scheduled order produced by packer.cpp.
 //  * Rows are processed 4 at a time. A stage holds 4 rows column-interleaved: the 16-byte chunk
 //    at position pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per slot
@@ -136,14 +136,14 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
 
     // this lane's slots: offsets (two u16 per register) and coefficients
-    uint32_t op[MS / 2];
+    uint32_t op[MS];
     float cf[MS];
     {
         const size_t wl = (size_t)hb * a.W + warp;
-        const uint32_t* po = a.offp + wl * (MS / 2) * 32 + lane;
+        const uint32_t* po = a.offp + wl * MS * 32 + lane;
         const float* pc = a.coef + wl * MS * 32 + lane;
 #pragma unroll
-        for (int t = 0; t < MS / 2; ++t) op[t] = __ldg(po + t * 32);
+        for (int t = 0; t < MS; ++t) op[t] = __ldg(po + t * 32);
 #pragma unroll
         for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
     }
@@ -165,9 +165,8 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
 #pragma unroll
         for (int t = 0; t < MS; t += 2) {
-            const uint32_t pr = op[t >> 1];
-            const float4 v0 = lds128(base + (pr & 0xffffu));
-            const float4 v1 = lds128(base + (pr >> 16));
+            const float4 v0 = lds128(base + op[t]);
+            const float4 v1 = lds128(base + op[t + 1]);
             acc0 = fmaf(v0.x, cf[t], acc0);
             acc1 = fmaf(v0.y, cf[t], acc1);
             acc2 = fmaf(v0.z, cf[t], acc2);

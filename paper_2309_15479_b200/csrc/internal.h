@@ -15,6 +15,7 @@ constexpr int kMaxDevices = 16;
 constexpr int kRows = 4;          // rows per stage: one LDS.128 gathers the same column of 4 rows
 constexpr int kMaxSlots = 64;     // slot positions per lane held in registers
 constexpr int kPadChunks = 8;     // zero chunks after the data: one per 16-B bank group
+constexpr int kMaxN = 6400;       // 2 stages x (4*ceil(n/4)+8) x 16 B + partials <= 227 KB
 
 // GPU packing of a params object.
 //
@@ -36,7 +37,7 @@ struct Packing {
     int nq = 0;               // chunk columns per row-quarter
     int stage_chunks = 0;     // 4*nq + kPadChunks
     std::vector<int> block_h0, block_kb;       // hash range per block
-    std::vector<uint32_t> offp;  // [HB][W][MS/2][32]: two u16 byte offsets (slot t low, t+1 high)
+    std::vector<uint32_t> offp;  // [HB][W][MS][32]: smem byte offset of slot t (16 * chunk position)
     std::vector<float> coef;     // [HB][W][MS][32]
     std::vector<uint16_t> unit_lane;  // [HB][kb_max][parts]: lane id (warp*32+lane) of each part
     double efficiency = 0;       // useful slots / (lanes * MS) over all warps

@@ -278,11 +278,11 @@ void try_parts(const fastlsh_params& p, int P, Trial& out) {
     // fold colours beyond kMaxSlots into existing positions (creates bank conflicts)
     int64_t conflicts = 0;
     if (MS > kMaxSlots) MS = kMaxSlots;
-    MS = (MS + 1) & ~1;
+    MS = (MS + 1) & ~1;  // the gather loop issues slots in pairs
     pk.slots = MS;
 
     const size_t lanes_total = (size_t)HB * Wn * 32;
-    pk.offp.assign(lanes_total * (MS / 2), 0);
+    pk.offp.assign(lanes_total * MS, 0);
     pk.coef.assign(lanes_total * MS, 0.0f);
     pk.unit_lane.assign((size_t)HB * pk.kb_max * P, 0);
     int64_t useful = 0;
@@ -334,8 +334,7 @@ void try_parts(const fastlsh_params& p, int P, Trial& out) {
                 const size_t wl = ((size_t)bl * Wn + w);
                 for (int t = 0; t < MS; ++t) {
                     const uint32_t off = (uint32_t)tpos[(size_t)t * 8 + l] * 16u;
-                    uint32_t& word = pk.offp[(wl * (MS / 2) + t / 2) * 32 + lane];
-                    word |= (t & 1) ? (off << 16) : off;
+                    pk.offp[(wl * MS + t) * 32 + lane] = off;
                     pk.coef[(wl * MS + t) * 32 + lane] = tcoef[(size_t)t * 8 + l];
                 }
                 if (l < (int)qp.members.size()) {

@@ -97,9 +97,7 @@ def _unpack(p):
     pk = p.packing()
     idx, a, b, _ = p.export()
     nq, MS, W, HB, P = pk["nq"], pk["slots"], pk["warps"], pk["hash_blocks"], pk["parts"]
-    offs = np.empty((HB, W, MS, 32), np.int64)
-    offs[:, :, 0::2, :] = pk["offp"] & 0xFFFF
-    offs[:, :, 1::2, :] = pk["offp"] >> 16
+    offs = pk["offp"].astype(np.int64)
     assert (offs % 16 == 0).all()
     pos = offs // 16
     assert (pos < 4 * nq + 8).all()

@@ -1,0 +1,53 @@
+"""Short driver for ncu captures of the hot-path kernels (one config, a few launches)."""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2309_15479_b200 as fl  # noqa: E402
+from fastlsh_inputs import configs, data  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--rows", type=int, default=262144)
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--keys", action="store_true")
+    ap.add_argument("--time", action="store_true")
+    args = ap.parse_args()
+    c = configs.get(args.config)
+    m = args.m or c.m
+    P = fl.Params.create(c.n, m, c.k, c.w, seed=c.seed)
+    K = fl.Keys.create(c.L, c.K, seed=c.seed) if (args.keys and c.L) else None
+    X = data.generate(c.data, c.n, 0, args.rows, seed=c.seed, device="cuda")
+    codes = torch.empty((args.rows, c.k), dtype=torch.int32, device="cuda")
+    keys = torch.empty((c.L, args.rows), dtype=torch.int64, device="cuda") if K else None
+    for _ in range(args.iters):
+        fl.fastlsh_hash(P, X, out=codes)
+        if K:
+            fl.build_keys(K, codes, out=keys)
+    torch.cuda.synchronize()
+    if args.time:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fl.fastlsh_hash(P, X, out=codes)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        gathers = args.rows * c.k * m
+        peak = 148 * 32 * 1.965e9
+        print(f"{args.config} m={m} rows={args.rows}: {ms:.3f} ms/launch, {gathers / ms / 1e6:.1f} Ggather/s, "
+              f"{gathers / (ms / 1e3) / peak:.3f} of smem roofline; info={P.info()}")
+
+
+if __name__ == "__main__":
+    main()
