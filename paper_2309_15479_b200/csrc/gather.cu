@@ -4,8 +4,8 @@
 //
 // Design:
 //  * One CTA owns a block of hashes; its lanes hold their hash part's slots in registers for the
-//    whole kernel: MS 32-bit smem byte offsets and MS f32 coefficients, in
-//    the bank-scheduled order produced by packer.cpp.
+//    whole kernel: MS 32-bit smem byte offsets and MS f32 coefficients, in the bank-scheduled
+//    order produced by packer.cpp.
 //  * Rows are processed 4 at a time. A stage holds 4 rows column-interleaved: the 16-byte chunk
 //    at position pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per slot
 //    therefore gathers the sampled coordinate of 4 rows, and one FFMA per row accumulates it.
@@ -13,10 +13,11 @@
 //    slot position, so each LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
 //  * Stages are double buffered: while a CTA gathers from stage j it has already issued the
 //    coalesced 128-bit global loads of group j+1 (held in registers), stored transposed into the
-//    other stage after the gather loop.
-//  * Epilogue (fused): lanes deposit their 4 partial projections; after one CTA barrier the
-//    threads sum the parts of each hash in fixed order, add b (__fadd_rn), divide by w
-//    (__fdiv_rn), floor toward -inf, and write int32 codes with coalesced stores.
+//    other stage after the gather loop. A thread's staging items are the same in every stage, so
+//    their source/destination offsets are computed once.
+//  * Epilogue (fused): lanes deposit their 4 partial projections; after one CTA barrier each
+//    thread takes a hash, sums its parts in fixed order for the 4 rows, adds b (__fadd_rn),
+//    divides by w (__fdiv_rn), floors toward -inf and writes int32 codes (coalesced over hashes).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -60,56 +61,40 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// Load up to kBatch float4 items of group g starting at item `first` into registers.
-__device__ __forceinline__ void stage_load(const GatherArgs& a, long long g, int first, float4 (&buf)[kBatch]) {
-    const int items = 4 * a.nq;
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-        const int it = first + i * blockDim.x;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (it < items) {
-            const int r = it & 3, q = it >> 2;
-            const long long row = g * 4 + r;
-            if (row < a.N) {
-                if (a.vec4) {
-                    v = __ldg(reinterpret_cast<const float4*>(a.X + row * a.n) + q);
-                } else {
-                    const float* src = a.X + row * a.n;
-                    const int c = 4 * q;
-                    v.x = (c + 0 < a.n) ? __ldg(src + c + 0) : 0.f;
-                    v.y = (c + 1 < a.n) ? __ldg(src + c + 1) : 0.f;
-                    v.z = (c + 2 < a.n) ? __ldg(src + c + 2) : 0.f;
-                    v.w = (c + 3 < a.n) ? __ldg(src + c + 3) : 0.f;
-                }
-            }
-        }
-        buf[i] = v;
-    }
-}
-
-// Store the batch transposed: column 4q+i of row r goes to chunk i*nq+q, lane r.
-__device__ __forceinline__ void stage_store(const GatherArgs& a, float* stage, int first, const float4 (&buf)[kBatch]) {
-    const int items = 4 * a.nq;
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-        const int it = first + i * blockDim.x;
-        if (it < items) {
-            const int r = it & 3, q = it >> 2;
-            stage[(0 * a.nq + q) * 4 + r] = buf[i].x;
-            stage[(1 * a.nq + q) * 4 + r] = buf[i].y;
-            stage[(2 * a.nq + q) * 4 + r] = buf[i].z;
-            stage[(3 * a.nq + q) * 4 + r] = buf[i].w;
+// Load float4 item `it` (row r = it % 4, quad q = it / 4) of the group starting at row `row0`.
+__device__ __forceinline__ float4 load_item(const GatherArgs& a, long long row0, int it) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int r = it & 3, q = it >> 2;
+    const long long row = row0 + r;
+    if (row < a.N) {
+        const float* src = a.X + row * a.n;
+        if (a.vec4) {
+            v = __ldg(reinterpret_cast<const float4*>(src) + q);
+        } else {
+            const int c = 4 * q;
+            v.x = (c + 0 < a.n) ? __ldg(src + c + 0) : 0.f;
+            v.y = (c + 1 < a.n) ? __ldg(src + c + 1) : 0.f;
+            v.z = (c + 2 < a.n) ? __ldg(src + c + 2) : 0.f;
+            v.w = (c + 3 < a.n) ? __ldg(src + c + 3) : 0.f;
         }
     }
+    return v;
 }
 
-__device__ __forceinline__ void stage_fill(const GatherArgs& a, long long g, float* stage, int from_item) {
+// Column 4q+i of row r goes to chunk i*nq+q, component r.
+__device__ __forceinline__ void store_item(float* stage, int nq, int it, const float4 v) {
+    const int r = it & 3, q = it >> 2;
+    float* d = stage + q * 4 + r;
+    d[0 * 4 * nq] = v.x;
+    d[1 * 4 * nq] = v.y;
+    d[2 * 4 * nq] = v.z;
+    d[3 * 4 * nq] = v.w;
+}
+
+// Items beyond the register batch (large n): synchronous load + store.
+__device__ __forceinline__ void stage_rest(const GatherArgs& a, long long row0, float* stage, int from) {
     const int items = 4 * a.nq;
-    for (int first = from_item; first < items; first += kBatch * blockDim.x) {
-        float4 buf[kBatch];
-        stage_load(a, g, first, buf);
-        stage_store(a, stage, first, buf);
-    }
+    for (int it = from; it < items; it += blockDim.x) store_item(stage, a.nq, it, load_item(a, row0, it));
 }
 
 template <int MS>
@@ -126,16 +111,18 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     const long long rs = blockIdx.x / a.HB;
     const int kb = a.block_kb[hb];
     const int h0 = a.block_h0[hb];
-    float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * a.P + 1) & ~1));
+    const int P = a.P;
+    float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * P + 1) & ~1));
+    const int items = 4 * a.nq;
 
     // zero chunks (padding slots read these), hash metadata
     for (int i = tid; i < 2 * kPadChunks; i += nthreads)
         stage[i / kPadChunks][4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = tid; i < kb * a.P; i += nthreads)
-        s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * a.P + i];
+    for (int i = tid; i < kb * P; i += nthreads)
+        s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
 
-    // this lane's slots: offsets (two u16 per register) and coefficients
+    // this lane's slots: byte offsets into a stage and coefficients
     uint32_t op[MS];
     float cf[MS];
     {
@@ -149,7 +136,7 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     }
 
     long long g = rs;
-    if (g < a.groups) stage_fill(a, g, reinterpret_cast<float*>(stage[0]), tid);
+    if (g < a.groups) stage_rest(a, g * 4, reinterpret_cast<float*>(stage[0]), tid);
     __syncthreads();
 
     const float w = a.w;
@@ -158,7 +145,13 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         const long long gn = g + gpr;
         const bool has_next = gn < a.groups;
         float4 buf[kBatch];
-        if (has_next) stage_load(a, gn, tid, buf);
+        if (has_next) {
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) {
+                const int it = tid + i * nthreads;
+                buf[i] = (it < items) ? load_item(a, gn * 4, it) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
 
         // gather-FMA over the scheduled slots: 4 rows per LDS.128
         const uint32_t base = smem_u32(stage[j & 1]);
@@ -180,38 +173,45 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 
         if (has_next) {
             float* nst = reinterpret_cast<float*>(stage[(j + 1) & 1]);
-            stage_store(a, nst, tid, buf);
-            if (4 * a.nq > kBatch * nthreads) stage_fill(a, gn, nst, tid + kBatch * nthreads);
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) {
+                const int it = tid + i * nthreads;
+                if (it < items) store_item(nst, a.nq, it, buf[i]);
+            }
+            if (items > kBatch * nthreads) stage_rest(a, gn * 4, nst, tid + kBatch * nthreads);
         }
         __syncthreads();
 
-        // epilogue: sum parts in fixed order, +b, /w, floor, coalesced int32 stores
-        const float* pf = reinterpret_cast<const float*>(part + (j & 1) * a.W * 32);
-        for (int it = tid; it < 4 * kb; it += nthreads) {
-            const int r = it / kb, h = it - r * kb;
-            const long long row = g * 4 + r;
-            if (row >= a.N) continue;
-            float p = 0.f;
-            for (int q = 0; q < a.P; ++q) p += pf[(int)s_unit[h * a.P + q] * 4 + r];
-            const long long o = row * a.k + h0 + h;
+        // epilogue: one hash per thread, its parts summed in fixed order for the 4 rows
+        const float4* pb = part + (j & 1) * a.W * 32;
+        const long long row0 = g * 4;
+        const int nrows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
+        for (int h = tid; h < kb; h += nthreads) {
+            float4 s = pb[s_unit[h * P]];
+            for (int q = 1; q < P; ++q) {
+                const float4 v = pb[s_unit[h * P + q]];
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+            const float pr[4] = {s.x, s.y, s.z, s.w};
+            const long long o0 = row0 * a.k + h0 + h;
             if (a.proj) {
-                a.proj[o] = p;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (r < nrows) a.proj[o0 + (long long)r * a.k] = pr[r];
             } else {
-                const float qv = __fdiv_rn(__fadd_rn(p, s_b[h]), w);
-                int code;
-                if (!isfinite(qv)) {
-                    code = INT_MIN;
-                    atomicAdd(a.flags + 0, 1ull);
-                } else {
+                const float bh = s_b[h];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (r >= nrows) break;
+                    const float qv = __fdiv_rn(__fadd_rn(pr[r], bh), w);
                     const float f = floorf(qv);
-                    if (f <= -2147483648.0f || f >= 2147483648.0f) {
+                    int code = (int)f;
+                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
                         code = INT_MIN;
-                        atomicAdd(a.flags + 1, 1ull);
-                    } else {
-                        code = (int)f;
+                        atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
                     }
+                    a.codes[o0 + (long long)r * a.k] = code;
                 }
-                a.codes[o] = code;
             }
         }
     }
@@ -271,7 +271,8 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     const int threads = pk.warps * 32;
     const size_t smem = (size_t)2 * pk.stage_chunks * 16 + (size_t)2 * pk.warps * 32 * 16 +
                         (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -279,6 +280,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, smem);
     if (e != cudaSuccess) return set_cuda_error(e);
     if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+    // persistent grid: as many row streams per hash block as fit resident at once
     const long long resident = (long long)sms * per_sm;
     long long gpr = resident / pk.hash_blocks;
     if (gpr > a.groups) gpr = a.groups;

@@ -199,14 +199,13 @@ struct Trial {
     double cost = 1e300;
 };
 
-void try_parts(const fastlsh_params& p, int P, Trial& out) {
+void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
     const int n = p.n, m = p.m, k = p.k;
     Packing pk;
     pk.parts = P;
     pk.nq = (n + 3) / 4;
     pk.stage_chunks = 4 * pk.nq + kPadChunks;
     const int dmax = (m + P - 1) / P;
-    const int lanes_cap = 256;                  // 8 warps per CTA
     const int kb_cap = std::max(1, lanes_cap / P);
     const int HB = (k + kb_cap - 1) / kb_cap;
     pk.hash_blocks = HB;
@@ -356,12 +355,22 @@ void try_parts(const fastlsh_params& p, int P, Trial& out) {
 
 void build_packing(const fastlsh_params& p, Packing& out) {
     const int pmin = (p.m + kMaxSlots - 1) / kMaxSlots;
+    int plo = pmin, phi = std::min(p.m, pmin + 2);
+    int warps_cap = 8;
+    if (const char* e = std::getenv("FASTLSH_PARTS")) {  // experiment knob: force the split
+        int v = std::atoi(e);
+        if (v >= pmin && v <= p.m) plo = phi = v;
+    }
+    if (const char* e = std::getenv("FASTLSH_WARPS")) {  // experiment knob: warps per CTA
+        int v = std::atoi(e);
+        if (v >= 1 && v <= 8) warps_cap = v;
+    }
     Trial best;
-    for (int P = pmin; P <= std::min(p.m, pmin + 2); ++P) {
+    for (int P = plo; P <= phi; ++P) {
         // beyond 256 lanes per hash the block holds a single hash; keep P <= 256
         if (P > 256) break;
         Trial t;
-        try_parts(p, P, t);
+        try_parts(p, P, warps_cap * 32, t);
         if (t.cost < best.cost) best = std::move(t);
     }
     out = std::move(best.pk);
