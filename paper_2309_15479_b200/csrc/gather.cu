@@ -11,10 +11,9 @@
 //    therefore gathers the sampled coordinate of 4 rows, and one FFMA per row accumulates it.
 //    The packer guarantees the 8 lanes of each quarter-warp hit 8 distinct bank groups at every
 //    slot position, so each LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
-//  * Stages are double buffered: while a CTA gathers from stage j it has already issued the
-//    coalesced 128-bit global loads of group j+1 (held in registers), stored transposed into the
-//    other stage after the gather loop. A thread's staging items are the same in every stage, so
-//    their source/destination offsets are computed once.
+//  * Stages are double buffered: before gathering from stage j the CTA issues 4-byte cp.async
+//    copies of group j+1 straight into their transposed positions of the other stage (no
+//    registers held across the gather loop); they are waited for just before the stage barrier.
 //  * Epilogue (fused): lanes deposit their 4 partial projections; after one CTA barrier each
 //    thread takes a hash, sums its parts in fixed order for the 4 rows, adds b (__fadd_rn),
 //    divides by w (__fdiv_rn), floors toward -inf and writes int32 codes (coalesced over hashes).
@@ -97,11 +96,37 @@ __device__ __forceinline__ void stage_rest(const GatherArgs& a, long long row0, 
     for (int it = from; it < items; it += blockDim.x) store_item(stage, a.nq, it, load_item(a, row0, it));
 }
 
+// Asynchronous transposing stage fill: every float of the 4 rows is copied global -> shared by
+// a 4-byte cp.async straight into its interleaved position (no registers held across the gather
+// loop; rows past N and columns past n are zero-filled by the src-size operand).
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void stage_async(const GatherArgs& a, long long row0, uint32_t stage_u32) {
+    const int items = 4 * a.nq;
+    const int nq4 = 16 * a.nq;  // bytes between the 4 column components of an item
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int r = it & 3, q = it >> 2;
+        const long long row = row0 + r;
+        const bool live = row < a.N;
+        const float* src = a.X + (live ? row : 0) * (long long)a.n + 4 * q;
+        const uint32_t dst = stage_u32 + (uint32_t)(q * 16 + r * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const bool ok = live && (4 * q + i < a.n);
+            cp_async4(dst + i * nq4, ok ? src + i : a.X, ok ? 4u : 0u);
+        }
+    }
+    cp_async_commit();
+}
+
 template <int MS>
 __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) float4 smem[];
     const int SC = a.stage_chunks;
-    float4* stage[2] = {smem, smem + SC};
     float4* part = smem + 2 * SC;  // [2][W*32]
     uint16_t* s_unit = reinterpret_cast<uint16_t*>(part + 2 * a.W * 32);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -117,7 +142,7 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 
     // zero chunks (padding slots read these), hash metadata
     for (int i = tid; i < 2 * kPadChunks; i += nthreads)
-        stage[i / kPadChunks][4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
+        smem[(i / kPadChunks) * SC + 4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = tid; i < kb * P; i += nthreads)
         s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
@@ -135,26 +160,25 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
     }
 
+    const uint32_t stage0_u32 = smem_u32(smem);
+    const uint32_t stage_bytes = (uint32_t)SC * 16u;
     long long g = rs;
-    if (g < a.groups) stage_rest(a, g * 4, reinterpret_cast<float*>(stage[0]), tid);
+    if (g < a.groups) stage_async(a, g * 4, stage0_u32);
+    cp_async_wait_all();
     __syncthreads();
 
     const float w = a.w;
+    const float inv_w = 1.0f / w;
+    const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
     int j = 0;
     for (; g < a.groups; g += gpr, ++j) {
         const long long gn = g + gpr;
         const bool has_next = gn < a.groups;
-        float4 buf[kBatch];
-        if (has_next) {
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) {
-                const int it = tid + i * nthreads;
-                buf[i] = (it < items) ? load_item(a, gn * 4, it) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
+        // next group's rows stream into the other stage while this one is gathered
+        if (has_next) stage_async(a, gn * 4, stage0_u32 + ((j + 1) & 1) * stage_bytes);
 
         // gather-FMA over the scheduled slots: 4 rows per LDS.128
-        const uint32_t base = smem_u32(stage[j & 1]);
+        const uint32_t base = stage0_u32 + (j & 1) * stage_bytes;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
 #pragma unroll
         for (int t = 0; t < MS; t += 2) {
@@ -170,16 +194,7 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
             acc3 = fmaf(v1.w, cf[t + 1], acc3);
         }
         part[(j & 1) * a.W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
-
-        if (has_next) {
-            float* nst = reinterpret_cast<float*>(stage[(j + 1) & 1]);
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) {
-                const int it = tid + i * nthreads;
-                if (it < items) store_item(nst, a.nq, it, buf[i]);
-            }
-            if (items > kBatch * nthreads) stage_rest(a, gn * 4, nst, tid + kBatch * nthreads);
-        }
+        cp_async_wait_all();
         __syncthreads();
 
         // epilogue: one hash per thread, its parts summed in fixed order for the 4 rows
@@ -203,7 +218,9 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if (r >= nrows) break;
-                    const float qv = __fdiv_rn(__fadd_rn(pr[r], bh), w);
+                    // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
+                    const float num = __fadd_rn(pr[r], bh);
+                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
                     const float f = floorf(qv);
                     int code = (int)f;
                     if (!(f > -2147483648.0f && f < 2147483648.0f)) {
