@@ -64,7 +64,7 @@ typedef struct {
  *   idx[i][j] = hi64(u64(philox(j,i,1)) * n),  a[i][j] = BoxMuller(philox(j,i,2)) as f32,
  *   b[i] = f32(w * u53(philox(0,i,3))) clamped to [0, w).
  * n, m, k >= 1; w finite and > 0; m > n is legal (sampling with replacement).
- * EINVAL otherwise. EUNSUPPORTED if n > 6400 (two 4-row stages of X must fit in 227 KB of
+ * EINVAL otherwise. EUNSUPPORTED if n > 4400 (three 4-row stages of X must fit in 227 KB of
  * shared memory) or m > 16384. */
 fastlsh_status fastlsh_params_create(int32_t n, int32_t m, int32_t k, float w, uint64_t seed,
                                      fastlsh_params** out);

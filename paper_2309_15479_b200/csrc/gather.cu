@@ -6,17 +6,22 @@
 //  * One CTA owns a block of hashes; its lanes hold their hash part's slots in registers for the
 //    whole kernel: MS 32-bit smem byte offsets and MS f32 coefficients, in the bank-scheduled
 //    order produced by packer.cpp.
-//  * Rows are processed 4 at a time. A stage holds 4 rows column-interleaved: the 16-byte chunk
-//    at position pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per slot
-//    therefore gathers the sampled coordinate of 4 rows, and one FFMA per row accumulates it.
+//  * Rows are processed 4 at a time ("groups"). A stage holds 4 rows column-interleaved: the
+//    16-byte chunk at position pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One
+//    LDS.128 per slot gathers the sampled coordinate of 4 rows; one FFMA per row accumulates it.
 //    The packer guarantees the 8 lanes of each quarter-warp hit 8 distinct bank groups at every
 //    slot position, so each LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
-//  * Stages are double buffered: before gathering from stage j the CTA issues 4-byte cp.async
-//    copies of group j+1 straight into their transposed positions of the other stage (no
-//    registers held across the gather loop); they are waited for just before the stage barrier.
-//  * Epilogue (fused): lanes deposit their 4 partial projections; after one CTA barrier each
-//    thread takes a hash, sums its parts in fixed order for the 4 rows, adds b (__fadd_rn),
-//    divides by w (__fdiv_rn), floors toward -inf and writes int32 codes (coalesced over hashes).
+//  * Pipeline without CTA barriers in steady state (mbarriers only, one iteration of slack):
+//      - a 3-stage ring of X groups, filled by 4-byte cp.async copies straight into their
+//        transposed positions (no registers held); each thread's copies arrive on full[s]
+//        (cp.async.mbarrier.arrive.noinc); readers arrive on empty[s] when done;
+//      - a 2-slot ring of per-lane partial projections: written after the gather loop
+//        (pfull[d]), consumed one iteration later by the epilogue (pempty[d]).
+//    At iteration j a thread fills group j+2, gathers group j, and finishes group j-1, so the
+//    epilogue and staging of some warps overlap the gathers of others.
+//  * Epilogue (fused): each thread takes a hash, sums its parts in fixed order for the 4 rows,
+//    adds b (__fadd_rn), divides by w (__fdiv_rn; an exact multiply when w is a power of two),
+//    floors toward -inf and writes int32 codes (coalesced over hashes).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -27,7 +32,8 @@
 namespace fastlsh {
 namespace {
 
-constexpr int kBatch = 4;  // float4 staging loads held in registers per thread
+constexpr int kStages = 3;
+constexpr int kPartSlots = 2;
 
 struct GatherArgs {
     const float* X;
@@ -45,7 +51,6 @@ struct GatherArgs {
     int32_t* codes;
     float* proj;
     unsigned long long* flags;
-    int vec4;
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -60,54 +65,39 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// Load float4 item `it` (row r = it % 4, quad q = it / 4) of the group starting at row `row0`.
-__device__ __forceinline__ float4 load_item(const GatherArgs& a, long long row0, int it) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int r = it & 3, q = it >> 2;
-    const long long row = row0 + r;
-    if (row < a.N) {
-        const float* src = a.X + row * a.n;
-        if (a.vec4) {
-            v = __ldg(reinterpret_cast<const float4*>(src) + q);
-        } else {
-            const int c = 4 * q;
-            v.x = (c + 0 < a.n) ? __ldg(src + c + 0) : 0.f;
-            v.y = (c + 1 < a.n) ? __ldg(src + c + 1) : 0.f;
-            v.z = (c + 2 < a.n) ? __ldg(src + c + 2) : 0.f;
-            v.w = (c + 3 < a.n) ? __ldg(src + c + 3) : 0.f;
-        }
-    }
-    return v;
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-// Column 4q+i of row r goes to chunk i*nq+q, component r.
-__device__ __forceinline__ void store_item(float* stage, int nq, int it, const float4 v) {
-    const int r = it & 3, q = it >> 2;
-    float* d = stage + q * 4 + r;
-    d[0 * 4 * nq] = v.x;
-    d[1 * 4 * nq] = v.y;
-    d[2 * 4 * nq] = v.z;
-    d[3 * 4 * nq] = v.w;
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Items beyond the register batch (large n): synchronous load + store.
-__device__ __forceinline__ void stage_rest(const GatherArgs& a, long long row0, float* stage, int from) {
-    const int items = 4 * a.nq;
-    for (int it = from; it < items; it += blockDim.x) store_item(stage, a.nq, it, load_item(a, row0, it));
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 
-// Asynchronous transposing stage fill: every float of the 4 rows is copied global -> shared by
-// a 4-byte cp.async straight into its interleaved position (no registers held across the gather
-// loop; rows past N and columns past n are zero-filled by the src-size operand).
 __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, uint32_t src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ void stage_async(const GatherArgs& a, long long row0, uint32_t stage_u32) {
+// All of this thread's prior cp.async copies arrive on `bar` when they land.
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// Transposing fill of one stage: every float of the 4 rows of a group is copied global -> shared
+// by a 4-byte cp.async into chunk i*nq+q, component r (rows past N and columns past n read as 0).
+// Lanes cover (row r = it%4, quad q = it/4): each warp instruction writes 128 contiguous bytes.
+__device__ __forceinline__ void stage_fill(const GatherArgs& a, long long row0, uint32_t stage_u32) {
     const int items = 4 * a.nq;
-    const int nq4 = 16 * a.nq;  // bytes between the 4 column components of an item
+    const uint32_t comp_stride = 16u * (uint32_t)a.nq;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
         const int r = it & 3, q = it >> 2;
         const long long row = row0 + r;
@@ -117,18 +107,18 @@ __device__ __forceinline__ void stage_async(const GatherArgs& a, long long row0,
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const bool ok = live && (4 * q + i < a.n);
-            cp_async4(dst + i * nq4, ok ? src + i : a.X, ok ? 4u : 0u);
+            cp_async4(dst + i * comp_stride, ok ? src + i : a.X, ok ? 4u : 0u);
         }
     }
-    cp_async_commit();
 }
 
 template <int MS>
 __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) float4 smem[];
     const int SC = a.stage_chunks;
-    float4* part = smem + 2 * SC;  // [2][W*32]
-    uint16_t* s_unit = reinterpret_cast<uint16_t*>(part + 2 * a.W * 32);
+    float4* part = smem + kStages * SC;  // [kPartSlots][W*32]
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(part + kPartSlots * a.W * 32);
+    uint16_t* s_unit = reinterpret_cast<uint16_t*>(bars + 2 * kStages + 2 * kPartSlots);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x;
     const int hb = blockIdx.x % a.HB;
@@ -138,10 +128,21 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     const int h0 = a.block_h0[hb];
     const int P = a.P;
     float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * P + 1) & ~1));
-    const int items = 4 * a.nq;
 
+    const uint32_t stage0 = smem_u32(smem);
+    const uint32_t stage_bytes = (uint32_t)SC * 16u;
+    const uint32_t bar0 = smem_u32(bars);
+    auto FULL = [&](int s) { return bar0 + 8u * s; };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
+    auto PFULL = [&](int d) { return bar0 + 8u * (2 * kStages + d); };
+    auto PEMPTY = [&](int d) { return bar0 + 8u * (2 * kStages + kPartSlots + d); };
+
+    if (tid == 0) {
+        for (int i = 0; i < 2 * kStages + 2 * kPartSlots; ++i) mbar_init(bar0 + 8u * i, nthreads);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     // zero chunks (padding slots read these), hash metadata
-    for (int i = tid; i < 2 * kPadChunks; i += nthreads)
+    for (int i = tid; i < kStages * kPadChunks; i += nthreads)
         smem[(i / kPadChunks) * SC + 4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = tid; i < kb * P; i += nthreads)
         s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
@@ -159,47 +160,25 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 #pragma unroll
         for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
     }
-
-    const uint32_t stage0_u32 = smem_u32(smem);
-    const uint32_t stage_bytes = (uint32_t)SC * 16u;
-    long long g = rs;
-    if (g < a.groups) stage_async(a, g * 4, stage0_u32);
-    cp_async_wait_all();
     __syncthreads();
+
+    const long long iters = rs < a.groups ? (a.groups - rs + gpr - 1) / gpr : 0;
+    // prologue: groups 0 and 1 of this CTA's row stream
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < iters) stage_fill(a, (rs + s * gpr) * 4, stage0 + s * stage_bytes);
+        cp_async_arrive(FULL(s));
+    }
 
     const float w = a.w;
     const float inv_w = 1.0f / w;
     const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
-    int j = 0;
-    for (; g < a.groups; g += gpr, ++j) {
-        const long long gn = g + gpr;
-        const bool has_next = gn < a.groups;
-        // next group's rows stream into the other stage while this one is gathered
-        if (has_next) stage_async(a, gn * 4, stage0_u32 + ((j + 1) & 1) * stage_bytes);
 
-        // gather-FMA over the scheduled slots: 4 rows per LDS.128
-        const uint32_t base = stage0_u32 + (j & 1) * stage_bytes;
-        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-#pragma unroll
-        for (int t = 0; t < MS; t += 2) {
-            const float4 v0 = lds128(base + op[t]);
-            const float4 v1 = lds128(base + op[t + 1]);
-            acc0 = fmaf(v0.x, cf[t], acc0);
-            acc1 = fmaf(v0.y, cf[t], acc1);
-            acc2 = fmaf(v0.z, cf[t], acc2);
-            acc3 = fmaf(v0.w, cf[t], acc3);
-            acc0 = fmaf(v1.x, cf[t + 1], acc0);
-            acc1 = fmaf(v1.y, cf[t + 1], acc1);
-            acc2 = fmaf(v1.z, cf[t + 1], acc2);
-            acc3 = fmaf(v1.w, cf[t + 1], acc3);
-        }
-        part[(j & 1) * a.W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
-        cp_async_wait_all();
-        __syncthreads();
-
-        // epilogue: one hash per thread, its parts summed in fixed order for the 4 rows
-        const float4* pb = part + (j & 1) * a.W * 32;
-        const long long row0 = g * 4;
+    // epilogue of iteration je: sum parts, quantise, store (one hash per thread, 4 rows)
+    auto epilogue = [&](long long je) {
+        const int d = (int)(je % kPartSlots);
+        mbar_wait(PFULL(d), (uint32_t)((je / kPartSlots) & 1));
+        const float4* pb = part + d * a.W * 32;
+        const long long row0 = (rs + je * gpr) * 4;
         const int nrows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
         for (int h = tid; h < kb; h += nthreads) {
             float4 s = pb[s_unit[h * P]];
@@ -231,7 +210,48 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
                 }
             }
         }
+        mbar_arrive(PEMPTY(d));
+    };
+
+    for (long long j = 0; j < iters; ++j) {
+        const int s = (int)(j % kStages);
+        // 1. refill the stage freed by iteration j-1 with group j+2
+        {
+            const long long jf = j + kStages - 1;
+            const int sf = (int)(jf % kStages);
+            if (j >= 1) mbar_wait(EMPTY(sf), (uint32_t)(((j - 1) / kStages) & 1));
+            if (jf < iters) stage_fill(a, (rs + jf * gpr) * 4, stage0 + sf * stage_bytes);
+            cp_async_arrive(FULL(sf));
+        }
+        // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128
+        mbar_wait(FULL(s), (uint32_t)((j / kStages) & 1));
+        const uint32_t base = stage0 + s * stage_bytes;
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+        for (int t = 0; t < MS; t += 2) {
+            const float4 v0 = lds128(base + op[t]);
+            const float4 v1 = lds128(base + op[t + 1]);
+            acc0 = fmaf(v0.x, cf[t], acc0);
+            acc1 = fmaf(v0.y, cf[t], acc1);
+            acc2 = fmaf(v0.z, cf[t], acc2);
+            acc3 = fmaf(v0.w, cf[t], acc3);
+            acc0 = fmaf(v1.x, cf[t + 1], acc0);
+            acc1 = fmaf(v1.y, cf[t + 1], acc1);
+            acc2 = fmaf(v1.z, cf[t + 1], acc2);
+            acc3 = fmaf(v1.w, cf[t + 1], acc3);
+        }
+        mbar_arrive(EMPTY(s));
+        // 3. publish this lane's partials for group j
+        const int d = (int)(j % kPartSlots);
+        if (j >= kPartSlots) mbar_wait(PEMPTY(d), (uint32_t)(((j - kPartSlots) / kPartSlots) & 1));
+        part[d * a.W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
+        mbar_arrive(PFULL(d));
+        // 4. finish group j-1 while other warps still gather group j
+        if (j >= 1) epilogue(j - 1);
     }
+    if (iters >= 1) epilogue(iters - 1);
+    // drain: every cp.async issued (including the empty arrivals past the end) has landed
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 typedef void (*KernelFn)(GatherArgs);
@@ -255,6 +275,12 @@ KernelFn select_kernel(int MS) {
 }
 
 }  // namespace
+
+size_t gather_smem_bytes(const Packing& pk) {
+    return (size_t)kStages * pk.stage_chunks * 16 + (size_t)kPartSlots * pk.warps * 32 * 16 +
+           (size_t)(2 * kStages + 2 * kPartSlots) * 8 + (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) +
+           (size_t)pk.kb_max * 4;
+}
 
 fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                              int64_t N, int32_t* codes, float* proj, cudaStream_t stream) {
@@ -283,11 +309,9 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.codes = codes;
     a.proj = proj;
     a.flags = d.flags;
-    a.vec4 = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
 
     const int threads = pk.warps * 32;
-    const size_t smem = (size_t)2 * pk.stage_chunks * 16 + (size_t)2 * pk.warps * 32 * 16 +
-                        (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
+    const size_t smem = gather_smem_bytes(pk);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);

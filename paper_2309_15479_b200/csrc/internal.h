@@ -15,7 +15,7 @@ constexpr int kMaxDevices = 16;
 constexpr int kRows = 4;          // rows per stage: one LDS.128 gathers the same column of 4 rows
 constexpr int kMaxSlots = 64;     // slot positions per lane held in registers
 constexpr int kPadChunks = 8;     // zero chunks after the data: one per 16-B bank group
-constexpr int kMaxN = 6400;       // 2 stages x (4*ceil(n/4)+8) x 16 B + partials <= 227 KB
+constexpr int kMaxN = 4400;       // 3 stages x (4*ceil(n/4)+8) x 16 B + partials <= 227 KB
 
 // GPU packing of a params object.
 //
