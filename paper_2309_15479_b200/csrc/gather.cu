@@ -2,22 +2,25 @@
 //
 // For every row v and hash i: h_i(v) = floor((a_i . S_i(v) + b_i) / w)   (Eq. 5).
 //
-// Design: a warp-specialised persistent kernel, one CTA per hash block.
-//  * Compute warps (W): each lane holds its hash part's slots in registers for the whole kernel
-//    (MS 32-bit smem byte offsets + MS f32 coefficients, in the bank-scheduled order of
-//    packer.cpp). Rows are processed 4 at a time ("groups"): a stage holds 4 rows
-//    column-interleaved — the 16-byte chunk at pos(c) = (c%4)*nq + c/4 is (x0[c],..,x3[c]) — so
-//    one LDS.128 per slot gathers the sampled coordinate of 4 rows and one FFMA per row
-//    accumulates it. The packer guarantees the 8 lanes of each quarter-warp hit 8 distinct bank
-//    groups at every slot, so each LDS.128 costs the ideal 4 wavefronts (32 gathers/wavefront).
-//  * Producer warp: TMA bulk copies (cp.async.bulk, complete_tx on an mbarrier) bring the 4
-//    rows of a group from HBM into a row-major landing ring with 128-bit transfers; the warp then
-//    transposes landing -> stage (conflict-free LDS.128 / STS.32) and arrives on full[s].
-//  * Epilogue warp: sums each hash's parts in fixed order for the 4 rows, adds b (__fadd_rn),
-//    divides by w (__fdiv_rn; an exact multiply when w is a power of two), floors toward -inf and
-//    writes int32 codes (coalesced over hashes).
-//  * Synchronisation is mbarrier-only: full/empty for the 3-stage ring, pfull/pempty for the
-//    2-slot ring of per-lane partial projections, lfull (+tx bytes) for the 2-slot landing ring.
+// Design: a persistent kernel, one CTA per (hash block, row stream).
+//  * Each lane holds its hash part's slots in registers for the whole kernel: MS 32-bit smem
+//    byte offsets and MS f32 coefficients, in the bank-scheduled order of packer.cpp.
+//  * Rows are processed 4 at a time ("groups"). A stage holds 4 rows column-interleaved: the
+//    16-byte chunk at pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per
+//    slot gathers the sampled coordinate of 4 rows; one FFMA per row accumulates it. The packer
+//    guarantees the 8 lanes of each quarter-warp hit 8 distinct bank groups at every slot, so each
+//    LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
+//  * Staging: TMA bulk copies (cp.async.bulk ... complete_tx) bring each group's rows from HBM
+//    into a row-major 2-slot landing ring with 128-bit transfers; the CTA's warps transpose
+//    landing -> stage with conflict-free LDS.128 / STS.32. (Rows that are not 16-B aligned fall
+//    back to 4-byte cp.async straight into the transposed positions.)
+//  * Pipeline without CTA barriers (mbarriers only, one iteration of slack): at iteration j every
+//    thread transposes its share of group j+2, gathers group j, publishes its partials for j, and
+//    finishes group j-1 (epilogue); thread 0 re-arms the landing slot freed by group j+2 with the
+//    TMA copies of group j+4.
+//  * Epilogue (fused): each thread takes a hash, sums its parts in fixed order for the 4 rows,
+//    adds b (__fadd_rn), divides by w (__fdiv_rn; an exact multiply when w is a power of two),
+//    floors toward -inf and writes int32 codes (coalesced over hashes).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -31,7 +34,7 @@ namespace {
 constexpr int kStages = 3;
 constexpr int kPartSlots = 2;
 constexpr int kLanding = 2;
-constexpr int kBars = 2 * kStages + 2 * kPartSlots + kLanding;
+constexpr int kBars = 2 * kStages + 2 * kPartSlots + 2 * kLanding;
 
 struct GatherArgs {
     const float* X;
@@ -49,7 +52,7 @@ struct GatherArgs {
     int32_t* codes;
     float* proj;
     unsigned long long* flags;
-    int tma;           // 1: rows are 16-B aligned and 4n % 16 == 0 -> TMA bulk path
+    int tma;           // 1: TMA landing ring + transposition; 0: 4-byte cp.async fill
     int landing_row;   // bytes per landing row (4n rounded up to 16)
 };
 
@@ -59,10 +62,6 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "r"(addr));
     return v;
-}
-
-__device__ __forceinline__ void sts32(uint32_t addr, float v) {
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -99,7 +98,16 @@ __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint
         : "memory");
 }
 
-// Issue the TMA copies of group `g` (its rows < N) into landing slot `l`; lane 0 only.
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// All of this thread's prior cp.async copies arrive on `bar` when they land.
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// TMA copies of group g's live rows into a landing slot (one thread).
 __device__ __forceinline__ void issue_group(const GatherArgs& a, long long g, uint32_t land, uint32_t bar) {
     const long long row0 = g * 4;
     const int rows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
@@ -109,38 +117,28 @@ __device__ __forceinline__ void issue_group(const GatherArgs& a, long long g, ui
         tma_bulk_g2s(land + r * a.landing_row, a.X + (row0 + r) * (long long)a.n, bytes, bar);
 }
 
-// Producer transposition of one group, split over NP producer warps (pw = this warp's index):
-// item (r, q) = 128-bit read of row r's chunk q in the landing buffer (8 consecutive q per
-// quarter-warp: conflict-free), 4 scalar stores to chunks i*nq+q, component r (32 consecutive
-// words per warp instruction: conflict-free). Rows >= N become 0.
-__device__ __forceinline__ void transpose_group(const GatherArgs& a, long long g, const float4* land,
-                                                float* stage, int lane, int pw, int NP) {
+// This warp's share of the transposition of group g: item (r, q) = 128-bit read of row r's
+// chunk q in the landing slot (8 consecutive q per quarter-warp: conflict-free) and 4 scalar
+// stores to chunks i*nq+q, component r (32 consecutive words per warp store: conflict-free).
+// Rows >= N become 0.
+__device__ __forceinline__ void transpose_share(const GatherArgs& a, long long g, const float4* land,
+                                                float* stage, int lane, int warp, int W) {
     const long long row0 = g * 4;
     const int rows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
     const int nq = a.nq;
-    const int comp = 4 * nq;                  // floats between the 4 column components
-    const int lrow = a.landing_row / 16;      // float4 per landing row
-    const int blocks = (nq + 7) >> 3;         // 8 chunks x 4 rows = 32 items per block
+    const int comp = 4 * nq;              // floats between the 4 column components
+    const int lrow = a.landing_row / 16;  // float4 per landing row
+    const int blocks = (nq + 7) >> 3;     // 8 chunks x 4 rows = 32 items per block
     const int r = lane >> 3;
     const bool live = r < rows;
-#pragma unroll 4
-    for (int bq = pw; bq < blocks; bq += NP) {
+    const float4* src = land + r * lrow + (lane & 7);
+    float* dst = stage + 4 * (lane & 7) + r;
+#pragma unroll 2
+    for (int bq = warp; bq < blocks; bq += W) {
         const int q = bq * 8 + (lane & 7);
         if (q < nq) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (live) {
-                if (a.tma) {
-                    v = land[r * lrow + q];
-                } else {
-                    const float* src = a.X + (row0 + r) * (long long)a.n + 4 * q;
-                    const int c = 4 * q;
-                    v.x = (c + 0 < a.n) ? __ldg(src + 0) : 0.f;
-                    v.y = (c + 1 < a.n) ? __ldg(src + 1) : 0.f;
-                    v.z = (c + 2 < a.n) ? __ldg(src + 2) : 0.f;
-                    v.w = (c + 3 < a.n) ? __ldg(src + 3) : 0.f;
-                }
-            }
-            float* d = stage + 4 * q + r;
+            const float4 v = live ? src[bq * 8] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float* d = dst + 32 * bq;
             d[0] = v.x;
             d[comp] = v.y;
             d[2 * comp] = v.z;
@@ -149,23 +147,35 @@ __device__ __forceinline__ void transpose_group(const GatherArgs& a, long long g
     }
 }
 
-__device__ __forceinline__ void named_bar(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+// Fallback fill (rows not 16-B aligned): every float copied by a 4-byte cp.async straight into
+// its transposed position (rows past N and columns past n read as 0).
+__device__ __forceinline__ void stage_fill_async(const GatherArgs& a, long long row0, uint32_t stage_u32) {
+    const int items = 4 * a.nq;
+    const uint32_t comp_stride = 16u * (uint32_t)a.nq;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int r = it & 3, q = it >> 2;
+        const long long row = row0 + r;
+        const bool live = row < a.N;
+        const float* src = a.X + (live ? row : 0) * (long long)a.n + 4 * q;
+        const uint32_t dst = stage_u32 + (uint32_t)(q * 16 + r * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const bool ok = live && (4 * q + i < a.n);
+            cp_async4(dst + i * comp_stride, ok ? src + i : a.X, ok ? 4u : 0u);
+        }
+    }
 }
 
-constexpr int kProducerWarps = 2;
-constexpr int kEpilogueWarps = 2;
-
 template <int MS>
-__global__ void __launch_bounds__(384, 1) gather_kernel(const GatherArgs a) {
-    constexpr int NP = kProducerWarps, NE = kEpilogueWarps;
+__global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) float4 smem[];
     const int SC = a.stage_chunks;
     const int W = a.W;
     float4* part = smem + kStages * SC;  // [kPartSlots][W*32]
     unsigned char* land_base = reinterpret_cast<unsigned char*>(part + kPartSlots * W * 32);
+    const int land_bytes = 4 * a.landing_row;
     unsigned long long* bars =
-        reinterpret_cast<unsigned long long*>(land_base + (a.tma ? kLanding * 4 * a.landing_row : 0));
+        reinterpret_cast<unsigned long long*>(land_base + (a.tma ? kLanding * land_bytes : 0));
     uint16_t* s_unit = reinterpret_cast<uint16_t*>(bars + kBars);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x;
@@ -180,24 +190,20 @@ __global__ void __launch_bounds__(384, 1) gather_kernel(const GatherArgs a) {
     const uint32_t stage0 = smem_u32(smem);
     const uint32_t stage_bytes = (uint32_t)SC * 16u;
     const uint32_t land0 = smem_u32(land_base);
-    const uint32_t land_bytes = 4u * (uint32_t)a.landing_row;
     const uint32_t bar0 = smem_u32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
     auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
     auto PFULL = [&](int d) { return bar0 + 8u * (2 * kStages + d); };
     auto PEMPTY = [&](int d) { return bar0 + 8u * (2 * kStages + kPartSlots + d); };
     auto LFULL = [&](int l) { return bar0 + 8u * (2 * kStages + 2 * kPartSlots + l); };
+    auto LEMPTY = [&](int l) { return bar0 + 8u * (2 * kStages + 2 * kPartSlots + kLanding + l); };
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(FULL(s), NP * 32);
-            mbar_init(EMPTY(s), W * 32);
+        for (int i = 0; i < 2 * kStages + 2 * kPartSlots; ++i) mbar_init(bar0 + 8u * i, nthreads);
+        for (int l = 0; l < kLanding; ++l) {
+            mbar_init(LFULL(l), 1);
+            mbar_init(LEMPTY(l), nthreads);
         }
-        for (int d = 0; d < kPartSlots; ++d) {
-            mbar_init(PFULL(d), W * 32);
-            mbar_init(PEMPTY(d), NE * 32);
-        }
-        for (int l = 0; l < kLanding; ++l) mbar_init(LFULL(l), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // zero chunks (padding slots read these), hash metadata
@@ -206,116 +212,146 @@ __global__ void __launch_bounds__(384, 1) gather_kernel(const GatherArgs a) {
     for (int i = tid; i < kb * P; i += nthreads)
         s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
+
+    // this lane's slots: byte offsets into a stage and coefficients
+    uint32_t op[MS];
+    float cf[MS];
+    {
+        const size_t wl = (size_t)hb * W + warp;
+        const uint32_t* po = a.offp + wl * MS * 32 + lane;
+        const float* pc = a.coef + wl * MS * 32 + lane;
+#pragma unroll
+        for (int t = 0; t < MS; ++t) op[t] = __ldg(po + t * 32);
+#pragma unroll
+        for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
+    }
     __syncthreads();
 
     const long long iters = rs < a.groups ? (a.groups - rs + gpr - 1) / gpr : 0;
+    auto group_of = [&](long long j) { return rs + j * gpr; };
 
-    if (warp < W) {
-        // ---------------- compute warps: gather-FMA only ----------------
-        uint32_t op[MS];
-        float cf[MS];
-        {
-            const size_t wl = (size_t)hb * W + warp;
-            const uint32_t* po = a.offp + wl * MS * 32 + lane;
-            const float* pc = a.coef + wl * MS * 32 + lane;
-#pragma unroll
-            for (int t = 0; t < MS; ++t) op[t] = __ldg(po + t * 32);
-#pragma unroll
-            for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
-        }
-        for (long long j = 0; j < iters; ++j) {
-            const int s = (int)(j % kStages);
-            mbar_wait(FULL(s), (uint32_t)((j / kStages) & 1));
-            const uint32_t base = stage0 + s * stage_bytes;
-            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-#pragma unroll
-            for (int t = 0; t < MS; t += 2) {
-                const float4 v0 = lds128(base + op[t]);
-                const float4 v1 = lds128(base + op[t + 1]);
-                acc0 = fmaf(v0.x, cf[t], acc0);
-                acc1 = fmaf(v0.y, cf[t], acc1);
-                acc2 = fmaf(v0.z, cf[t], acc2);
-                acc3 = fmaf(v0.w, cf[t], acc3);
-                acc0 = fmaf(v1.x, cf[t + 1], acc0);
-                acc1 = fmaf(v1.y, cf[t + 1], acc1);
-                acc2 = fmaf(v1.z, cf[t + 1], acc2);
-                acc3 = fmaf(v1.w, cf[t + 1], acc3);
+    // fill stage (jf % kStages) with group jf: this thread's share, then arrive on full
+    auto fill = [&](long long jf) {
+        const int sf = (int)(jf % kStages);
+        if (a.tma) {
+            if (jf < iters) {
+                const int l = (int)(jf % kLanding);
+                mbar_wait(LFULL(l), (uint32_t)((jf / kLanding) & 1));
+                transpose_share(a, group_of(jf), reinterpret_cast<const float4*>(land_base + l * land_bytes),
+                                reinterpret_cast<float*>(smem + sf * SC), lane, warp, W);
+                mbar_arrive(LEMPTY(l));
             }
-            mbar_arrive(EMPTY(s));
-            const int d = (int)(j % kPartSlots);
-            if (j >= kPartSlots) mbar_wait(PEMPTY(d), (uint32_t)(((j - kPartSlots) / kPartSlots) & 1));
-            part[d * W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
-            mbar_arrive(PFULL(d));
+            mbar_arrive(FULL(sf));
+        } else {
+            if (jf < iters) stage_fill_async(a, group_of(jf) * 4, stage0 + sf * stage_bytes);
+            cp_async_arrive(FULL(sf));
         }
-    } else if (warp < W + NP) {
-        // ---------------- producer warps: TMA rows -> landing -> transposed stage ----------------
-        const int pw = warp - W;
-        if (a.tma && pw == 0 && lane == 0) {
-            for (int l = 0; l < kLanding && l < iters; ++l)
-                issue_group(a, rs + l * gpr, land0 + l * land_bytes, LFULL(l));
-        }
-        for (long long j = 0; j < iters; ++j) {
-            const int s = (int)(j % kStages);
-            const int l = (int)(j % kLanding);
-            if (a.tma) mbar_wait(LFULL(l), (uint32_t)((j / kLanding) & 1));
-            if (j >= kStages) mbar_wait(EMPTY(s), (uint32_t)(((j - kStages) / kStages) & 1));
-            transpose_group(a, rs + j * gpr, reinterpret_cast<const float4*>(land_base + l * land_bytes),
-                            reinterpret_cast<float*>(smem + s * SC), lane, pw, NP);
-            mbar_arrive(FULL(s));
-            if (a.tma) {
-                // all producer reads of landing slot l are ordered before the next TMA write into it
+    };
+
+    // prologue: TMA for groups 0..kLanding-1, stages for groups 0..kStages-2, re-arm landings
+    if (a.tma && tid == 0)
+        for (int l = 0; l < kLanding && l < iters; ++l) issue_group(a, group_of(l), land0 + l * land_bytes, LFULL(l));
+    for (int s = 0; s < kStages - 1; ++s) fill(s);
+    if (a.tma && tid == 0) {
+        for (int l = 0; l < kLanding && l < kStages - 1; ++l) {
+            const long long jn = l + kLanding;  // next occupant of landing slot l
+            if (jn < iters && l < iters) {
+                mbar_wait(LEMPTY(l), 0);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                named_bar(1, NP * 32);
-                if (pw == 0 && lane == 0 && j + kLanding < iters)
-                    issue_group(a, rs + (j + kLanding) * gpr, land0 + l * land_bytes, LFULL(l));
+                issue_group(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
             }
-        }
-    } else if (warp < W + NP + NE) {
-        // ---------------- epilogue warps: parts -> +b, /w, floor -> int32 codes ----------------
-        const int ew = warp - W - NP;
-        const float w = a.w;
-        const float inv_w = 1.0f / w;
-        const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
-        for (long long j = 0; j < iters; ++j) {
-            const int d = (int)(j % kPartSlots);
-            mbar_wait(PFULL(d), (uint32_t)((j / kPartSlots) & 1));
-            const float4* pb = part + d * W * 32;
-            const long long row0 = (rs + j * gpr) * 4;
-            const int nrows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
-#pragma unroll 2
-            for (int h = ew * 32 + lane; h < kb; h += NE * 32) {
-                float4 sum = pb[s_unit[h * P]];
-                for (int q = 1; q < P; ++q) {
-                    const float4 v = pb[s_unit[h * P + q]];
-                    sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
-                }
-                const float pr[4] = {sum.x, sum.y, sum.z, sum.w};
-                const long long o0 = row0 * a.k + h0 + h;
-                if (a.proj) {
-#pragma unroll
-                    for (int r = 0; r < 4; ++r)
-                        if (r < nrows) a.proj[o0 + (long long)r * a.k] = pr[r];
-                } else {
-                    const float bh = s_b[h];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        if (r >= nrows) break;
-                        // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
-                        const float num = __fadd_rn(pr[r], bh);
-                        const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
-                        const float f = floorf(qv);
-                        int code = (int)f;
-                        if (!(f > -2147483648.0f && f < 2147483648.0f)) {
-                            code = INT_MIN;
-                            atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
-                        }
-                        a.codes[o0 + (long long)r * a.k] = code;
-                    }
-                }
-            }
-            mbar_arrive(PEMPTY(d));
         }
     }
+
+    const float w = a.w;
+    const float inv_w = 1.0f / w;
+    const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
+
+    // epilogue of iteration je: sum parts, quantise, store (one hash per thread, 4 rows)
+    auto epilogue = [&](long long je) {
+        const int d = (int)(je % kPartSlots);
+        mbar_wait(PFULL(d), (uint32_t)((je / kPartSlots) & 1));
+        const float4* pb = part + d * W * 32;
+        const long long row0 = group_of(je) * 4;
+        const int nrows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
+        for (int h = tid; h < kb; h += nthreads) {
+            float4 s = pb[s_unit[h * P]];
+            for (int q = 1; q < P; ++q) {
+                const float4 v = pb[s_unit[h * P + q]];
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+            const float pr[4] = {s.x, s.y, s.z, s.w};
+            const long long o0 = row0 * a.k + h0 + h;
+            if (a.proj) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (r < nrows) a.proj[o0 + (long long)r * a.k] = pr[r];
+            } else {
+                const float bh = s_b[h];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (r >= nrows) break;
+                    // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
+                    const float num = __fadd_rn(pr[r], bh);
+                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                    const float f = floorf(qv);
+                    int code = (int)f;
+                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
+                        code = INT_MIN;
+                        atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                    }
+                    a.codes[o0 + (long long)r * a.k] = code;
+                }
+            }
+        }
+        mbar_arrive(PEMPTY(d));
+    };
+
+    for (long long j = 0; j < iters; ++j) {
+        const int s = (int)(j % kStages);
+        // 1. fill the stage freed by iteration j-1 with group j+2
+        if (j >= 1) mbar_wait(EMPTY((int)((j - 1) % kStages)), (uint32_t)(((j - 1) / kStages) & 1));
+        fill(j + kStages - 1);
+        // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128
+        mbar_wait(FULL(s), (uint32_t)((j / kStages) & 1));
+        const uint32_t base = stage0 + s * stage_bytes;
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+#pragma unroll
+        for (int t = 0; t < MS; t += 2) {
+            const float4 v0 = lds128(base + op[t]);
+            const float4 v1 = lds128(base + op[t + 1]);
+            acc0 = fmaf(v0.x, cf[t], acc0);
+            acc1 = fmaf(v0.y, cf[t], acc1);
+            acc2 = fmaf(v0.z, cf[t], acc2);
+            acc3 = fmaf(v0.w, cf[t], acc3);
+            acc0 = fmaf(v1.x, cf[t + 1], acc0);
+            acc1 = fmaf(v1.y, cf[t + 1], acc1);
+            acc2 = fmaf(v1.z, cf[t + 1], acc2);
+            acc3 = fmaf(v1.w, cf[t + 1], acc3);
+        }
+        mbar_arrive(EMPTY(s));
+        // 3. thread 0: the landing slot of group j+2 is free once every thread transposed it
+        if (a.tma && tid == 0) {
+            const long long jt = j + kStages - 1;  // group transposed in step 1
+            const long long jn = jt + kLanding;    // next occupant of its landing slot
+            if (jn < iters) {
+                const int l = (int)(jt % kLanding);
+                mbar_wait(LEMPTY(l), (uint32_t)((jt / kLanding) & 1));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_group(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
+            }
+        }
+        // 4. publish this lane's partials for group j
+        const int d = (int)(j % kPartSlots);
+        if (j >= kPartSlots) mbar_wait(PEMPTY(d), (uint32_t)(((j - kPartSlots) / kPartSlots) & 1));
+        part[d * W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
+        mbar_arrive(PFULL(d));
+        // 5. finish group j-1 while other warps still gather group j
+        if (j >= 1) epilogue(j - 1);
+    }
+    if (iters >= 1) epilogue(iters - 1);
+    // drain: every cp.async issued (fallback path) has landed before the CTA exits
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 typedef void (*KernelFn)(GatherArgs);
@@ -376,9 +412,9 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     a.landing_row = ((4 * p->n + 15) / 16) * 16;
 
-    const int threads = (pk.warps + kProducerWarps + kEpilogueWarps) * 32;
+    const int threads = pk.warps * 32;
     size_t smem = smem_bytes(pk, a.tma, a.landing_row);
-    if (smem > 227 * 1024 && a.tma) {  // very large rows: skip the landing ring
+    if (a.tma && smem > 227 * 1024) {  // very long rows: no room for the landing ring
         a.tma = 0;
         smem = smem_bytes(pk, 0, a.landing_row);
     }

@@ -31,3 +31,11 @@ if idx:
     lo, hi = idx[0], idx[-1]
     loop = sum(int(r[iS]) for r in data[lo - 10:hi + 40])
     print(f"main gather loop (LDS.128 span {lo}-{hi}, {len(idx)} LDS.128): {100 * loop / tot:.1f}% of samples")
+
+if len(sys.argv) > 2:
+    top = int(sys.argv[2])
+    iA = hdr.index("Address")
+    ranked = sorted(range(len(data)), key=lambda i: -int(data[i][iS]))[:top]
+    for i in sorted(ranked):
+        r = data[i]
+        print(f"  [{i:5d}] {int(r[iS]):6d} {100*int(r[iS])/tot:5.1f}%  exec={r[iE]:>10s}  {r[iSrc][:90]}")
