@@ -5,26 +5,27 @@
 // Design: a persistent kernel, one CTA per (hash block, row stream).
 //  * Each lane holds its hash part's slots in registers for the whole kernel: MS 32-bit smem
 //    byte offsets and MS f32 coefficients, in the bank-scheduled order of packer.cpp.
-//  * Rows are processed 4 at a time ("groups"). A stage holds 4 rows column-interleaved: the
-//    16-byte chunk at pos(c) = (c%4)*nq + c/4 is (x0[c], x1[c], x2[c], x3[c]). One LDS.128 per
-//    slot gathers the sampled coordinate of 4 rows; one FFMA per row accumulates it. The packer
-//    guarantees the 8 lanes of each quarter-warp hit 8 distinct bank groups at every slot, so each
-//    LDS.128 costs the ideal 4 wavefronts (32 gathers per wavefront).
+//  * Rows are processed 4*RG at a time ("groups"). A stage is RG sub-stages of 4 rows, each
+//    column-interleaved: the 16-byte chunk at pos(c) = (c%4)*nq + c/4 is (x0[c],..,x3[c]). One
+//    LDS.128 per slot and sub-stage gathers the sampled coordinate of 4 rows; one FFMA per row
+//    accumulates it. The packer guarantees the 8 lanes of each quarter-warp hit 8 distinct bank
+//    groups at every slot, so each LDS.128 costs the ideal 4 wavefronts (32 gathers/wavefront).
 //  * Staging: TMA bulk copies (cp.async.bulk ... complete_tx) bring each group's rows from HBM
 //    into a row-major 2-slot landing ring with 128-bit transfers; the CTA's warps transpose
-//    landing -> stage with conflict-free LDS.128 / STS.32. (Rows that are not 16-B aligned fall
-//    back to 4-byte cp.async straight into the transposed positions.)
+//    landing -> stage with conflict-free LDS.128 / STS.32. (Rows that are not 16-B aligned, or
+//    too long for the landing ring, fall back to 4-byte cp.async into the transposed positions.)
 //  * Pipeline without CTA barriers (mbarriers only, one iteration of slack): at iteration j every
 //    thread transposes its share of group j+2, gathers group j, publishes its partials for j, and
 //    finishes group j-1 (epilogue); thread 0 re-arms the landing slot freed by group j+2 with the
 //    TMA copies of group j+4.
-//  * Epilogue (fused): each thread takes a hash, sums its parts in fixed order for the 4 rows,
+//  * Epilogue (fused): each thread takes a hash, sums its parts in fixed order for each row,
 //    adds b (__fadd_rn), divides by w (__fdiv_rn; an exact multiply when w is a power of two),
 //    floors toward -inf and writes int32 codes (coalesced over hashes).
 #include <cuda_runtime.h>
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -39,7 +40,7 @@ constexpr int kBars = 2 * kStages + 2 * kPartSlots + 2 * kLanding;
 struct GatherArgs {
     const float* X;
     long long N;
-    int n, nq, stage_chunks;
+    int n, nq, stage_chunks;  // stage_chunks: chunks of ONE 4-row sub-stage
     const uint32_t* offp;
     const float* coef;
     const uint16_t* unit_lane;
@@ -48,7 +49,7 @@ struct GatherArgs {
     const int* block_kb;
     float w;
     int k, P, W, HB, kb_max;
-    long long groups;
+    long long groups;  // ceil(N / (4*RG))
     int32_t* codes;
     float* proj;
     unsigned long long* flags;
@@ -107,24 +108,28 @@ __device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// TMA copies of group g's live rows into a landing slot (one thread).
+__device__ __forceinline__ int live_rows(long long N, long long row0, int cap) {
+    const long long left = N - row0;
+    return (int)(left < cap ? (left > 0 ? left : 0) : cap);
+}
+
+// TMA copies of a group's live rows into a landing slot (one thread).
+template <int RG>
 __device__ __forceinline__ void issue_group(const GatherArgs& a, long long g, uint32_t land, uint32_t bar) {
-    const long long row0 = g * 4;
-    const int rows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
+    const long long row0 = g * (4 * RG);
+    const int rows = live_rows(a.N, row0, 4 * RG);
     const uint32_t bytes = 4u * (uint32_t)a.n;
     mbar_arrive_tx(bar, bytes * rows);
     for (int r = 0; r < rows; ++r)
         tma_bulk_g2s(land + r * a.landing_row, a.X + (row0 + r) * (long long)a.n, bytes, bar);
 }
 
-// This warp's share of the transposition of group g: item (r, q) = 128-bit read of row r's
-// chunk q in the landing slot (8 consecutive q per quarter-warp: conflict-free) and 4 scalar
-// stores to chunks i*nq+q, component r (32 consecutive words per warp store: conflict-free).
-// Rows >= N become 0.
-__device__ __forceinline__ void transpose_share(const GatherArgs& a, long long g, const float4* land,
-                                                float* stage, int lane, int warp, int W) {
-    const long long row0 = g * 4;
-    const int rows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
+// This warp's share of the transposition of one 4-row sub-stage: item (r, q) = 128-bit read of
+// row r's chunk q in the landing slot (8 consecutive q per quarter-warp: conflict-free) and 4
+// scalar stores to chunks i*nq+q, component r (32 consecutive words per store: conflict-free).
+// Rows >= `rows` become 0.
+__device__ __forceinline__ void transpose_share(const GatherArgs& a, int rows, const float4* land, float* stage,
+                                                int lane, int warp, int W) {
     const int nq = a.nq;
     const int comp = 4 * nq;              // floats between the 4 column components
     const int lrow = a.landing_row / 16;  // float4 per landing row
@@ -147,7 +152,7 @@ __device__ __forceinline__ void transpose_share(const GatherArgs& a, long long g
     }
 }
 
-// Fallback fill (rows not 16-B aligned): every float copied by a 4-byte cp.async straight into
+// Fallback fill of one 4-row sub-stage: every float copied by a 4-byte cp.async straight into
 // its transposed position (rows past N and columns past n read as 0).
 __device__ __forceinline__ void stage_fill_async(const GatherArgs& a, long long row0, uint32_t stage_u32) {
     const int items = 4 * a.nq;
@@ -166,14 +171,14 @@ __device__ __forceinline__ void stage_fill_async(const GatherArgs& a, long long 
     }
 }
 
-template <int MS>
+template <int MS, int RG>
 __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) float4 smem[];
-    const int SC = a.stage_chunks;
+    const int SC = a.stage_chunks;  // one sub-stage
     const int W = a.W;
-    float4* part = smem + kStages * SC;  // [kPartSlots][W*32]
-    unsigned char* land_base = reinterpret_cast<unsigned char*>(part + kPartSlots * W * 32);
-    const int land_bytes = 4 * a.landing_row;
+    float4* part = smem + kStages * RG * SC;  // [kPartSlots][RG][W*32]
+    unsigned char* land_base = reinterpret_cast<unsigned char*>(part + kPartSlots * RG * W * 32);
+    const int land_bytes = 4 * RG * a.landing_row;
     unsigned long long* bars =
         reinterpret_cast<unsigned long long*>(land_base + (a.tma ? kLanding * land_bytes : 0));
     uint16_t* s_unit = reinterpret_cast<uint16_t*>(bars + kBars);
@@ -188,7 +193,8 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * P + 1) & ~1));
 
     const uint32_t stage0 = smem_u32(smem);
-    const uint32_t stage_bytes = (uint32_t)SC * 16u;
+    const uint32_t sub_bytes = (uint32_t)SC * 16u;
+    const uint32_t stage_bytes = RG * sub_bytes;
     const uint32_t land0 = smem_u32(land_base);
     const uint32_t bar0 = smem_u32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
@@ -207,13 +213,13 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // zero chunks (padding slots read these), hash metadata
-    for (int i = tid; i < kStages * kPadChunks; i += nthreads)
+    for (int i = tid; i < kStages * RG * kPadChunks; i += nthreads)
         smem[(i / kPadChunks) * SC + 4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = tid; i < kb * P; i += nthreads)
         s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
 
-    // this lane's slots: byte offsets into a stage and coefficients
+    // this lane's slots: byte offsets into a sub-stage and coefficients
     uint32_t op[MS];
     float cf[MS];
     {
@@ -233,32 +239,40 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     // fill stage (jf % kStages) with group jf: this thread's share, then arrive on full
     auto fill = [&](long long jf) {
         const int sf = (int)(jf % kStages);
+        const long long row0 = group_of(jf) * (4 * RG);
         if (a.tma) {
             if (jf < iters) {
                 const int l = (int)(jf % kLanding);
                 mbar_wait(LFULL(l), (uint32_t)((jf / kLanding) & 1));
-                transpose_share(a, group_of(jf), reinterpret_cast<const float4*>(land_base + l * land_bytes),
-                                reinterpret_cast<float*>(smem + sf * SC), lane, warp, W);
+                const float4* land = reinterpret_cast<const float4*>(land_base + l * land_bytes);
+#pragma unroll
+                for (int u = 0; u < RG; ++u)
+                    transpose_share(a, live_rows(a.N, row0 + 4 * u, 4), land + u * (a.landing_row / 4),
+                                    reinterpret_cast<float*>(smem + (sf * RG + u) * SC), lane, warp, W);
                 mbar_arrive(LEMPTY(l));
             }
             mbar_arrive(FULL(sf));
         } else {
-            if (jf < iters) stage_fill_async(a, group_of(jf) * 4, stage0 + sf * stage_bytes);
+            if (jf < iters)
+#pragma unroll
+                for (int u = 0; u < RG; ++u)
+                    stage_fill_async(a, row0 + 4 * u, stage0 + sf * stage_bytes + u * sub_bytes);
             cp_async_arrive(FULL(sf));
         }
     };
 
     // prologue: TMA for groups 0..kLanding-1, stages for groups 0..kStages-2, re-arm landings
     if (a.tma && tid == 0)
-        for (int l = 0; l < kLanding && l < iters; ++l) issue_group(a, group_of(l), land0 + l * land_bytes, LFULL(l));
+        for (int l = 0; l < kLanding && l < iters; ++l)
+            issue_group<RG>(a, group_of(l), land0 + l * land_bytes, LFULL(l));
     for (int s = 0; s < kStages - 1; ++s) fill(s);
     if (a.tma && tid == 0) {
         for (int l = 0; l < kLanding && l < kStages - 1; ++l) {
             const long long jn = l + kLanding;  // next occupant of landing slot l
-            if (jn < iters && l < iters) {
+            if (jn < iters) {
                 mbar_wait(LEMPTY(l), 0);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_group(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
+                issue_group<RG>(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
             }
         }
     }
@@ -267,30 +281,31 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     const float inv_w = 1.0f / w;
     const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
 
-    // epilogue of iteration je: sum parts, quantise, store (one hash per thread, 4 rows)
+    // epilogue of iteration je: sum parts, quantise, store (one hash per thread, 4*RG rows)
     auto epilogue = [&](long long je) {
         const int d = (int)(je % kPartSlots);
         mbar_wait(PFULL(d), (uint32_t)((je / kPartSlots) & 1));
-        const float4* pb = part + d * W * 32;
-        const long long row0 = group_of(je) * 4;
-        const int nrows = (int)((a.N - row0) < 4 ? (a.N - row0) : 4);
+        const long long row0 = group_of(je) * (4 * RG);
+        const int nrows = live_rows(a.N, row0, 4 * RG);
         for (int h = tid; h < kb; h += nthreads) {
-            float4 s = pb[s_unit[h * P]];
-            for (int q = 1; q < P; ++q) {
-                const float4 v = pb[s_unit[h * P + q]];
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-            }
-            const float pr[4] = {s.x, s.y, s.z, s.w};
-            const long long o0 = row0 * a.k + h0 + h;
-            if (a.proj) {
+            const float bh = s_b[h];
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
-                    if (r < nrows) a.proj[o0 + (long long)r * a.k] = pr[r];
-            } else {
-                const float bh = s_b[h];
+            for (int u = 0; u < RG; ++u) {
+                const float4* pb = part + (d * RG + u) * W * 32;
+                float4 s = pb[s_unit[h * P]];
+                for (int q = 1; q < P; ++q) {
+                    const float4 v = pb[s_unit[h * P + q]];
+                    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+                }
+                const float pr[4] = {s.x, s.y, s.z, s.w};
+                const long long o0 = (row0 + 4 * u) * a.k + h0 + h;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    if (r >= nrows) break;
+                    if (4 * u + r >= nrows) break;
+                    if (a.proj) {
+                        a.proj[o0 + (long long)r * a.k] = pr[r];
+                        continue;
+                    }
                     // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
                     const float num = __fadd_rn(pr[r], bh);
                     const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
@@ -312,22 +327,22 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         // 1. fill the stage freed by iteration j-1 with group j+2
         if (j >= 1) mbar_wait(EMPTY((int)((j - 1) % kStages)), (uint32_t)(((j - 1) / kStages) & 1));
         fill(j + kStages - 1);
-        // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128
+        // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128 and sub-stage
         mbar_wait(FULL(s), (uint32_t)((j / kStages) & 1));
         const uint32_t base = stage0 + s * stage_bytes;
-        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+        float acc[RG][4];
 #pragma unroll
-        for (int t = 0; t < MS; t += 2) {
-            const float4 v0 = lds128(base + op[t]);
-            const float4 v1 = lds128(base + op[t + 1]);
-            acc0 = fmaf(v0.x, cf[t], acc0);
-            acc1 = fmaf(v0.y, cf[t], acc1);
-            acc2 = fmaf(v0.z, cf[t], acc2);
-            acc3 = fmaf(v0.w, cf[t], acc3);
-            acc0 = fmaf(v1.x, cf[t + 1], acc0);
-            acc1 = fmaf(v1.y, cf[t + 1], acc1);
-            acc2 = fmaf(v1.z, cf[t + 1], acc2);
-            acc3 = fmaf(v1.w, cf[t + 1], acc3);
+        for (int u = 0; u < RG; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.f;
+#pragma unroll
+        for (int t = 0; t < MS; ++t) {
+#pragma unroll
+            for (int u = 0; u < RG; ++u) {
+                const float4 v = lds128(base + u * sub_bytes + op[t]);
+                acc[u][0] = fmaf(v.x, cf[t], acc[u][0]);
+                acc[u][1] = fmaf(v.y, cf[t], acc[u][1]);
+                acc[u][2] = fmaf(v.z, cf[t], acc[u][2]);
+                acc[u][3] = fmaf(v.w, cf[t], acc[u][3]);
+            }
         }
         mbar_arrive(EMPTY(s));
         // 3. thread 0: the landing slot of group j+2 is free once every thread transposed it
@@ -338,13 +353,15 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
                 const int l = (int)(jt % kLanding);
                 mbar_wait(LEMPTY(l), (uint32_t)((jt / kLanding) & 1));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_group(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
+                issue_group<RG>(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
             }
         }
         // 4. publish this lane's partials for group j
         const int d = (int)(j % kPartSlots);
         if (j >= kPartSlots) mbar_wait(PEMPTY(d), (uint32_t)(((j - kPartSlots) / kPartSlots) & 1));
-        part[d * W * 32 + tid] = make_float4(acc0, acc1, acc2, acc3);
+#pragma unroll
+        for (int u = 0; u < RG; ++u)
+            part[(d * RG + u) * W * 32 + tid] = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
         mbar_arrive(PFULL(d));
         // 5. finish group j-1 while other warps still gather group j
         if (j >= 1) epilogue(j - 1);
@@ -357,11 +374,11 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 typedef void (*KernelFn)(GatherArgs);
 
 template <int MS>
-KernelFn kernel_for() { return gather_kernel<MS>; }
+KernelFn kernel_for(int rg) { return rg == 2 ? gather_kernel<MS, 2> : gather_kernel<MS, 1>; }
 
-KernelFn select_kernel(int MS) {
+KernelFn select_kernel(int MS, int rg) {
     switch (MS) {
-#define FASTLSH_CASE(X) case X: return kernel_for<X>();
+#define FASTLSH_CASE(X) case X: return kernel_for<X>(rg);
         FASTLSH_CASE(2) FASTLSH_CASE(4) FASTLSH_CASE(6) FASTLSH_CASE(8) FASTLSH_CASE(10)
         FASTLSH_CASE(12) FASTLSH_CASE(14) FASTLSH_CASE(16) FASTLSH_CASE(18) FASTLSH_CASE(20)
         FASTLSH_CASE(22) FASTLSH_CASE(24) FASTLSH_CASE(26) FASTLSH_CASE(28) FASTLSH_CASE(30)
@@ -374,10 +391,18 @@ KernelFn select_kernel(int MS) {
     }
 }
 
-size_t smem_bytes(const Packing& pk, int tma, int landing_row) {
-    return (size_t)kStages * pk.stage_chunks * 16 + (size_t)kPartSlots * pk.warps * 32 * 16 +
-           (tma ? (size_t)kLanding * 4 * landing_row : 0) + (size_t)kBars * 8 +
+size_t smem_bytes(const Packing& pk, int rg, int tma, int landing_row) {
+    return (size_t)kStages * rg * pk.stage_chunks * 16 + (size_t)kPartSlots * rg * pk.warps * 32 * 16 +
+           (tma ? (size_t)kLanding * 4 * rg * landing_row : 0) + (size_t)kBars * 8 +
            (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
+}
+
+int rows_per_group_override() {
+    static const int v = [] {
+        const char* e = std::getenv("FASTLSH_RG");  // experiment knob: 1 or 2 sub-stages
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
 }
 
 }  // namespace
@@ -385,7 +410,15 @@ size_t smem_bytes(const Packing& pk, int tma, int landing_row) {
 fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                              int64_t N, int32_t* codes, float* proj, cudaStream_t stream) {
     const Packing& pk = p->pack;
-    KernelFn fn = select_kernel(pk.slots);
+    const int landing_row = ((4 * p->n + 15) / 16) * 16;
+    int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    // 8 rows per stage when the 3-stage ring (+ landing ring) fits; else 4; TMA needs the ring
+    int rg = 2;
+    if (smem_bytes(pk, 2, tma, landing_row) > 227 * 1024) rg = 1;
+    if (int o = rows_per_group_override()) rg = (o == 1 ? 1 : 2);
+    if (tma && smem_bytes(pk, rg, 1, landing_row) > 227 * 1024) tma = 0;
+    if (smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg = 1;
+    KernelFn fn = select_kernel(pk.slots, rg);
     if (!fn) return FASTLSH_EUNSUPPORTED;
     GatherArgs a;
     a.X = X;
@@ -405,19 +438,15 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.W = pk.warps;
     a.HB = pk.hash_blocks;
     a.kb_max = pk.kb_max;
-    a.groups = (N + 3) / 4;
+    a.groups = (N + 4 * rg - 1) / (4 * rg);
     a.codes = codes;
     a.proj = proj;
     a.flags = d.flags;
-    a.tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    a.landing_row = ((4 * p->n + 15) / 16) * 16;
+    a.tma = tma;
+    a.landing_row = landing_row;
 
     const int threads = pk.warps * 32;
-    size_t smem = smem_bytes(pk, a.tma, a.landing_row);
-    if (a.tma && smem > 227 * 1024) {  // very long rows: no room for the landing ring
-        a.tma = 0;
-        smem = smem_bytes(pk, 0, a.landing_row);
-    }
+    const size_t smem = smem_bytes(pk, rg, tma, landing_row);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
