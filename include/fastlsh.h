@@ -130,7 +130,8 @@ fastlsh_status e2lsh_project(const fastlsh_params* p, const float* X, int64_t N,
 
 /* ---- compound bucket keys (§3.2) --------------------------- */
 
-/* r[l][j] uniform in [0, 2^61-1) from Philox stream 4 (R9). L, K >= 1. */
+/* r[l][j] uniform in [0, 2^61-1) from Philox stream 4 (R9). L, K >= 1 and
+ * L * (K + 1) <= 8192 (the multipliers live in shared memory), else EINVAL. */
 fastlsh_status fastlsh_keys_create(int32_t L, int32_t K, uint64_t seed, fastlsh_keys** out);
 fastlsh_status fastlsh_keys_create_from_arrays(int32_t L, int32_t K, const uint64_t* r,
                                                fastlsh_keys** out); /* r[L*(K+1)], each < 2^61-1 */

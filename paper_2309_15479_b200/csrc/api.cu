@@ -341,7 +341,7 @@ fastlsh_status e2lsh_project(const fastlsh_params* p, const float* X, int64_t N,
 fastlsh_status fastlsh_keys_create(int32_t L, int32_t K, uint64_t seed, fastlsh_keys** out) {
     if (!out) return FASTLSH_EINVAL;
     *out = nullptr;
-    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 16384) return FASTLSH_EINVAL;
+    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 8192) return FASTLSH_EINVAL;
     fastlsh_keys* ks = new (std::nothrow) fastlsh_keys();
     if (!ks) return FASTLSH_ENOMEM;
     ks->L = L; ks->K = K;
@@ -357,7 +357,7 @@ fastlsh_status fastlsh_keys_create_from_arrays(int32_t L, int32_t K, const uint6
                                                fastlsh_keys** out) {
     if (!out || !r) return FASTLSH_EINVAL;
     *out = nullptr;
-    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 16384) return FASTLSH_EINVAL;
+    if (L <= 0 || K <= 0 || (int64_t)L * (K + 1) > 8192) return FASTLSH_EINVAL;
     for (int64_t t = 0; t < (int64_t)L * (K + 1); ++t) if (r[t] >= kP61) return FASTLSH_EINVAL;
     fastlsh_keys* ks = new (std::nothrow) fastlsh_keys();
     if (!ks) return FASTLSH_ENOMEM;

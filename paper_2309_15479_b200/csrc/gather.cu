@@ -32,10 +32,8 @@
 namespace fastlsh {
 namespace {
 
-constexpr int kStages = 3;
 constexpr int kPartSlots = 2;
-constexpr int kLanding = 2;
-constexpr int kBars = 2 * kStages + 2 * kPartSlots + 2 * kLanding;
+constexpr int kBars = 2 * 3 + 2 * kPartSlots + 2 * 2;  // room for up to 3 stages and 2 landings
 
 struct GatherArgs {
     const float* X;
@@ -171,16 +169,16 @@ __device__ __forceinline__ void stage_fill_async(const GatherArgs& a, long long 
     }
 }
 
-template <int MS, int RG>
+template <int MS, int RG, int NS, int NL>
 __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const GatherArgs a) {
     extern __shared__ __align__(128) float4 smem[];
     const int SC = a.stage_chunks;  // one sub-stage
     const int W = a.W;
-    float4* part = smem + kStages * RG * SC;  // [kPartSlots][RG][W*32]
+    float4* part = smem + NS * RG * SC;  // [kPartSlots][RG][W*32]
     unsigned char* land_base = reinterpret_cast<unsigned char*>(part + kPartSlots * RG * W * 32);
     const int land_bytes = 4 * RG * a.landing_row;
     unsigned long long* bars =
-        reinterpret_cast<unsigned long long*>(land_base + (a.tma ? kLanding * land_bytes : 0));
+        reinterpret_cast<unsigned long long*>(land_base + (a.tma ? NL * land_bytes : 0));
     uint16_t* s_unit = reinterpret_cast<uint16_t*>(bars + kBars);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x;
@@ -198,22 +196,22 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     const uint32_t land0 = smem_u32(land_base);
     const uint32_t bar0 = smem_u32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
-    auto EMPTY = [&](int s) { return bar0 + 8u * (kStages + s); };
-    auto PFULL = [&](int d) { return bar0 + 8u * (2 * kStages + d); };
-    auto PEMPTY = [&](int d) { return bar0 + 8u * (2 * kStages + kPartSlots + d); };
-    auto LFULL = [&](int l) { return bar0 + 8u * (2 * kStages + 2 * kPartSlots + l); };
-    auto LEMPTY = [&](int l) { return bar0 + 8u * (2 * kStages + 2 * kPartSlots + kLanding + l); };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (NS + s); };
+    auto PFULL = [&](int d) { return bar0 + 8u * (2 * NS + d); };
+    auto PEMPTY = [&](int d) { return bar0 + 8u * (2 * NS + kPartSlots + d); };
+    auto LFULL = [&](int l) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + l); };
+    auto LEMPTY = [&](int l) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + NL + l); };
 
     if (tid == 0) {
-        for (int i = 0; i < 2 * kStages + 2 * kPartSlots; ++i) mbar_init(bar0 + 8u * i, nthreads);
-        for (int l = 0; l < kLanding; ++l) {
+        for (int i = 0; i < 2 * NS + 2 * kPartSlots; ++i) mbar_init(bar0 + 8u * i, nthreads);
+        for (int l = 0; l < NL; ++l) {
             mbar_init(LFULL(l), 1);
             mbar_init(LEMPTY(l), nthreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // zero chunks (padding slots read these), hash metadata
-    for (int i = tid; i < kStages * RG * kPadChunks; i += nthreads)
+    for (int i = tid; i < NS * RG * kPadChunks; i += nthreads)
         smem[(i / kPadChunks) * SC + 4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = tid; i < kb * P; i += nthreads)
         s_unit[i] = a.unit_lane[(size_t)hb * a.kb_max * P + i];
@@ -236,14 +234,14 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     const long long iters = rs < a.groups ? (a.groups - rs + gpr - 1) / gpr : 0;
     auto group_of = [&](long long j) { return rs + j * gpr; };
 
-    // fill stage (jf % kStages) with group jf: this thread's share, then arrive on full
+    // fill stage (jf % NS) with group jf: this thread's share, then arrive on full
     auto fill = [&](long long jf) {
-        const int sf = (int)(jf % kStages);
+        const int sf = (int)(jf % NS);
         const long long row0 = group_of(jf) * (4 * RG);
         if (a.tma) {
             if (jf < iters) {
-                const int l = (int)(jf % kLanding);
-                mbar_wait(LFULL(l), (uint32_t)((jf / kLanding) & 1));
+                const int l = (int)(jf % NL);
+                mbar_wait(LFULL(l), (uint32_t)((jf / NL) & 1));
                 const float4* land = reinterpret_cast<const float4*>(land_base + l * land_bytes);
 #pragma unroll
                 for (int u = 0; u < RG; ++u)
@@ -261,14 +259,14 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         }
     };
 
-    // prologue: TMA for groups 0..kLanding-1, stages for groups 0..kStages-2, re-arm landings
+    // prologue: TMA for groups 0..NL-1, stages for groups 0..NS-2, re-arm landings
     if (a.tma && tid == 0)
-        for (int l = 0; l < kLanding && l < iters; ++l)
+        for (int l = 0; l < NL && l < iters; ++l)
             issue_group<RG>(a, group_of(l), land0 + l * land_bytes, LFULL(l));
-    for (int s = 0; s < kStages - 1; ++s) fill(s);
+    for (int s = 0; s < NS - 1; ++s) fill(s);
     if (a.tma && tid == 0) {
-        for (int l = 0; l < kLanding && l < kStages - 1; ++l) {
-            const long long jn = l + kLanding;  // next occupant of landing slot l
+        for (int l = 0; l < NL && l < NS - 1; ++l) {
+            const long long jn = l + NL;  // next occupant of landing slot l
             if (jn < iters) {
                 mbar_wait(LEMPTY(l), 0);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -323,12 +321,12 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
     };
 
     for (long long j = 0; j < iters; ++j) {
-        const int s = (int)(j % kStages);
+        const int s = (int)(j % NS);
         // 1. fill the stage freed by iteration j-1 with group j+2
-        if (j >= 1) mbar_wait(EMPTY((int)((j - 1) % kStages)), (uint32_t)(((j - 1) / kStages) & 1));
-        fill(j + kStages - 1);
+        if (j >= 1) mbar_wait(EMPTY((int)((j - 1) % NS)), (uint32_t)(((j - 1) / NS) & 1));
+        fill(j + NS - 1);
         // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128 and sub-stage
-        mbar_wait(FULL(s), (uint32_t)((j / kStages) & 1));
+        mbar_wait(FULL(s), (uint32_t)((j / NS) & 1));
         const uint32_t base = stage0 + s * stage_bytes;
         float acc[RG][4];
 #pragma unroll
@@ -347,11 +345,11 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
         mbar_arrive(EMPTY(s));
         // 3. thread 0: the landing slot of group j+2 is free once every thread transposed it
         if (a.tma && tid == 0) {
-            const long long jt = j + kStages - 1;  // group transposed in step 1
-            const long long jn = jt + kLanding;    // next occupant of its landing slot
+            const long long jt = j + NS - 1;  // group transposed in step 1
+            const long long jn = jt + NL;    // next occupant of its landing slot
             if (jn < iters) {
-                const int l = (int)(jt % kLanding);
-                mbar_wait(LEMPTY(l), (uint32_t)((jt / kLanding) & 1));
+                const int l = (int)(jt % NL);
+                mbar_wait(LEMPTY(l), (uint32_t)((jt / NL) & 1));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue_group<RG>(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
             }
@@ -373,8 +371,12 @@ __global__ void __launch_bounds__(256, (MS <= 32 ? 2 : 1)) gather_kernel(const G
 
 typedef void (*KernelFn)(GatherArgs);
 
+// (rows per group / 4, stages, landing slots): 8 rows in a 3-stage ring with two landing slots,
+// or 4 rows likewise when 8 do not fit in shared memory.
 template <int MS>
-KernelFn kernel_for(int rg) { return rg == 2 ? gather_kernel<MS, 2> : gather_kernel<MS, 1>; }
+KernelFn kernel_for(int rg) {
+    return rg == 2 ? gather_kernel<MS, 2, 3, 2> : gather_kernel<MS, 1, 3, 2>;
+}
 
 KernelFn select_kernel(int MS, int rg) {
     switch (MS) {
@@ -392,14 +394,15 @@ KernelFn select_kernel(int MS, int rg) {
 }
 
 size_t smem_bytes(const Packing& pk, int rg, int tma, int landing_row) {
-    return (size_t)kStages * rg * pk.stage_chunks * 16 + (size_t)kPartSlots * rg * pk.warps * 32 * 16 +
-           (tma ? (size_t)kLanding * 4 * rg * landing_row : 0) + (size_t)kBars * 8 +
+    const int ns = rg == 4 ? 2 : 3, nl = rg == 4 ? 1 : 2;
+    return (size_t)ns * rg * pk.stage_chunks * 16 + (size_t)kPartSlots * rg * pk.warps * 32 * 16 +
+           (tma ? (size_t)nl * 4 * rg * landing_row : 0) + (size_t)kBars * 8 +
            (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
 }
 
 int rows_per_group_override() {
     static const int v = [] {
-        const char* e = std::getenv("FASTLSH_RG");  // experiment knob: 1 or 2 sub-stages
+        const char* e = std::getenv("FASTLSH_RG");  // experiment knob: 1, 2 or 4 sub-stages
         return e ? std::atoi(e) : 0;
     }();
     return v;
@@ -412,12 +415,13 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     const Packing& pk = p->pack;
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    // 8 rows per stage when the 3-stage ring (+ landing ring) fits; else 4; TMA needs the ring
+    // 8 rows per stage when the 3-stage ring (+ landing ring) fits, else 4. (16 rows in a
+    // 2-stage ring measured slower on C1: the shallower ring exposes the staging latency.)
     int rg = 2;
-    if (smem_bytes(pk, 2, tma, landing_row) > 227 * 1024) rg = 1;
-    if (int o = rows_per_group_override()) rg = (o == 1 ? 1 : 2);
+    while (rg > 1 && smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg /= 2;
+    if (int o = rows_per_group_override()) rg = (o == 2 ? 2 : 1);
     if (tma && smem_bytes(pk, rg, 1, landing_row) > 227 * 1024) tma = 0;
-    if (smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg = 1;
+    while (rg > 1 && smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg /= 2;
     KernelFn fn = select_kernel(pk.slots, rg);
     if (!fn) return FASTLSH_EUNSUPPORTED;
     GatherArgs a;

@@ -1,10 +1,13 @@
 // keys.cu — K3: compound bucket keys (§3.2).
 //
 // key_l(v) = (r[l][0] + sum_{j<K} r[l][j+1] * u32(code[v][l*K+j])) mod (2^61 - 1), exactly
-// (reading R9). A CTA takes 32 rows; for each slice of tables it stages the rows' codes
-// into shared memory with coalesced loads, one thread per (row, table) folds the K codes with
-// 64x64->128-bit products and Mersenne reduction, and the [table][row] keys are written as
-// contiguous 256-byte runs per table (table-major output for the NCCL all-gather).
+// (reading R9).
+//
+// A CTA takes 32 rows. Warp w handles rows w, w+8, ...; its lanes take consecutive tables of a
+// row, so a warp's loads cover one contiguous run of the row's codes (coalesced). Each term
+// r * u32(c) < 2^93 is accumulated exactly in 128 bits (K <= 2^30 terms cannot overflow) and
+// reduced mod 2^61-1 once. Keys go through shared memory so that the [table][row] output is
+// written as contiguous 256-byte runs per table (table-major, ready for the NCCL all-gather).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -17,49 +20,52 @@ namespace {
 constexpr uint64_t P61 = (1ull << 61) - 1;
 constexpr int kKeyRows = 32;
 constexpr int kKeyThreads = 256;
-constexpr int kCodeSmemInts = 8192;  // 32 KB of staged codes per slice
+constexpr int kTablesPerTile = 256;  // 64 KB of staged keys per tile
 
-__device__ __forceinline__ uint64_t mulmod61(uint64_t r, uint32_t c) {
-    const uint64_t lo = r * (uint64_t)c;
-    const uint64_t hi = __umul64hi(r, (uint64_t)c);  // < 2^29 since r < 2^61
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo) {
+    // hi*2^64 + lo with 2^64 = 8 * 2^61 == 8 (mod 2^61 - 1); hi < 2^40 here
     uint64_t x = (lo & P61) + (lo >> 61) + (hi << 3);
-    if (x >= P61) x -= P61;
-    return x;
+    x = (x & P61) + (x >> 61);
+    return x >= P61 ? x - P61 : x;
 }
 
 __global__ void __launch_bounds__(kKeyThreads) keys_kernel(const uint64_t* __restrict__ rmul,
                                                            const int32_t* __restrict__ codes,
                                                            long long N, int k, int L, int K,
-                                                           uint64_t* __restrict__ out, long long ldk) {
+                                                           uint64_t* __restrict__ out, long long ldk,
+                                                           int TL) {
     extern __shared__ __align__(16) unsigned char ksmem[];
-    uint64_t* s_r = reinterpret_cast<uint64_t*>(ksmem);
-    int32_t* s_c = reinterpret_cast<int32_t*>(s_r + L * (K + 1));
+    uint64_t* s_r = reinterpret_cast<uint64_t*>(ksmem);        // [L][K+1]
+    uint64_t* s_key = s_r + L * (K + 1);                        // [TL][kKeyRows]
     for (int i = threadIdx.x; i < L * (K + 1); i += blockDim.x) s_r[i] = rmul[i];
-    const int slice_ints = max(kCodeSmemInts, kKeyRows * K);
-    const int TL = max(1, min(L, slice_ints / (kKeyRows * K)));  // tables per slice
-    for (long long v0 = (long long)blockIdx.x * kKeyRows; v0 < N; v0 += (long long)gridDim.x * kKeyRows) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (long long t = blockIdx.x; t < ((N + kKeyRows - 1) / kKeyRows) * ((L + TL - 1) / TL); t += gridDim.x) {
+        const long long v0 = (t / ((L + TL - 1) / TL)) * kKeyRows;
+        const int l0 = (int)(t % ((L + TL - 1) / TL)) * TL;
+        const int l1 = min(L, l0 + TL);
         const int rows = (int)min((long long)kKeyRows, N - v0);
-        for (int l0 = 0; l0 < L; l0 += TL) {
-            const int tl = min(TL, L - l0);
-            const int cols = tl * K;
-            __syncthreads();
-            for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) {
-                const int r = i / cols, c = i - r * cols;
-                s_c[r * cols + c] = codes[(v0 + r) * k + l0 * K + c];
-            }
-            __syncthreads();
-            for (int i = threadIdx.x; i < tl * kKeyRows; i += blockDim.x) {
-                const int l = i / kKeyRows, r = i - l * kKeyRows;
-                if (r >= rows) continue;
-                const uint64_t* rl = s_r + (l0 + l) * (K + 1);
-                uint64_t acc = rl[0];
-                const int32_t* cr = s_c + r * cols + l * K;
+        __syncthreads();  // s_r ready / previous tile's keys written out
+        for (int rr = warp; rr < rows; rr += nw) {
+            const int32_t* crow = codes + (v0 + rr) * (long long)k;
+            for (int l = l0 + lane; l < l1; l += 32) {
+                const uint64_t* rl = s_r + l * (K + 1);
+                const int32_t* c = crow + l * K;
+                uint64_t lo = rl[0], hi = 0;
                 for (int j = 0; j < K; ++j) {
-                    acc += mulmod61(rl[j + 1], (uint32_t)cr[j]);
-                    if (acc >= P61) acc -= P61;
+                    const uint64_t r = rl[j + 1];
+                    const uint64_t u = (uint32_t)__ldg(c + j);
+                    const uint64_t plo = r * u;
+                    const uint64_t phi = __umul64hi(r, u);
+                    lo += plo;
+                    hi += phi + (lo < plo ? 1 : 0);
                 }
-                out[(long long)(l0 + l) * ldk + v0 + r] = acc;
+                s_key[(l - l0) * kKeyRows + rr] = reduce128(hi, lo);
             }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < (l1 - l0) * kKeyRows; i += blockDim.x) {
+            const int l = i / kKeyRows, rr = i - l * kKeyRows;
+            if (rr < rows) out[(long long)(l0 + l) * ldk + v0 + rr] = s_key[i];
         }
     }
 }
@@ -70,17 +76,22 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
                                  const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
                                  int64_t ldk, cudaStream_t stream) {
     const int L = keys->L, K = keys->K;
-    const size_t smem = (size_t)L * (K + 1) * 8 + (size_t)(K * kKeyRows > kCodeSmemInts ? K * kKeyRows : kCodeSmemInts) * 4;
+    const int TL = L < kTablesPerTile ? L : kTablesPerTile;  // tables per tile
+    const size_t smem = (size_t)L * (K + 1) * 8 + (size_t)TL * kKeyRows * 8;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(keys_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
-    int dev = 0, sms = 0;
+    int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long blocks = (N + kKeyRows - 1) / kKeyRows;
-    const long long cap = (long long)sms * 4;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(keys_kernel),
+                                                      kKeyThreads, smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+    long long blocks = ((N + kKeyRows - 1) / kKeyRows) * ((L + TL - 1) / TL);
+    const long long cap = (long long)sms * per_sm;
     if (blocks > cap) blocks = cap;
-    keys_kernel<<<(unsigned)blocks, kKeyThreads, smem, stream>>>(dev_r, codes, N, k, L, K, out, ldk);
+    keys_kernel<<<(unsigned)blocks, kKeyThreads, smem, stream>>>(dev_r, codes, N, k, L, K, out, ldk, TL);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e);
     return FASTLSH_OK;
