@@ -155,13 +155,17 @@ def _config_dict(cfg, world):
             "l2": f"inputs {cfg.N * cfg.n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
 
 
-def _traffic_from_profiles(kernel_substr: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def _traffic_from_profiles(cfg, rows: int):
+    """DRAM bytes per launch of the dominant kernel, from the committed `ncu --set full` capture
+    (profiles/ncu_gather_full.json: dram__bytes_read + dram__bytes_write of one K1 launch on the
+    same params), scaled per row to this launch's row count. None if no capture is committed."""
     path = os.path.join(ROOT, "profiles", "ncu_gather_full.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+        if d.get("config", "C1") != cfg.name:
+            return None
+        return d["dram_bytes_per_row"] * rows
     except Exception:
         return None
 
@@ -275,7 +279,7 @@ def main():
     t_roof_nominal = max(hbm_bytes / 8.0e12, gathers / g_peak)
     roofline = {"bound": "smem", "achieved": gathers / t_hash / 1e9, "peak": g_peak / 1e9,
                 "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
-                "traffic": _traffic_from_profiles("gather_kernel"),
+                "traffic": _traffic_from_profiles(cfg, N),
                 "kernel": "gather_kernel (K1 fastlsh_hash)",
                 "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
                 "north_star_frac": t_roof / t_hash, "north_star_frac_nominal_8TBs": t_roof_nominal / t_hash,
