@@ -1,12 +1,392 @@
-// e2lsh_tcgen05.cu — K4: dense E2LSH baseline on tcgen05 tensor cores.
-// (placeholder until the tcgen05 GEMM lands)
+// e2lsh_tcgen05.cu — K4: dense E2LSH baseline on 5th-gen tensor cores.
+//
+// codes = floor((X . A^T + b) / w), E2LSH Eq. 1, with A[k][n] the dense
+// coefficient matrix of the params (a_i itself for E2LSH params; the duplicates-merged sampled
+// matrix for FastLSH params). fp32 accuracy from TF32 tensor cores by the 3xTF32 split
+//     X.A ~= Xhi.Ahi + Xhi.Alo + Xlo.Ahi,   hi = fp32 with the low 13 mantissa bits cleared
+// (precision 3; precision 1 = plain Xhi.Ahi, the ungated reference point).
+//
+// One CTA computes a 256-row x 256-hash output tile (non-persistent grid). fp32 operands make the
+// GEMM bandwidth-hungry (A is re-read by every row tile), so rows per tile are 256: two UMMA
+// M=128 halves accumulate into two 256-column TMEM accumulators (all 512 columns).
+//   warp 0  : TMA producer — 2D tensor-map loads (64B swizzle, K-major) of the X tile
+//             [256 rows x 16 floats] and the Ahi/Alo tiles [256 x 16] per K-block, 3 stages.
+//   warps 2-9: split X in shared memory (in place: X -> Xhi, and Xlo into its own tile), then
+//             after the main loop: tcgen05.ld the accumulators (warp%4 = TMEM lane quadrant) and
+//             apply the fused +b, /w, floor epilogue (int32 codes or fp32 projections), stored
+//             through a per-warp transpose buffer as coalesced 128-byte row segments.
+//   warp 1  : TMEM allocation and the single-thread tcgen05.mma issue (kind::tf32, M=128,
+//             N=256, K=8 per instruction; 2 halves x 2 k-steps x 3 products per K-block);
+//             tcgen05.commit releases the smem stage and finally signals the epilogue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
 #include "internal.h"
 
 namespace fastlsh {
+namespace {
 
-fastlsh_status launch_e2lsh(const fastlsh_params*, DeviceCopy&, const float*, int64_t, int32_t*,
-                            float*, int, cudaStream_t) {
-    return FASTLSH_EUNSUPPORTED;
+constexpr int BM = 256;         // rows per tile: two UMMA M=128 halves, two TMEM accumulators
+constexpr int BN = 256;         // hashes per tile (UMMA N)
+constexpr int BK = 16;          // floats per K-block (one 64-byte swizzle row)
+constexpr int kStagesE = 3;
+constexpr int kThreadsE = 320;  // 10 warps
+constexpr uint32_t kXTileBytes = BM * BK * 4;   // 16 KB
+constexpr uint32_t kATileBytes = BN * BK * 4;   // 16 KB
+constexpr uint32_t kStageBytesE = 2 * kXTileBytes + 2 * kATileBytes;  // X, Xlo, Ahi, Alo
+
+struct E2Args {
+    long long N;
+    int n, k, kpad;
+    const float* b;
+    float w;
+    int precision;
+    int32_t* codes;
+    float* proj;
+    unsigned long long* flags;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 64-byte swizzle: rows of 64 B, 8-row atoms of
+// 512 B (SBO), LBO unused (1), version 1 (sm_100), layout type 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (16 B units)
+    d |= (uint64_t)(512 >> 4) << 32;        // SBO
+    d |= (uint64_t)1 << 46;                 // version
+    d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, N = 256, M = 128.
+constexpr uint32_t kIdescTF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kIdescTF32), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreadsE, 1)
+e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_ahi,
+                     const __grid_constant__ CUtensorMap map_alo, const E2Args a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-B alignment for the swizzle atoms
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagesE * kStageBytesE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStagesE + 1);
+    constexpr int kConvThreads = kThreadsE - 64;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long m0 = (long long)blockIdx.x * BM;
+    const int h0 = blockIdx.y * BN;
+    const int KB = (a.n + BK - 1) / BK;
+
+    const uint32_t sbase = smem_u32(smem);
+    auto XT = [&](int s) { return sbase + s * kStageBytesE; };
+    auto XL = [&](int s) { return sbase + s * kStageBytesE + kXTileBytes; };
+    auto AH = [&](int s) { return sbase + s * kStageBytesE + 2 * kXTileBytes; };
+    auto AL = [&](int s) { return sbase + s * kStageBytesE + 2 * kXTileBytes + kATileBytes; };
+    const uint32_t bar0 = smem_u32(bars);
+    auto FULL = [&](int s) { return bar0 + 8u * s; };
+    auto CONV = [&](int s) { return bar0 + 8u * (kStagesE + s); };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (2 * kStagesE + s); };
+    const uint32_t ACC = bar0 + 8u * (3 * kStagesE);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesE; ++s) {
+            mbar_init(FULL(s), 1);
+            mbar_init(CONV(s), kConvThreads);
+            mbar_init(EMPTY(s), 1);
+        }
+        mbar_init(ACC, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * BN)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            const uint32_t bytes = kXTileBytes + (a.precision == 3 ? 2 : 1) * kATileBytes;
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % kStagesE;
+                if (kb >= kStagesE) mbar_wait(EMPTY(s), (uint32_t)(((kb - kStagesE) / kStagesE) & 1));
+                mbar_arrive_tx(FULL(s), bytes);
+                tma_load_2d(XT(s), &map_x, kb * BK, (int)m0, FULL(s));
+                tma_load_2d(AH(s), &map_ahi, kb * BK, h0, FULL(s));
+                if (a.precision == 3) tma_load_2d(AL(s), &map_alo, kb * BK, h0, FULL(s));
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread) ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % kStagesE;
+                mbar_wait(CONV(s), (uint32_t)((kb / kStagesE) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
+                    const uint64_t dah = umma_desc_sw64(AH(s) + off);
+                    const uint64_t dal = umma_desc_sw64(AL(s) + off);
+                    const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+#pragma unroll
+                    for (int mh = 0; mh < 2; ++mh) {  // rows [128*mh, 128*mh+128) -> accumulator mh
+                        const uint32_t xo = off + mh * (kXTileBytes / 2);
+                        const uint64_t dxh = umma_desc_sw64(XT(s) + xo);
+                        const uint32_t td = tmem + mh * BN;
+                        umma_tf32(td, dxh, dah, acc0);
+                        if (a.precision == 3) {
+                            umma_tf32(td, dxh, dal, 1u);
+                            umma_tf32(td, umma_desc_sw64(XL(s) + xo), dah, 1u);
+                        }
+                    }
+                }
+                umma_commit(EMPTY(s));  // stage s reusable once these MMAs complete
+            }
+            umma_commit(ACC);  // accumulator complete
+        }
+    } else {
+        // ---------------- warps 2..9: split X in place, then the epilogue ----------------
+        const int t = threadIdx.x - 64;  // 0..255
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % kStagesE;
+            mbar_wait(FULL(s), (uint32_t)((kb / kStagesE) & 1));
+            if (a.precision == 3) {
+                float4* xt = reinterpret_cast<float4*>(smem + s * kStageBytesE);
+                float4* xl = reinterpret_cast<float4*>(smem + s * kStageBytesE + kXTileBytes);
+#pragma unroll
+                for (int i = 0; i < (int)(kXTileBytes / 16) / kConvThreads; ++i) {
+                    float4 v = xt[t + kConvThreads * i];
+                    float4 h, l;
+                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
+                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
+                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
+                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+                    xt[t + kConvThreads * i] = h;
+                    xl[t + kConvThreads * i] = l;
+                }
+                // make the generic-proxy stores visible to the tensor core (async proxy)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            mbar_arrive(CONV(s));
+        }
+        // epilogue: TMEM lane quadrant = warp % 4, one output row per thread
+        mbar_wait(ACC, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int quad = warp & 3;               // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;        // accumulator (row half) of this warp
+        const long long rbase = m0 + half * 128 + quad * 32;  // this warp's 32 rows
+        const float w = a.w;
+        const float inv_w = 1.0f / w;
+        const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
+        // 32x33 transpose buffer per warp (the operand stages are idle now): a lane computes one row,
+        // then the warp stores row segments of 32 consecutive hashes (128 B, coalesced)
+        uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + (warp - 2) * 32 * 33;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * BN + c0), v);
+            if (h0 + c0 >= a.k) break;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int h = h0 + c0 + j;
+                const float p = __uint_as_float(v[j]);
+                uint32_t out = v[j];
+                if (!a.proj && h < a.k) {
+                    const float num = __fadd_rn(p, a.b[h]);
+                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                    const float f = floorf(qv);
+                    int code = (int)f;
+                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
+                        code = INT_MIN;
+                        if (rbase + lane < a.N) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                    }
+                    out = (uint32_t)code;
+                }
+                tb[lane * 33 + j] = out;
+            }
+            __syncwarp();
+            const int h = h0 + c0 + lane;
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+                const long long row = rbase + r;
+                if (row < a.N && h < a.k) {
+                    const uint32_t val = tb[r * 33 + lane];
+                    if (a.proj) a.proj[row * a.k + h] = __uint_as_float(val);
+                    else a.codes[row * a.k + h] = (int32_t)val;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2D f32 tensor map over a row-major [rows][cols] matrix, box [box_rows][16 floats], 64B swizzle.
+bool make_map(CUtensorMap* m, const float* base, long long rows, int cols, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Dense hi/lo coefficient matrices on the device (once per params object and device).
+static fastlsh_status ensure_dense(const fastlsh_params* p, DeviceCopy& d) {
+    if (d.dense_hi) return FASTLSH_OK;
+    const int kpad = (p->k + BN - 1) / BN * BN;
+    std::vector<double> A((size_t)kpad * p->n, 0.0);
+    for (int i = 0; i < p->k; ++i)
+        for (int j = 0; j < p->m; ++j) A[(size_t)i * p->n + p->idx[(size_t)i * p->m + j]] += p->a[(size_t)i * p->m + j];
+    std::vector<float> hi(A.size()), lo(A.size());
+    for (size_t t = 0; t < A.size(); ++t) {
+        const float f = (float)A[t];
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        u &= 0xFFFFE000u;
+        float h;
+        std::memcpy(&h, &u, 4);
+        hi[t] = h;
+        lo[t] = f - h;  // exact
+    }
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d.dense_hi), hi.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&d.dense_lo), lo.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(d.dense_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d.dense_lo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(d.dense_hi); cudaFree(d.dense_lo);
+        d.dense_hi = d.dense_lo = nullptr;
+        return set_cuda_error(e);
+    }
+    d.dense_kpad = kpad;
+    return FASTLSH_OK;
+}
+
+fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
+                            float* proj, int precision, cudaStream_t stream) {
+    if (p->n % 4 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
+    {
+        std::lock_guard<std::mutex> g(const_cast<fastlsh_params*>(p)->mu);
+        fastlsh_status st = ensure_dense(p, d);
+        if (st != FASTLSH_OK) return st;
+    }
+    CUtensorMap mx, mh, ml;
+    if (!make_map(&mx, X, N, p->n, BM) || !make_map(&mh, d.dense_hi, d.dense_kpad, p->n, BN) ||
+        !make_map(&ml, d.dense_lo, d.dense_kpad, p->n, BN))
+        return FASTLSH_EUNSUPPORTED;
+    E2Args a;
+    a.N = N;
+    a.n = p->n;
+    a.k = p->k;
+    a.kpad = d.dense_kpad;
+    a.b = d.b;
+    a.w = p->w;
+    a.precision = precision;
+    a.codes = codes;
+    a.proj = proj;
+    a.flags = d.flags;
+    const size_t smem = kStagesE * kStageBytesE + 1024 + 128;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    dim3 grid((unsigned)((N + BM - 1) / BM), (unsigned)(d.dense_kpad / BN));
+    e2lsh_tcgen05_kernel<<<grid, kThreadsE, smem, stream>>>(mx, mh, ml, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e);
+    return FASTLSH_OK;
 }
 
 }  // namespace fastlsh

@@ -1,0 +1,62 @@
+"""Dense E2LSH baseline (tcgen05 3xTF32 GEMM) vs the CPU oracle."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2309_15479_b200 as fl
+from fastlsh_inputs import configs, data, e2lsh_arrays, fastlsh_arrays
+from parity import check_codes, check_projections
+
+pytestmark = pytest.mark.gpu
+THREADS = max(1, min(16, len(os.sched_getaffinity(0))))
+
+
+@pytest.mark.parametrize("N,n,k,w,recipe", [(1000, 128, 64, 4.0, "sift_u8"), (777, 960, 500, 1.0, "gist_mixture"),
+                                            (300, 784, 2000, 2.0, "sparse80"), (129, 4096, 256, 0.5, "trevi_sphere"),
+                                            (5, 32, 16, 1.0, "sift_u8")])
+def test_e2lsh_3xtf32_parity(N, n, k, w, recipe):
+    idx, A, b = e2lsh_arrays(n, k, w, seed=2)
+    P = fl.Params.from_arrays(n, w, idx, A, b)
+    X = data.generate(recipe, n, 0, N, seed=3, device="cuda")
+    proj = fl.e2lsh_project(P, X, precision=3).cpu().numpy()
+    codes = fl.e2lsh_hash(P, X, precision=3).cpu().numpy()
+    p, s, code = oracle.e2lsh(X.cpu().numpy(), A, b, w, threads=THREADS)
+    check_projections(proj, p, s)
+    check_codes(codes, p, s, code, b, w)
+
+
+def test_e2lsh_library_params_match_identity_fastlsh():
+    """e2lsh_params_create draws the same coefficients as identity-FastLSH (R11)."""
+    n, k, w = 256, 128, 1.0
+    P = fl.Params.e2lsh(n, k, w, seed=5)
+    idx, A, b = e2lsh_arrays(n, k, w, seed=5)
+    X = torch.randn((513, n), device="cuda")
+    codes = fl.e2lsh_hash(P, X).cpu().numpy()
+    p, s, code = oracle.e2lsh(X.cpu().numpy(), A, b, w, threads=THREADS)
+    check_codes(codes, p, s, code, b, w)
+
+
+def test_dense_path_on_fastlsh_params():
+    """The dense GEMM on FastLSH params (duplicates-merged coefficient matrix) computes Eq. 5."""
+    c = configs.get("C0")
+    idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, c.seed)
+    P = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    X = data.generate(c.data, c.n, 0, 2000, seed=1, device="cuda")
+    proj = fl.e2lsh_project(P, X).cpu().numpy()
+    p, s, _ = oracle.fastlsh(X.cpu().numpy(), idx, a, b, c.w, threads=THREADS)
+    check_projections(proj, p, s)
+
+
+def test_plain_tf32_is_less_accurate_than_3xtf32():
+    n, k, w = 960, 256, 1.0
+    idx, A, b = e2lsh_arrays(n, k, w, seed=7)
+    P = fl.Params.from_arrays(n, w, idx, A, b)
+    X = data.generate("gist_mixture", n, 0, 512, seed=1, device="cuda")
+    p, s, _ = oracle.e2lsh(X.cpu().numpy(), A, b, w, threads=THREADS)
+    e3 = np.abs(fl.e2lsh_project(P, X, precision=3).cpu().numpy() - p) / s
+    e1 = np.abs(fl.e2lsh_project(P, X, precision=1).cpu().numpy() - p) / s
+    assert e3.max() < 1e-5
+    assert e1.max() > 10 * e3.max()

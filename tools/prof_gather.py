@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--keys", action="store_true")
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--dense", action="store_true", help="time the tcgen05 dense baseline too")
+    ap.add_argument("--dense-e2lsh", action="store_true", help="dense baseline on E2LSH params (m = n)")
     args = ap.parse_args()
     c = configs.get(args.config)
     m = args.m or c.m
@@ -35,6 +37,22 @@ def main():
         if K:
             fl.build_keys(K, codes, out=keys)
     torch.cuda.synchronize()
+    if args.dense:
+        Pd = fl.Params.e2lsh(c.n, c.k, c.w, seed=c.seed) if args.dense_e2lsh else P
+        for prec in (3, 1):
+            fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 5
+            kpad = (c.k + 255) // 256 * 256
+            flops = 2.0 * args.rows * c.n * kpad * (3 if prec == 3 else 1)
+            print(f"dense e2lsh {args.config} prec={prec} rows={args.rows}: {ms:.3f} ms, "
+                  f"{args.rows * c.k / ms / 1e6:.3e} hashes/s, {flops / ms / 1e9:.1f} TFLOP/s (tf32 MMA rate)")
     if args.time:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
