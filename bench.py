@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -193,6 +194,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2309_15479_b200 as fl
+    from paper_2309_15479_b200.distributed import allgather_keys
     from fastlsh_inputs import data
 
     world, rank, local = _dist_env()
@@ -226,8 +228,7 @@ def main():
         if record:
             e[2].record(stream)
         if gathered is not None:
-            for l in range(cfg.L):
-                dist.all_gather_into_tensor(gathered[l], keys[l])
+            allgather_keys(keys, out=gathered)
         if record:
             e[3].record(stream)
             ev.append(e)
@@ -287,6 +288,29 @@ def main():
                 "peak_source": peaks["source"] + f"; smem peak = 148 SM x 32 x {peaks['sm_max_mhz']:.0f} MHz",
                 "kernel_share_of_step": statistics.mean(hash_ms) / ms_per_step if ms_per_step else None}
 
+    # on-box comparator: the dense E2LSH GEMM (tcgen05, m = n) on the same rows, k and w
+    dense = None
+    if not args.no_dense:
+        Pd = fl.Params.e2lsh(cfg.n, cfg.k, cfg.w, seed=cfg.seed)
+        dense = {}
+        for prec in (3, 1):
+            fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            d0.record(stream)
+            for _ in range(3):
+                fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+            d1.record(stream)
+            torch.cuda.synchronize()
+            ms = d0.elapsed_time(d1) / 3
+            kpad = (cfg.k + 255) // 256 * 256
+            dense[f"tf32x{prec}"] = {"ms": ms, "hashes_per_s": N * cfg.k / (ms / 1e3),
+                                     "mma_tflops": 2.0 * N * cfg.n * kpad * prec / (ms / 1e3) / 1e12,
+                                     "fastlsh_hash_speedup": ms / statistics.mean(hash_ms)}
+        dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows; tf32x3 is the "
+                         "parity-gated comparator (3xTF32), tf32x1 the ungated reference point")
+        del Pd
+
     # end to end through the public host-buffer API: H2D of X, hash + keys, D2H of codes + keys
     Xh = X.cpu().pin_memory()
     codes_h = torch.empty((N, cfg.k), dtype=torch.int32).pin_memory()
@@ -322,6 +346,7 @@ def main():
                 "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},
+                "dense_e2lsh": dense,
                 "packing": {k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
                                                  "bank_efficiency", "conflict_wavefronts")}}
         print(json.dumps(line))
