@@ -99,7 +99,7 @@ std::vector<QuarterState> group_units(const std::vector<Unit>& units, int Q, int
     int T = dmax;
     for (int guard = 0; guard < 64; ++guard, ++T) {
         bool any_excess = false;
-        for (int sweep = 0; sweep < 200; ++sweep) {
+        for (int sweep = 0; sweep < 24; ++sweep) {
             bool improved = false;
             any_excess = false;
             for (int q = 0; q < Q; ++q) {
@@ -346,8 +346,14 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
     }
     pk.conflict_wavefronts = conflicts;
     pk.efficiency = (double)useful / ((double)lanes_total * MS);
-    // cost in smem wavefronts per row: 4 per LDS.128 per warp per slot (one per quarter) + conflicts
-    out.cost = (double)HB * Wn * MS + (double)conflicts / 4.0;
+    // Cost model (shared-memory wavefronts per row / achievable pipe rate), from measurements on
+    // B200 (tools/microbench_lds.cu): gather = one wavefront per LDS.128 per warp per slot per 4
+    // rows -> HB*W*MS per row (+ scheduler conflicts); staging = landing read + transposed write of
+    // the row per hash block -> HB*n/16; epilogue partial traffic ~ k*P/4. The pipe reaches ~98%
+    // with 16 warps/SM (MS <= 32: <= 128 registers) but ~75% with 8 warps/SM (MS > 32).
+    const double wf = (double)HB * Wn * MS + (double)conflicts / 4.0 + (double)HB * p.n / 16.0 + p.k * P / 4.0;
+    const double rate = MS <= 32 ? 0.98 : 0.75;
+    out.cost = wf / rate;
     out.pk = std::move(pk);
 }
 
@@ -356,21 +362,32 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
 void build_packing(const fastlsh_params& p, Packing& out) {
     const int pmin = (p.m + kMaxSlots - 1) / kMaxSlots;
     int plo = pmin, phi = std::min(p.m, pmin + 2);
-    int warps_cap = 8;
+    // candidates: the fewest parts (<= 64 slots each), one or two more, and the split whose parts
+    // of <= 28 slots usually schedule into MS <= 32 (16 warps per SM)
+    const int p32 = std::min(p.m, (p.m + 27) / 28);
+    std::vector<int> cands;
+    for (int P = plo; P <= (pmin >= 16 ? plo : phi); ++P) cands.push_back(P);  // large m: fewer trials
+    if (p32 > phi) cands.push_back(p32);
+    int warps_force = 0;
     if (const char* e = std::getenv("FASTLSH_PARTS")) {  // experiment knob: force the split
         int v = std::atoi(e);
-        if (v >= pmin && v <= p.m) plo = phi = v;
+        if (v >= pmin && v <= p.m) cands.assign(1, v);
     }
     if (const char* e = std::getenv("FASTLSH_WARPS")) {  // experiment knob: warps per CTA
         int v = std::atoi(e);
-        if (v >= 1 && v <= 8) warps_cap = v;
+        if (v >= 1 && v <= 16) warps_force = v;
     }
     Trial best;
-    for (int P = plo; P <= phi; ++P) {
+    for (int P : cands) {
         // beyond 256 lanes per hash the block holds a single hash; keep P <= 256
         if (P > 256) break;
+        // 16 warps per CTA when the slots fit 128 registers per lane (MS <= 32), else 8
         Trial t;
-        try_parts(p, P, warps_cap * 32, t);
+        try_parts(p, P, (warps_force ? warps_force : 16) * 32, t);
+        if (!warps_force && t.pk.slots > 32) {
+            t = Trial();
+            try_parts(p, P, 8 * 32, t);
+        }
         if (t.cost < best.cost) best = std::move(t);
     }
     out = std::move(best.pk);
