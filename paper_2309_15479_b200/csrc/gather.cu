@@ -395,14 +395,27 @@ typedef void (*KernelFn)(GatherArgs);
 
 // (rows per group / 4, stages, landing slots): 8 rows in a 3-stage ring with two landing slots,
 // or 4 rows likewise when 8 do not fit in shared memory.
+// Pipeline shapes (rows per stage / 4, stages, landing slots), in order of preference; the first
+// whose shared memory fits is used. 16-row stages amortise the per-stage costs when rows are short
+// (n <= ~300); 8 rows suit mid-size rows (C1); very long rows (n = 4096) get a 2-stage ring with
+// one landing slot so that TMA staging still fits.
+struct Shape { int rg, ns, nl; };
+constexpr Shape kShapes[] = {{4, 3, 2}, {2, 3, 2}, {1, 3, 2}, {1, 2, 1}};
+constexpr int kNumShapes = 4;
+
 template <int MS>
-KernelFn kernel_for(int rg) {
-    return rg == 2 ? gather_kernel<MS, 2, 3, 2> : gather_kernel<MS, 1, 3, 2>;
+KernelFn kernel_for(int shape) {
+    switch (shape) {
+        case 0: return gather_kernel<MS, 4, 3, 2>;
+        case 1: return gather_kernel<MS, 2, 3, 2>;
+        case 2: return gather_kernel<MS, 1, 3, 2>;
+        default: return gather_kernel<MS, 1, 2, 1>;
+    }
 }
 
-KernelFn select_kernel(int MS, int rg) {
+KernelFn select_kernel(int MS, int shape) {
     switch (MS) {
-#define FASTLSH_CASE(X) case X: return kernel_for<X>(rg);
+#define FASTLSH_CASE(X) case X: return kernel_for<X>(shape);
         FASTLSH_CASE(2) FASTLSH_CASE(4) FASTLSH_CASE(6) FASTLSH_CASE(8) FASTLSH_CASE(10)
         FASTLSH_CASE(12) FASTLSH_CASE(14) FASTLSH_CASE(16) FASTLSH_CASE(18) FASTLSH_CASE(20)
         FASTLSH_CASE(22) FASTLSH_CASE(24) FASTLSH_CASE(26) FASTLSH_CASE(28) FASTLSH_CASE(30)
@@ -415,8 +428,8 @@ KernelFn select_kernel(int MS, int rg) {
     }
 }
 
-size_t smem_bytes(const Packing& pk, int rg, int tma, int landing_row) {
-    const int ns = rg == 4 ? 2 : 3, nl = rg == 4 ? 1 : 2;
+size_t smem_bytes(const Packing& pk, int shape, int tma, int landing_row) {
+    const int rg = kShapes[shape].rg, ns = kShapes[shape].ns, nl = kShapes[shape].nl;
     return (size_t)ns * rg * pk.stage_chunks * 16 + (size_t)kPartSlots * rg * pk.warps * 32 * 16 +
            (tma ? (size_t)nl * 4 * rg * landing_row : 0) + (size_t)kBars * 8 +
            (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
@@ -437,14 +450,24 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     const Packing& pk = p->pack;
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    // 8 rows per stage when the 3-stage ring (+ landing ring) fits, else 4. (16 rows in a
-    // 2-stage ring measured slower on C1: the shallower ring exposes the staging latency.)
-    int rg = 2;
-    while (rg > 1 && smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg /= 2;
-    if (int o = rows_per_group_override()) rg = (o == 2 ? 2 : 1);
-    if (tma && smem_bytes(pk, rg, 1, landing_row) > 227 * 1024) tma = 0;
-    while (rg > 1 && smem_bytes(pk, rg, tma, landing_row) > 227 * 1024) rg /= 2;
-    KernelFn fn = select_kernel(pk.slots, rg);
+    // the first pipeline shape that fits (with the TMA landing ring if the rows allow TMA); 16-row
+    // stages only for short rows, where they measured faster
+    constexpr size_t kSmemMax = 227 * 1024;
+    int shape = -1;
+    for (int s = (p->n <= 320 ? 0 : 1); s < kNumShapes && shape < 0; ++s)
+        if (smem_bytes(pk, s, tma, landing_row) <= kSmemMax) shape = s;
+    if (shape < 0 && tma) {  // no room for a landing ring: 4-byte cp.async fill
+        tma = 0;
+        for (int s = 1; s < kNumShapes && shape < 0; ++s)
+            if (smem_bytes(pk, s, 0, landing_row) <= kSmemMax) shape = s;
+    }
+    if (int o = rows_per_group_override()) {  // experiment knob: FASTLSH_RG = 4, 2, 1 (3 stages)
+        const int forced = o == 4 ? 0 : o == 2 ? 1 : 2;
+        if (smem_bytes(pk, forced, tma, landing_row) <= kSmemMax) shape = forced;
+    }
+    if (shape < 0) return FASTLSH_EUNSUPPORTED;
+    const int rg = kShapes[shape].rg;
+    KernelFn fn = select_kernel(pk.slots, shape);
     if (!fn) return FASTLSH_EUNSUPPORTED;
     GatherArgs a;
     a.X = X;
@@ -472,7 +495,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.landing_row = landing_row;
 
     const int threads = pk.warps * 32;
-    const size_t smem = smem_bytes(pk, rg, tma, landing_row);
+    const size_t smem = smem_bytes(pk, shape, tma, landing_row);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
