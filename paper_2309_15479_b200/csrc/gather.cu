@@ -33,7 +33,7 @@ namespace fastlsh {
 namespace {
 
 constexpr int kPartSlots = 2;
-constexpr int kBars = 2 * 3 + 2 * kPartSlots + 2 * 2;  // room for up to 3 stages and 2 landings
+constexpr int kBars = 2 * 4 + 2 * kPartSlots + 2 * 2;  // room for up to 4 stages and 2 landings
 
 struct GatherArgs {
     const float* X;
@@ -191,6 +191,10 @@ __device__ __forceinline__ void stage_fill_async(const GatherArgs& a, long long 
 
 template <int MS, int RG, int NS, int NL>
 __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const GatherArgs a) {
+    // fill distance: group j+FD is staged at iteration j, into the slot freed by group j+FD-NS;
+    // with 4 stages that wait is two iterations behind (more slack between warps)
+    constexpr int FD = NS >= 3 ? 2 : 1;
+    static_assert(FD <= NL, "the prologue transposes groups whose TMA was issued up front");
     extern __shared__ __align__(128) float4 smem[];
     const int SC = a.stage_chunks;  // one sub-stage
     const int W = a.W;
@@ -279,13 +283,13 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         }
     };
 
-    // prologue: TMA for groups 0..NL-1, stages for groups 0..NS-2, re-arm landings
+    // prologue: TMA for groups 0..NL-1, stages for groups 0..FD-1 (FD <= NL), re-arm landings
     if (a.tma && tid == 0)
         for (int l = 0; l < NL && l < iters; ++l)
             issue_group<RG>(a, group_of(l), land0 + l * land_bytes, LFULL(l));
-    for (int s = 0; s < NS - 1; ++s) fill(s);
+    for (int s = 0; s < FD; ++s) fill(s);
     if (a.tma && tid == 0) {
-        for (int l = 0; l < NL && l < NS - 1; ++l) {
+        for (int l = 0; l < NL && l < FD; ++l) {
             const long long jn = l + NL;  // next occupant of landing slot l
             if (jn < iters) {
                 mbar_wait_one(LEMPTY(l), 0);
@@ -344,9 +348,12 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
 
     for (long long j = 0; j < iters; ++j) {
         const int s = (int)(j % NS);
-        // 1. fill the stage freed by iteration j-1 with group j+2
-        if (j >= 1) mbar_wait(EMPTY((int)((j - 1) % NS)), (uint32_t)(((j - 1) / NS) & 1));
-        fill(j + NS - 1);
+        // 1. fill stage (j+FD) % NS with group j+FD once its previous group (j+FD-NS) is gathered
+        {
+            const long long jp = j + FD - NS;
+            if (jp >= 0) mbar_wait(EMPTY((int)(jp % NS)), (uint32_t)((jp / NS) & 1));
+            fill(j + FD);
+        }
         // 2. gather-FMA over the scheduled slots: 4 rows per LDS.128 and sub-stage
         mbar_wait(FULL(s), (uint32_t)((j / NS) & 1));
         const uint32_t base = stage0 + s * stage_bytes;
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         mbar_arrive(EMPTY(s));
         // 3. thread 0: the landing slot of group j+2 is free once every thread transposed it
         if (a.tma && tid == 0) {
-            const long long jt = j + NS - 1;  // group transposed in step 1
+            const long long jt = j + FD;  // group transposed in step 1
             const long long jn = jt + NL;    // next occupant of its landing slot
             if (jn < iters) {
                 const int l = (int)(jt % NL);
@@ -400,15 +407,16 @@ typedef void (*KernelFn)(GatherArgs);
 // (n <= ~300); 8 rows suit mid-size rows (C1); very long rows (n = 4096) get a 2-stage ring with
 // one landing slot so that TMA staging still fits.
 struct Shape { int rg, ns, nl; };
-constexpr Shape kShapes[] = {{4, 3, 2}, {2, 3, 2}, {1, 3, 2}, {1, 2, 1}};
-constexpr int kNumShapes = 4;
+constexpr Shape kShapes[] = {{4, 4, 2}, {2, 4, 2}, {2, 3, 2}, {1, 3, 2}, {1, 2, 1}};
+constexpr int kNumShapes = 5;
 
 template <int MS>
 KernelFn kernel_for(int shape) {
     switch (shape) {
-        case 0: return gather_kernel<MS, 4, 3, 2>;
-        case 1: return gather_kernel<MS, 2, 3, 2>;
-        case 2: return gather_kernel<MS, 1, 3, 2>;
+        case 0: return gather_kernel<MS, 4, 4, 2>;
+        case 1: return gather_kernel<MS, 2, 4, 2>;
+        case 2: return gather_kernel<MS, 2, 3, 2>;
+        case 3: return gather_kernel<MS, 1, 3, 2>;
         default: return gather_kernel<MS, 1, 2, 1>;
     }
 }
@@ -437,7 +445,7 @@ size_t smem_bytes(const Packing& pk, int shape, int tma, int landing_row) {
 
 int rows_per_group_override() {
     static const int v = [] {
-        const char* e = std::getenv("FASTLSH_RG");  // experiment knob: 1, 2 or 4 sub-stages
+        const char* e = std::getenv("FASTLSH_SHAPE");  // experiment knob: 1-based kShapes index
         return e ? std::atoi(e) : 0;
     }();
     return v;
@@ -450,22 +458,45 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     const Packing& pk = p->pack;
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    // the first pipeline shape that fits (with the TMA landing ring if the rows allow TMA); 16-row
-    // stages only for short rows, where they measured faster
+    // Pipeline shape: among the shapes whose shared memory fits (with the TMA landing ring when
+    // the rows allow TMA), the one with the most resident warps per SM up to 16 (measured: the
+    // gather loop saturates the shared-memory pipe at 16 warps/SM, ~75% at 8), earlier (deeper,
+    // larger) shapes on ties. Cached per device copy and TMA mode.
     constexpr size_t kSmemMax = 227 * 1024;
-    int shape = -1;
-    for (int s = (p->n <= 320 ? 0 : 1); s < kNumShapes && shape < 0; ++s)
-        if (smem_bytes(pk, s, tma, landing_row) <= kSmemMax) shape = s;
-    if (shape < 0 && tma) {  // no room for a landing ring: 4-byte cp.async fill
-        tma = 0;
-        for (int s = 1; s < kNumShapes && shape < 0; ++s)
-            if (smem_bytes(pk, s, 0, landing_row) <= kSmemMax) shape = s;
+    const int threads = pk.warps * 32;
+    int enc = d.shape_cache[tma];  // shape + 16 * (uses TMA), -1 = not chosen yet
+    if (enc < 0) {
+        int best_score = -1;
+        for (int pass = 0; pass < 2 && enc < 0; ++pass) {
+            const int t = pass == 0 ? tma : 0;  // pass 1: no room for a landing ring -> cp.async
+            if (pass == 1 && !tma) break;
+            for (int s = 0; s < kNumShapes; ++s) {
+                const size_t sm = smem_bytes(pk, s, t, landing_row);
+                if (sm > kSmemMax) continue;
+                KernelFn f = select_kernel(pk.slots, s);
+                if (!f) return FASTLSH_EUNSUPPORTED;
+                int occ = 0;
+                cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(f), threads, sm);
+                if (e != cudaSuccess) return set_cuda_error(e);
+                const int score = occ * pk.warps < 16 ? occ * pk.warps : 16;
+                if (occ > 0 && score > best_score) {
+                    best_score = score;
+                    enc = s + 16 * t;
+                }
+            }
+        }
+        if (enc < 0) return FASTLSH_EUNSUPPORTED;
+        d.shape_cache[tma] = enc;
     }
-    if (int o = rows_per_group_override()) {  // experiment knob: FASTLSH_RG = 4, 2, 1 (3 stages)
-        const int forced = o == 4 ? 0 : o == 2 ? 1 : 2;
+    int shape = enc % 16;
+    tma = enc / 16;
+    if (int o = rows_per_group_override()) {  // experiment knob: FASTLSH_SHAPE = 1..kNumShapes
+        const int forced = (o >= 1 && o <= kNumShapes) ? o - 1 : 1;
         if (smem_bytes(pk, forced, tma, landing_row) <= kSmemMax) shape = forced;
     }
-    if (shape < 0) return FASTLSH_EUNSUPPORTED;
     const int rg = kShapes[shape].rg;
     KernelFn fn = select_kernel(pk.slots, shape);
     if (!fn) return FASTLSH_EUNSUPPORTED;
@@ -494,7 +525,6 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.tma = tma;
     a.landing_row = landing_row;
 
-    const int threads = pk.warps * 32;
     const size_t smem = smem_bytes(pk, shape, tma, landing_row);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

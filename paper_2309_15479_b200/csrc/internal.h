@@ -64,6 +64,8 @@ struct DeviceCopy {
     int ws_L = 0;
     cudaStream_t ws_stream[2] = {nullptr, nullptr};
     cudaEvent_t ws_event[4] = {nullptr, nullptr, nullptr, nullptr};
+    // gather pipeline shape chosen per TMA mode (index: rows 16-B aligned), -1 = not chosen yet
+    mutable int shape_cache[2] = {-1, -1};
 };
 
 }  // namespace fastlsh

@@ -150,5 +150,7 @@ def test_bench_config_packing_quality(lib):
     c = configs.get("C1")
     p = fl.Params.create(c.n, c.m, c.k, c.w, seed=1)
     info = p.info()
+    # the cost model splits m=60 into 2 parts so that 16 warps/SM fit (MS <= 32 registers)
     assert info["conflict_wavefronts"] == 0
-    assert info["bank_efficiency"] >= 0.93
+    assert info["slots"] <= 32 and info["warps_per_block"] == 16
+    assert info["bank_efficiency"] >= 0.9
