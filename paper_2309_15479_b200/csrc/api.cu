@@ -249,19 +249,6 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* cp, int32_t* sizes, 
     return FASTLSH_OK;
 }
 
-fastlsh_status fastlsh_params_set_table_size(fastlsh_params* p, int32_t K) {
-    if (!p || K < 1) return FASTLSH_EINVAL;
-    std::lock_guard<std::mutex> g(p->mu);
-    for (int d = 0; d < kMaxDevices; ++d)
-        if (p->dev[d].ready) return FASTLSH_ESTATE;
-    if (p->table_align != K) {
-        p->table_align = K;
-        p->packed = false;
-        p->pack = Packing();
-    }
-    return FASTLSH_OK;
-}
-
 fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_stream_t stream) {
     if (!p) return FASTLSH_EINVAL;
     int dev = 0;
@@ -436,24 +423,8 @@ fastlsh_status fastlsh_build_keys(const fastlsh_keys* ks, const int32_t* codes, 
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
                                  int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
                                  fastlsh_stream_t stream) {
-    if (!ks || !keys_out) return fastlsh_hash(p, X, N, codes, stream);
-    if (!p || N < 0 || (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
-    if (N == 0) return FASTLSH_OK;
-    if (!X || !codes || ldk < N || (reinterpret_cast<uintptr_t>(X) & 3) ||
-        (reinterpret_cast<uintptr_t>(codes) & 3) || (reinterpret_cast<uintptr_t>(keys_out) & 7))
-        return FASTLSH_EINVAL;
-    int dev = 0;
-    fastlsh_status st = ready_params(p, &dev);
-    if (st != FASTLSH_OK) return st;
-    if (keys_fusable(p, ks)) {  // keys built in the hashing kernel's epilogue
-        const uint64_t* dr = nullptr;
-        st = keys_device(ks, dev, &dr);
-        if (st != FASTLSH_OK) return st;
-        FusedKeys fk{dr, ks->L, ks->K, keys_out, ldk};
-        return launch_gather(p, p->dev[dev], X, N, codes, nullptr, reinterpret_cast<cudaStream_t>(stream), &fk);
-    }
-    st = fastlsh_hash(p, X, N, codes, stream);
-    if (st != FASTLSH_OK) return st;
+    fastlsh_status st = fastlsh_hash(p, X, N, codes, stream);
+    if (st != FASTLSH_OK || !ks || !keys_out) return st;
     return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
 }
 
@@ -511,7 +482,6 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;
     }
-    const bool fuse = want_keys && keys_fusable(p, ks);
     const int64_t nchunks = (N + chunk_rows - 1) / chunk_rows;
     for (int64_t c = 0; c < nchunks; ++c) {
         const int b = (int)(c & 1);
@@ -520,17 +490,12 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         const int64_t rows = (N - r0 < chunk_rows) ? N - r0 : chunk_rows;
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
-        if (fuse) {
-            FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
-            st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
-        } else {
-            st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
-        }
+        st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
         if (st != FASTLSH_OK) return st;
         FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
         if (want_keys) {
-            if (!fuse) st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
+            st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
             if (st != FASTLSH_OK) return st;
             // keys of this chunk: [L][rows] on device -> columns r0.. of the [L][N] host matrix
             FL_CUDA(cudaMemcpy2DAsync(keys_host + r0, (size_t)N * sizeof(uint64_t), d.ws_keys[b],
