@@ -56,6 +56,10 @@ typedef struct {
     int32_t rows_per_group;    /* rows staged together per pipeline stage                        */
     double bank_efficiency;    /* useful gathers / (lanes * slots) over all warps                 */
     int64_t conflict_wavefronts; /* extra smem wavefronts per row left by the scheduler          */
+    int32_t kernel;            /* hashing kernel for 16-B aligned X: 1 = shared-memory gather K1,
+                                  2 = tensor-memory gather K1t                 */
+    int32_t tmem_hash_blocks;  /* K1t: CTAs hash blocks (0 when K1t does not apply)              */
+    int32_t tmem_hashes_per_warp; /* K1t: hashes (register accumulator pairs) per warp           */
 } fastlsh_params_info_t;
 
 /* ---- parameters: S_i, a_i, b_i, w --------------------- */
@@ -103,8 +107,18 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 /* ---- hashing ----------------------------------------------------------- */
 
+/* Choose the hashing kernel of these params (both compute Eq. 5, with the same
+ * epilogue; only the summation order of the fp32 projection differs, within the same bound):
+ *   0 = automatic (default): the tensor-memory gather K1t when it applies — n % 4 == 0, m <= 128,
+ *       the packed records fit in shared memory, X 16-byte aligned — else the shared-memory K1;
+ *   1 = always the shared-memory gather K1;
+ *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED).
+ * EINVAL for other values; EUNSUPPORTED for 2 when K1t cannot serve the params at all. */
+fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
+
 /* codes[r*k + i] = floor((a_i . S_i(X[r]) + b_i) / w) as int32, for r < N, i < k — Eq. 5.
- * fp32 accumulation in a bank-conflict-free slot order (in chunks of <= 64 products), then
+ * fp32 accumulation (K1: bank-conflict-free slot order in chunks of <= 64 products; K1t: slots
+ * grouped by 128-coordinate block, one accumulator over <= 128 products), then
  * __fadd_rn(p, b), __fdiv_rn(., w), floor toward -inf. Non-finite or out-of-int32 quotients
  * write INT32_MIN and count in the params' flags. Requires fastlsh_params_upload. */
 fastlsh_status fastlsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,

@@ -19,7 +19,7 @@ OK, EINVAL, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5
 EXPORTED = [
     "fastlsh_params_create", "fastlsh_params_create_from_arrays", "e2lsh_params_create",
     "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
-    "fastlsh_params_upload",
+    "fastlsh_params_upload", "fastlsh_params_set_kernel",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_host", "fastlsh_read_flags",
@@ -43,7 +43,8 @@ class _Info(ctypes.Structure):
                 ("slots", ctypes.c_int32), ("units", ctypes.c_int32),
                 ("warps_per_block", ctypes.c_int32), ("hash_blocks", ctypes.c_int32),
                 ("rows_per_group", ctypes.c_int32), ("bank_efficiency", ctypes.c_double),
-                ("conflict_wavefronts", ctypes.c_int64)]
+                ("conflict_wavefronts", ctypes.c_int64), ("kernel", ctypes.c_int32),
+                ("tmem_hash_blocks", ctypes.c_int32), ("tmem_hashes_per_warp", ctypes.c_int32)]
 
 
 _lib = None
@@ -66,6 +67,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_params_export": [P, P, P, P, P],
         "fastlsh_params_info": [P, ctypes.POINTER(_Info)],
         "fastlsh_params_upload": [P, i32, P],
+        "fastlsh_params_set_kernel": [P, i32],
         "fastlsh_params_packing": [P, P, P, P, P, P, P],
         "fastlsh_hash": [P, P, i64, P, P],
         "fastlsh_project": [P, P, i64, P, P],
@@ -185,6 +187,13 @@ class Params:
         return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, nq=nq, stage_chunks=sc,
                     offp=offp.reshape(HB, W, MS, 32), coef=coef.reshape(HB, W, MS, 32),
                     unit_lane=unit.reshape(HB, kbm, P), block_h0=h0, block_kb=kb)
+
+    def set_kernel(self, kernel):
+        """Pin the hashing kernel: "auto" (0), "smem" (1, K1) or "tmem" (2, K1t); see
+        fastlsh_params_set_kernel. Returns self."""
+        code = {"auto": 0, "smem": 1, "tmem": 2}.get(kernel, kernel)
+        _check(self._lib.fastlsh_params_set_kernel(self._h, int(code)), "fastlsh_params_set_kernel")
+        return self
 
     def upload(self, device=None, stream=None):
         import torch

@@ -80,6 +80,11 @@ fastlsh_status ensure_packed(fastlsh_params* p) {
         return FASTLSH_ENOMEM;
     }
     if (p->pack.slots <= 0) return FASTLSH_EUNSUPPORTED;
+    try {
+        if (!p->is_e2lsh) build_tmem_packing(*p, p->tpack);
+    } catch (...) {
+        return FASTLSH_ENOMEM;
+    }
     p->packed = true;
     return FASTLSH_OK;
 }
@@ -98,6 +103,7 @@ void free_device_copy(DeviceCopy& d) {
     cudaFree(d.offp); cudaFree(d.coef); cudaFree(d.unit_lane); cudaFree(d.b);
     cudaFree(d.block_h0); cudaFree(d.block_kb); cudaFree(d.flags);
     cudaFree(d.dense_hi); cudaFree(d.dense_lo);
+    cudaFree(d.t_recs); cudaFree(d.t_counts); cudaFree(d.t_offs); cudaFree(d.t_hinfo); cudaFree(d.t_groups);
     for (int i = 0; i < 2; ++i) {
         cudaFree(d.ws_x[i]); cudaFree(d.ws_codes[i]); cudaFree(d.ws_keys[i]);
         if (d.ws_stream[i]) cudaStreamDestroy(d.ws_stream[i]);
@@ -107,6 +113,19 @@ void free_device_copy(DeviceCopy& d) {
 }
 
 }  // namespace
+
+// K1t (TMEM gather) serves the call when pinned (kernel 2; an inapplicable call fails) or, in
+// auto mode, when kAutoTmem is set and its packing exists and X is 16-B aligned.
+constexpr bool kAutoTmem = false;  // K1t is still slower than K1 on the bench workload (C1)
+fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
+                           int32_t* codes, float* proj, cudaStream_t stream) {
+    if (p->kernel == 2 || (p->kernel == 0 && kAutoTmem)) {
+        fastlsh_status st = launch_gather_tmem(p, d, X, N, codes, proj, stream);
+        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 2) return st;
+    }
+    return launch_gather(p, d, X, N, codes, proj, stream);
+}
+
 }  // namespace fastlsh
 
 using namespace fastlsh;
@@ -222,6 +241,9 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
+    info->kernel = (p->kernel == 2 || (p->kernel == 0 && kAutoTmem && p->tpack.ok)) ? 2 : 1;
+    info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
+    info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
 }
 
@@ -271,7 +293,12 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
         (st = upload_vec(&d.unit_lane, pk.unit_lane, s)) != FASTLSH_OK ||
         (st = upload_vec(&d.b, p->b, s)) != FASTLSH_OK ||
         (st = upload_vec(&d.block_h0, h0, s)) != FASTLSH_OK ||
-        (st = upload_vec(&d.block_kb, kb, s)) != FASTLSH_OK) {
+        (st = upload_vec(&d.block_kb, kb, s)) != FASTLSH_OK ||
+        (p->tpack.ok && ((st = upload_vec(&d.t_recs, p->tpack.recs, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.t_counts, p->tpack.counts, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.t_offs, p->tpack.offs, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.t_hinfo, p->tpack.hinfo, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.t_groups, p->tpack.groups, s)) != FASTLSH_OK))) {
         free_device_copy(d);
         return st;
     }
@@ -286,6 +313,17 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
     return FASTLSH_OK;
 }
 
+
+fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
+    if (!p || kernel < 0 || kernel > 2) return FASTLSH_EINVAL;
+    std::lock_guard<std::mutex> g(p->mu);
+    fastlsh_status st = ensure_packed(p);
+    if (st != FASTLSH_OK) return st;
+    if (kernel == 2 && !p->tpack.ok) return FASTLSH_EUNSUPPORTED;
+    p->kernel = kernel;
+    return FASTLSH_OK;
+}
+
 static fastlsh_status hash_common(const fastlsh_params* p, const float* X, int64_t N,
                                   int32_t* codes, float* proj, fastlsh_stream_t stream) {
     if (!p || N < 0) return FASTLSH_EINVAL;
@@ -297,7 +335,7 @@ static fastlsh_status hash_common(const fastlsh_params* p, const float* X, int64
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
     if (st != FASTLSH_OK) return st;
-    return launch_gather(p, p->dev[dev], X, N, codes, proj, reinterpret_cast<cudaStream_t>(stream));
+    return launch_hash(p, p->dev[dev], X, N, codes, proj, reinterpret_cast<cudaStream_t>(stream));
 }
 
 fastlsh_status fastlsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
@@ -490,7 +528,7 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         const int64_t rows = (N - r0 < chunk_rows) ? N - r0 : chunk_rows;
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
-        st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
+        st = launch_hash(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
         if (st != FASTLSH_OK) return st;
         FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));

@@ -44,6 +44,27 @@ struct Packing {
     int64_t conflict_wavefronts = 0;  // extra wavefronts per stage (all blocks) beyond 4 per LDS
 };
 
+// GPU packing for the TMEM kernel K1t (gather_tmem.cu). Hash block hb serves
+// hashes [h0, h0+kb) as groups of 4 consecutive hashes; each warp slot s owns <= nhw/4 groups,
+// chosen so that every coordinate block costs the 4 warp slots about the same number of slots.
+// Records (TMEM column 2*(c - 128*block), coefficient bits) are grouped by (hb, warp slot,
+// coordinate block, hash), each hash's run padded to an even count; counts[hb][s][block][32]
+// give the run lengths (hash j of a warp slot = group j/4, member j%4).
+constexpr int kTMaxHB = 64;
+constexpr int kTInfo = 8;          // ints per hash block in TPacking::hinfo
+constexpr int kTGroups = 8;        // max groups of 4 hashes per warp slot
+struct TPacking {
+    bool ok = false;
+    int nb = 0, tb = 0, nhw = 0, HB = 0, recs_max = 0, kb_max = 0;  // nb even, tb coords per block
+    size_t smem = 0;
+    std::vector<int32_t> hinfo;    // [HB][8]: h0, kb, rec_base, rec_count, ngroups[4]
+    std::vector<int32_t> groups;   // [HB][4][8]: first hash of each group of the warp slot
+    std::vector<uint32_t> recs;    // [records][2]
+    std::vector<uint8_t> counts;   // [HB][4][nb][32]
+    std::vector<uint32_t> offs;    // [HB][4][nb] first record (relative to rec_base)
+    double balance = 0;            // sum over blocks of max warp-slot cost / mean cost
+};
+
 struct DeviceCopy {
     bool ready = false;
     uint32_t* offp = nullptr;
@@ -53,6 +74,11 @@ struct DeviceCopy {
     int32_t* block_h0 = nullptr;
     int32_t* block_kb = nullptr;
     unsigned long long* flags = nullptr;  // [0] nonfinite, [1] saturated
+    uint32_t* t_recs = nullptr;           // K1t packing (TPacking), when applicable
+    uint8_t* t_counts = nullptr;
+    uint32_t* t_offs = nullptr;
+    int32_t* t_hinfo = nullptr;
+    int32_t* t_groups = nullptr;
     float* dense_hi = nullptr;            // dense E2LSH operand A (tf32 hi) [kpad][n]
     float* dense_lo = nullptr;            // A - hi (tf32 lo)
     int dense_kpad = 0;
@@ -78,7 +104,9 @@ struct fastlsh_params {
     std::vector<float> a;      // [k][m]
     std::vector<float> b;      // [k]
     fastlsh::Packing pack;
+    fastlsh::TPacking tpack;
     bool packed = false;
+    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 shared-memory K1, 2 TMEM K1t
     fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
     std::mutex mu;
 };
@@ -98,6 +126,13 @@ void build_packing(const fastlsh_params& p, Packing& out);
 // gather.cu
 fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                              int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+// gather_tmem.cu
+void build_tmem_packing(const fastlsh_params& p, TPacking& out);
+fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, const float* X,
+                                  int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+// the hashing dispatcher (api.cu): K1t when selected/applicable, else K1
+fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
+                           int32_t* codes, float* proj, cudaStream_t stream);
 // keys.cu
 fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r,
                                  const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
