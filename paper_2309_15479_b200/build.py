@@ -14,7 +14,7 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+COMMON = [*os.environ.get("FASTLSH_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 SOURCES = ["api.cu", "gather.cu", "gather_tmem.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
 

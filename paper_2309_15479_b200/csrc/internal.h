@@ -45,24 +45,25 @@ struct Packing {
 };
 
 // GPU packing for the TMEM kernel K1t (gather_tmem.cu). Hash block hb serves
-// hashes [h0, h0+kb) as groups of 4 consecutive hashes; each warp slot s owns <= nhw/4 groups,
-// chosen so that every coordinate block costs the 4 warp slots about the same number of slots.
-// Records (TMEM column 2*(c - 128*block), coefficient bits) are grouped by (hb, warp slot,
-// coordinate block, hash), each hash's run padded to an even count; counts[hb][s][block][32]
-// give the run lengths (hash j of a warp slot = group j/4, member j%4).
+// hashes [h0, h0+kb) as groups of 4 consecutive hashes spread over the CTA's 16 warps (<= 4 groups
+// each; warp w works in TMEM lane quadrant w % 4), chosen so that every coordinate block costs the
+// warps about the same. Records (TMEM column 8*(c - 64*block), coefficient bits) are grouped by
+// (hb, warp, coordinate block, hash); counts[hb][warp][block][16]
+// give the run lengths (hash j of a warp = group j/4, member j%4).
 constexpr int kTMaxHB = 64;
-constexpr int kTInfo = 8;          // ints per hash block in TPacking::hinfo
-constexpr int kTGroups = 8;        // max groups of 4 hashes per warp slot
+constexpr int kTWarps = 16;
+constexpr int kTGroups = 2;                  // max groups of 4 hashes per warp
+constexpr int kTInfo = 4 + kTWarps;          // ints per hash block in TPacking::hinfo
 struct TPacking {
     bool ok = false;
-    int nb = 0, tb = 0, nhw = 0, HB = 0, recs_max = 0, kb_max = 0;  // nb even, tb coords per block
+    int nb = 0, nhw = 0, HB = 0, recs_max = 0, kb_max = 0;  // nb coordinate blocks of 64
     size_t smem = 0;
-    std::vector<int32_t> hinfo;    // [HB][8]: h0, kb, rec_base, rec_count, ngroups[4]
-    std::vector<int32_t> groups;   // [HB][4][8]: first hash of each group of the warp slot
+    std::vector<int32_t> hinfo;    // [HB][20]: h0, kb, rec_base, rec_count, ngroups[16]
+    std::vector<int32_t> groups;   // [HB][16][2]: first hash of each group of the warp
     std::vector<uint32_t> recs;    // [records][2]
-    std::vector<uint8_t> counts;   // [HB][4][nb][32]
-    std::vector<uint32_t> offs;    // [HB][4][nb] first record (relative to rec_base)
-    double balance = 0;            // sum over blocks of max warp-slot cost / mean cost
+    std::vector<uint8_t> counts;   // [HB][16][nb][16]
+    std::vector<uint32_t> offs;    // [HB][16][nb] first record (relative to rec_base)
+    double balance = 0;            // critical-path slots / mean slots per warp (>= 1)
 };
 
 struct DeviceCopy {

@@ -219,3 +219,53 @@ def test_keys_from_oracle_codes_c1():
     Kobj = fl.Keys.create(c.L, c.K, seed=1)
     keys_gpu = fl.build_keys(Kobj, torch.as_tensor(code.astype(np.int32)).cuda()).cpu().numpy().view(np.uint64)
     assert np.array_equal(keys_gpu, okeys.build_keys(code, r, c.L, c.K))
+
+
+# ---- K1t (tensor-memory gather, opt-in): the same parity rule on the same inputs ---------------------
+
+TMEM_CASES = [("C0", None), ("C1", 2003), ("C3", 4099), ("C4", 1001), ("C1", 70_001)]
+
+
+@pytest.mark.parametrize("name,N", TMEM_CASES)
+def test_tmem_kernel_parity(name, N):
+    c = configs.get(name)
+    N = N or c.N
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w, c.seed)
+    P.set_kernel("tmem")
+    assert P.info()["kernel"] == 2
+    X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
+    rows = None if N <= 5000 else _sample_rows(N, 1500, seed=3, extra=[255, 256, N - 2])
+    rel, amb, codes = _run_and_check(P, idx, a, b, c.w, X, rows=rows)
+    assert amb < 1e-2
+    P.set_kernel("smem")
+    codes_smem = fl.fastlsh_hash(P, X)
+    # both kernels compute Eq. 5 in fp32 with different summation orders: codes may differ only
+    # where a projection sits within fp32 rounding of a bucket boundary
+    assert (codes != codes_smem).float().mean().item() < 1e-3
+
+
+@pytest.mark.parametrize("N,n,m,k", [(1, 128, 16, 64), (257, 64, 128, 7), (300, 4, 4, 100), (513, 960, 60, 130),
+                                     (100, 8, 33, 1), (1000, 132, 20, 300)])
+def test_tmem_kernel_edge_shapes(N, n, m, k):
+    P, idx, a, b = _params(n, m, k, 1.5, seed=N + n)
+    P.set_kernel("tmem")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(N * 31 + n)
+    X = torch.randn((N, n), generator=g, device="cuda")
+    _run_and_check(P, idx, a, b, 1.5, X)
+
+
+def test_tmem_kernel_determinism_and_flags():
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    P.set_kernel("tmem")
+    X = data.generate(c.data, c.n, 0, 3000, seed=1, device="cuda")
+    c1 = fl.fastlsh_hash(P, X)
+    parts = torch.cat([fl.fastlsh_hash(P, X[i:j].contiguous()) for i, j in [(0, 999), (999, 3000)]])
+    assert torch.equal(c1, fl.fastlsh_hash(P, X)) and torch.equal(c1, parts)
+    X[5, :] = float("nan")
+    fl.read_flags(P, reset=True)
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    assert (codes[5] == -(2 ** 31)).all()
+    nf, sat = fl.read_flags(P, reset=True)
+    assert nf == c.k and sat == 0

@@ -154,3 +154,21 @@ def test_bench_config_packing_quality(lib):
     assert info["conflict_wavefronts"] == 0
     assert info["slots"] <= 32 and info["warps_per_block"] == 16
     assert info["bank_efficiency"] >= 0.9
+
+
+def test_kernel_selection_rules(lib):
+    """fastlsh_params_set_kernel: 0/1/2 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128."""
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import fastlsh_arrays
+    idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
+    P = fl.Params.from_arrays(128, 4.0, idx, a, b)
+    for k in ("auto", "smem", "tmem"):
+        P.set_kernel(k)
+    assert P.info()["kernel"] == 2 and P.info()["tmem_hash_blocks"] >= 1
+    with pytest.raises(fl.FastLSHError):
+        P.set_kernel(3)
+    idx, a, b = fastlsh_arrays(130, 16, 64, 4.0, 1)   # n % 4 != 0: no TMA tensor map
+    Q = fl.Params.from_arrays(130, 4.0, idx, a, b)
+    with pytest.raises(fl.FastLSHError):
+        Q.set_kernel("tmem")
+    assert Q.info()["kernel"] == 1

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--rows", type=int, default=262144)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--keys", action="store_true")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "smem", "tmem"])
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--dense", action="store_true", help="time the tcgen05 dense baseline too")
     ap.add_argument("--dense-e2lsh", action="store_true", help="dense baseline on E2LSH params (m = n)")
@@ -28,6 +29,7 @@ def main():
     c = configs.get(args.config)
     m = args.m or c.m
     P = fl.Params.create(c.n, m, c.k, c.w, seed=c.seed)
+    P.set_kernel(args.kernel)
     K = fl.Keys.create(c.L, c.K, seed=c.seed) if (args.keys and c.L) else None
     X = data.generate(c.data, c.n, 0, args.rows, seed=c.seed, device="cuda")
     codes = torch.empty((args.rows, c.k), dtype=torch.int32, device="cuda")
