@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
+    ap.add_argument("--fused-keys", action="store_true",
+                    help="build keys in K1's epilogue (measured slower on C1: 6.80 vs 6.42 ms/step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -204,8 +206,10 @@ def main():
     dev = torch.device("cuda", local)
 
     P = fl.Params.create(cfg.n, cfg.m, cfg.k, cfg.w, seed=cfg.seed)
-    info = P.info()
     Kobj = fl.Keys.create(cfg.L, cfg.K, seed=cfg.seed) if cfg.L else None
+    if Kobj is not None and args.fused_keys:
+        P.set_table_size(cfg.K)  # whole tables per CTA: keys are built in K1's epilogue
+    info = P.info()
     N = cfg.N
     X = data.generate(cfg.data, cfg.n, rank * N, (rank + 1) * N, seed=cfg.seed, device=dev)
     codes = torch.empty((N, cfg.k), dtype=torch.int32, device=dev)
@@ -213,18 +217,24 @@ def main():
     gathered = torch.empty((cfg.L, world * N), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
     stream = torch.cuda.current_stream()
 
-    launches_per_step = 1 + (1 if Kobj else 0)
+    fused_keys = bool(Kobj) and args.fused_keys
+    launches_per_step = 1 + (1 if (Kobj and not fused_keys) else 0)
     ev = []
 
     def step(record: bool):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
         if record:
             e[0].record(stream)
-        fl.fastlsh_hash(P, X, out=codes)
-        if record:
-            e[1].record(stream)
-        if Kobj:
-            fl.build_keys(Kobj, codes, out=keys)
+        if Kobj and args.fused_keys:
+            fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
+            if record:
+                e[1].record(stream)
+        else:
+            fl.fastlsh_hash(P, X, out=codes)
+            if record:
+                e[1].record(stream)
+            if Kobj:
+                fl.build_keys(Kobj, codes, out=keys)
         if record:
             e[2].record(stream)
         if gathered is not None:
@@ -281,7 +291,7 @@ def main():
     roofline = {"bound": "smem", "achieved": gathers / t_hash / 1e9, "peak": g_peak / 1e9,
                 "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
                 "traffic": _traffic_from_profiles(cfg, N),
-                "kernel": "gather_kernel (K1 fastlsh_hash)",
+                "kernel": "gather_kernel (K1 fastlsh_hash" + (", keys fused in its epilogue)" if fused_keys else ")"),
                 "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
                 "north_star_frac": t_roof / t_hash, "north_star_frac_nominal_8TBs": t_roof_nominal / t_hash,
                 "hbm_achieved_gbs": hbm_bytes / t_hash / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"],
@@ -343,6 +353,7 @@ def main():
                 "config": _config_dict(cfg, world), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks,
+                "keys_fused": fused_keys,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},

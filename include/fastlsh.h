@@ -101,6 +101,12 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* p, int32_t* sizes, u
                                       float* coef, uint16_t* unit_lane, int32_t* block_h0,
                                       int32_t* block_kb);
 
+/* Hint that keys of K consecutive codes will be built from these params: the GPU
+ * packing then keeps whole tables inside each CTA hash block, which lets fastlsh_hash_keys build
+ * the keys in the hashing kernel's epilogue (codes are still written). Must be called before the
+ * first upload (ESTATE otherwise); K >= 1 (EINVAL otherwise). Results are identical either way. */
+fastlsh_status fastlsh_params_set_table_size(fastlsh_params* p, int32_t K);
+
 /* Pack the bank-scheduled GPU layout and copy it to the CURRENT device (cudaSetDevice first).
  * `device` must equal the current device. Idempotent per device. */
 fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_stream_t stream);

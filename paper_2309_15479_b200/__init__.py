@@ -19,7 +19,7 @@ OK, EINVAL, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5
 EXPORTED = [
     "fastlsh_params_create", "fastlsh_params_create_from_arrays", "e2lsh_params_create",
     "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
-    "fastlsh_params_upload", "fastlsh_params_set_kernel",
+    "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_host", "fastlsh_read_flags",
@@ -68,6 +68,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_params_info": [P, ctypes.POINTER(_Info)],
         "fastlsh_params_upload": [P, i32, P],
         "fastlsh_params_set_kernel": [P, i32],
+        "fastlsh_params_set_table_size": [P, i32],
         "fastlsh_params_packing": [P, P, P, P, P, P, P],
         "fastlsh_hash": [P, P, i64, P, P],
         "fastlsh_project": [P, P, i64, P, P],
@@ -193,6 +194,12 @@ class Params:
         fastlsh_params_set_kernel. Returns self."""
         code = {"auto": 0, "smem": 1, "tmem": 2}.get(kernel, kernel)
         _check(self._lib.fastlsh_params_set_kernel(self._h, int(code)), "fastlsh_params_set_kernel")
+        return self
+
+    def set_table_size(self, K: int):
+        """Pack hash blocks as whole tables of K hashes so keys are built inside the hashing kernel
+        (fastlsh_params_set_table_size); call before the first upload."""
+        _check(self._lib.fastlsh_params_set_table_size(self._h, int(K)), "fastlsh_params_set_table_size")
         return self
 
     def upload(self, device=None, stream=None):

@@ -117,9 +117,12 @@ void free_device_copy(DeviceCopy& d) {
 // K1t (TMEM gather) serves the call when pinned (kernel 2; an inapplicable call fails) or, in
 // auto mode, when kAutoTmem is set and its packing exists and X is 16-B aligned.
 constexpr bool kAutoTmem = false;  // K1t is still slower than K1 on the bench workload (C1)
+bool tmem_selected(const fastlsh_params* p) {
+    return p->kernel == 2 || (p->kernel == 0 && kAutoTmem && p->tpack.ok);
+}
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
-    if (p->kernel == 2 || (p->kernel == 0 && kAutoTmem)) {
+    if (tmem_selected(p)) {
         fastlsh_status st = launch_gather_tmem(p, d, X, N, codes, proj, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 2) return st;
     }
@@ -241,7 +244,7 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
-    info->kernel = (p->kernel == 2 || (p->kernel == 0 && kAutoTmem && p->tpack.ok)) ? 2 : 1;
+    info->kernel = tmem_selected(p) ? 2 : 1;
     info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
     info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
@@ -268,6 +271,19 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* cp, int32_t* sizes, 
     if (unit_lane) std::memcpy(unit_lane, pk.unit_lane.data(), pk.unit_lane.size() * sizeof(uint16_t));
     if (block_h0) for (size_t i = 0; i < pk.block_h0.size(); ++i) block_h0[i] = pk.block_h0[i];
     if (block_kb) for (size_t i = 0; i < pk.block_kb.size(); ++i) block_kb[i] = pk.block_kb[i];
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_set_table_size(fastlsh_params* p, int32_t K) {
+    if (!p || K < 1) return FASTLSH_EINVAL;
+    std::lock_guard<std::mutex> g(p->mu);
+    for (int d = 0; d < kMaxDevices; ++d)
+        if (p->dev[d].ready) return FASTLSH_ESTATE;
+    if (p->table_align != K) {
+        p->table_align = K;
+        p->packed = false;
+        p->pack = Packing();
+    }
     return FASTLSH_OK;
 }
 
@@ -461,8 +477,24 @@ fastlsh_status fastlsh_build_keys(const fastlsh_keys* ks, const int32_t* codes, 
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
                                  int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
                                  fastlsh_stream_t stream) {
-    fastlsh_status st = fastlsh_hash(p, X, N, codes, stream);
-    if (st != FASTLSH_OK || !ks || !keys_out) return st;
+    if (!ks || !keys_out) return fastlsh_hash(p, X, N, codes, stream);
+    if (!p || N < 0 || (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X || !codes || ldk < N || (reinterpret_cast<uintptr_t>(X) & 3) ||
+        (reinterpret_cast<uintptr_t>(codes) & 3) || (reinterpret_cast<uintptr_t>(keys_out) & 7))
+        return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    if (keys_fusable(p, ks) && !tmem_selected(p)) {  // keys built in K1's epilogue
+        const uint64_t* dr = nullptr;
+        st = keys_device(ks, dev, &dr);
+        if (st != FASTLSH_OK) return st;
+        FusedKeys fk{dr, ks->L, ks->K, keys_out, ldk};
+        return launch_gather(p, p->dev[dev], X, N, codes, nullptr, reinterpret_cast<cudaStream_t>(stream), &fk);
+    }
+    st = fastlsh_hash(p, X, N, codes, stream);
+    if (st != FASTLSH_OK) return st;
     return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
 }
 
@@ -520,6 +552,7 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;
     }
+    const bool fuse = want_keys && keys_fusable(p, ks) && !tmem_selected(p);
     const int64_t nchunks = (N + chunk_rows - 1) / chunk_rows;
     for (int64_t c = 0; c < nchunks; ++c) {
         const int b = (int)(c & 1);
@@ -528,12 +561,17 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         const int64_t rows = (N - r0 < chunk_rows) ? N - r0 : chunk_rows;
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
-        st = launch_hash(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
+        if (fuse) {
+            FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
+            st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
+        } else {
+            st = launch_hash(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
+        }
         if (st != FASTLSH_OK) return st;
         FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
         if (want_keys) {
-            st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
+            if (!fuse) st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
             if (st != FASTLSH_OK) return st;
             // keys of this chunk: [L][rows] on device -> columns r0.. of the [L][N] host matrix
             FL_CUDA(cudaMemcpy2DAsync(keys_host + r0, (size_t)N * sizeof(uint64_t), d.ws_keys[b],

@@ -33,7 +33,7 @@ namespace fastlsh {
 namespace {
 
 constexpr int kPartSlots = 2;
-constexpr int kBars = 2 * 4 + 2 * kPartSlots + 2 * 2;  // room for up to 4 stages and 2 landings
+constexpr int kBars = 2 * 4 + 2 * kPartSlots + 2 * 2 + 4;  // up to 4 stages, 2 landings, 2 code slots
 
 struct GatherArgs {
     const float* X;
@@ -53,6 +53,11 @@ struct GatherArgs {
     unsigned long long* flags;
     int tma;           // 1: TMA landing ring + transposition; 0: 4-byte cp.async fill
     int landing_row;   // bytes per landing row (4n rounded up to 16)
+    // fused compound keys: keys != nullptr when every hash block holds whole tables
+    const uint64_t* kr;  // multipliers [L][K+1]
+    int L, K, tables_max;
+    uint64_t* keys;      // [L][ldk]
+    long long ldk;
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -212,7 +217,13 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
     const int kb = a.block_kb[hb];
     const int h0 = a.block_h0[hb];
     const int P = a.P;
-    float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * P + 1) & ~1));
+    float* s_b = reinterpret_cast<float*>(s_unit + ((a.kb_max * P + 3) & ~3));
+    // fused keys: codes of the last two groups [2][4*RG][kb_max] and this block's multipliers
+    const bool fused = a.keys != nullptr;
+    int32_t* cbuf = reinterpret_cast<int32_t*>(s_b + ((a.kb_max + 1) & ~1));
+    uint64_t* s_kr = reinterpret_cast<uint64_t*>(cbuf + (fused ? 2 * 4 * RG * a.kb_max : 0));
+    const int t_lo = fused ? h0 / a.K : 0;                                     // first table of the block
+    const int nt = fused ? max(0, min(a.L, (h0 + kb) / a.K) - t_lo) : 0;      // whole tables in the block
 
     const uint32_t stage0 = smem_u32(smem);
     const uint32_t sub_bytes = (uint32_t)SC * 16u;
@@ -225,6 +236,8 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
     auto PEMPTY = [&](int d) { return bar0 + 8u * (2 * NS + kPartSlots + d); };
     auto LFULL = [&](int l) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + l); };
     auto LEMPTY = [&](int l) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + NL + l); };
+    auto CFULL = [&](int d) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + 2 * NL + d); };
+    auto CEMPTY = [&](int d) { return bar0 + 8u * (2 * NS + 2 * kPartSlots + 2 * NL + 2 + d); };
 
     if (tid == 0) {
         for (int i = 0; i < 2 * NS + 2 * kPartSlots; ++i) mbar_init(bar0 + 8u * i, nthreads);
@@ -232,8 +245,13 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
             mbar_init(LFULL(l), 1);
             mbar_init(LEMPTY(l), nthreads);
         }
+        for (int d = 0; d < 2; ++d) {
+            mbar_init(CFULL(d), nthreads);
+            mbar_init(CEMPTY(d), nthreads);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int i = tid; i < nt * (a.K + 1); i += nthreads) s_kr[i] = a.kr[(size_t)t_lo * (a.K + 1) + i];
     // zero chunks (padding slots read these), hash metadata
     for (int i = tid; i < NS * RG * kPadChunks; i += nthreads)
         smem[(i / kPadChunks) * SC + 4 * a.nq + (i % kPadChunks)] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -309,6 +327,10 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         mbar_wait(PFULL(d), (uint32_t)((je / kPartSlots) & 1));
         const long long row0 = group_of(je) * (4 * RG);
         const int nrows = live_rows(a.N, row0, 4 * RG);
+        // fused keys: code slot cs is free once the keys of group je-2 are built
+        const int cs = (int)(je & 1);
+        int32_t* cb = cbuf + cs * 4 * RG * a.kb_max;
+        if (fused && je >= 2) mbar_wait(CEMPTY(cs), (uint32_t)(((je - 2) >> 1) & 1));
         // items (hash, sub-stage) spread over all threads so every warp does an equal share
         for (int it = tid; it < kb * RG; it += nthreads) {
             int u = 0, h = it;
@@ -340,10 +362,44 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
                         atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
                     }
                     a.codes[o0 + (long long)r * a.k] = code;
+                    if (fused) cb[(4 * u + r) * a.kb_max + h] = code;
                 }
             }
         }
         mbar_arrive(PEMPTY(d));
+        if (fused) mbar_arrive(CFULL(cs));
+    };
+
+    // fused keys of group jk: key_l(v) = (r0 + sum_j r_{j+1} u32(c_{lK+j})) mod 2^61-1,
+    // items (table, row) with rows fastest (coalesced u64 stores), exact 128-bit accumulation
+    auto build_keys = [&](long long jk) {
+        const int cs = (int)(jk & 1);
+        mbar_wait(CFULL(cs), (uint32_t)((jk >> 1) & 1));
+        const int32_t* cb = cbuf + cs * 4 * RG * a.kb_max;
+        const long long row0 = group_of(jk) * (4 * RG);
+        const int nrows = live_rows(a.N, row0, 4 * RG);
+        const int K = a.K;
+        for (int it = tid; it < nt * 4 * RG; it += nthreads) {
+            const int rr = it % (4 * RG), t = it / (4 * RG);
+            if (rr >= nrows) continue;
+            const uint64_t* rl = s_kr + t * (K + 1);
+            const int32_t* c = cb + rr * a.kb_max + (t_lo + t) * K - h0;
+            uint64_t lo = rl[0], hi = 0;
+            for (int jj = 0; jj < K; ++jj) {
+                const uint64_t r = rl[jj + 1];
+                const uint64_t u32c = (uint32_t)c[jj];
+                const uint64_t plo = r * u32c;
+                const uint64_t phi = __umul64hi(r, u32c);
+                lo += plo;
+                hi += phi + (lo < plo ? 1 : 0);
+            }
+            // hi*2^64 + lo, 2^64 == 8 (mod 2^61 - 1); hi < 2^40
+            constexpr uint64_t P61 = (1ull << 61) - 1;
+            uint64_t x = (lo & P61) + (lo >> 61) + (hi << 3);
+            x = (x & P61) + (x >> 61);
+            a.keys[(long long)(t_lo + t) * a.ldk + row0 + rr] = x >= P61 ? x - P61 : x;
+        }
+        mbar_arrive(CEMPTY(cs));
     };
 
     for (long long j = 0; j < iters; ++j) {
@@ -392,8 +448,14 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         mbar_arrive(PFULL(d));
         // 5. finish group j-1 while other warps still gather group j
         if (j >= 1) epilogue(j - 1);
+        // 6. fused keys of group j-2 (its codes are complete in shared memory)
+        if (fused && j >= 2) build_keys(j - 2);
     }
     if (iters >= 1) epilogue(iters - 1);
+    if (fused) {
+        if (iters >= 2) build_keys(iters - 2);
+        if (iters >= 1) build_keys(iters - 1);
+    }
     // drain: every cp.async issued (fallback path) has landed before the CTA exits
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -436,11 +498,13 @@ KernelFn select_kernel(int MS, int shape) {
     }
 }
 
-size_t smem_bytes(const Packing& pk, int shape, int tma, int landing_row) {
+// keys_words: 0, or (tables per block) * (K + 1) when compound keys are fused
+size_t smem_bytes(const Packing& pk, int shape, int tma, int landing_row, int keys_words) {
     const int rg = kShapes[shape].rg, ns = kShapes[shape].ns, nl = kShapes[shape].nl;
     return (size_t)ns * rg * pk.stage_chunks * 16 + (size_t)kPartSlots * rg * pk.warps * 32 * 16 +
            (tma ? (size_t)nl * 4 * rg * landing_row : 0) + (size_t)kBars * 8 +
-           (size_t)(((pk.kb_max * pk.parts + 1) & ~1) * 2) + (size_t)pk.kb_max * 4;
+           (size_t)(((pk.kb_max * pk.parts + 3) & ~3) * 2) + (size_t)((pk.kb_max + 1) & ~1) * 4 +
+           (keys_words ? (size_t)2 * 4 * rg * pk.kb_max * 4 + (size_t)keys_words * 8 : 0);
 }
 
 int rows_per_group_override() {
@@ -454,24 +518,29 @@ int rows_per_group_override() {
 }  // namespace
 
 fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
-                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream) {
+                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
+                             const FusedKeys* fk) {
     const Packing& pk = p->pack;
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    const int fused = (fk && fk->keys && codes) ? 1 : 0;
+    const int tables_max = fused ? pk.kb_max / fk->K + 1 : 0;
+    const int keys_words = fused ? tables_max * (fk->K + 1) : 0;
     // Pipeline shape: among the shapes whose shared memory fits (with the TMA landing ring when
     // the rows allow TMA), the one with the most resident warps per SM up to 16 (measured: the
     // gather loop saturates the shared-memory pipe at 16 warps/SM, ~75% at 8), earlier (deeper,
-    // larger) shapes on ties. Cached per device copy and TMA mode.
+    // larger) shapes on ties. Cached per device copy, TMA mode and fused-keys mode.
     constexpr size_t kSmemMax = 227 * 1024;
     const int threads = pk.warps * 32;
-    int enc = d.shape_cache[tma];  // shape + 16 * (uses TMA), -1 = not chosen yet
+    int& cache = d.shape_cache[tma + 2 * fused];
+    int enc = cache;  // shape + 16 * (uses TMA), -1 = not chosen yet
     if (enc < 0) {
         int best_score = -1;
         for (int pass = 0; pass < 2 && enc < 0; ++pass) {
             const int t = pass == 0 ? tma : 0;  // pass 1: no room for a landing ring -> cp.async
             if (pass == 1 && !tma) break;
             for (int s = 0; s < kNumShapes; ++s) {
-                const size_t sm = smem_bytes(pk, s, t, landing_row);
+                const size_t sm = smem_bytes(pk, s, t, landing_row, keys_words);
                 if (sm > kSmemMax) continue;
                 KernelFn f = select_kernel(pk.slots, s);
                 if (!f) return FASTLSH_EUNSUPPORTED;
@@ -489,13 +558,13 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
             }
         }
         if (enc < 0) return FASTLSH_EUNSUPPORTED;
-        d.shape_cache[tma] = enc;
+        cache = enc;
     }
     int shape = enc % 16;
     tma = enc / 16;
     if (int o = rows_per_group_override()) {  // experiment knob: FASTLSH_SHAPE = 1..kNumShapes
         const int forced = (o >= 1 && o <= kNumShapes) ? o - 1 : 1;
-        if (smem_bytes(pk, forced, tma, landing_row) <= kSmemMax) shape = forced;
+        if (smem_bytes(pk, forced, tma, landing_row, keys_words) <= kSmemMax) shape = forced;
     }
     const int rg = kShapes[shape].rg;
     KernelFn fn = select_kernel(pk.slots, shape);
@@ -524,8 +593,14 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.flags = d.flags;
     a.tma = tma;
     a.landing_row = landing_row;
+    a.kr = fused ? fk->r : nullptr;
+    a.L = fused ? fk->L : 0;
+    a.K = fused ? fk->K : 1;
+    a.tables_max = tables_max;
+    a.keys = fused ? fk->keys : nullptr;
+    a.ldk = fused ? fk->ldk : 0;
 
-    const size_t smem = smem_bytes(pk, shape, tma, landing_row);
+    const size_t smem = smem_bytes(pk, shape, tma, landing_row, keys_words);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
@@ -545,6 +620,17 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e);
     return FASTLSH_OK;
+}
+
+bool keys_fusable(const fastlsh_params* p, const fastlsh_keys* ks) {
+    if (!p->packed || p->table_align != ks->K || (int64_t)ks->L * ks->K > p->k) return false;
+    const Packing& pk = p->pack;
+    for (int bl = 0; bl < pk.hash_blocks; ++bl) {
+        if (pk.block_h0[bl] % ks->K) return false;
+        const int end = pk.block_h0[bl] + pk.block_kb[bl];
+        if (end % ks->K && end < ks->L * ks->K) return false;  // a table split across blocks
+    }
+    return true;
 }
 
 }  // namespace fastlsh

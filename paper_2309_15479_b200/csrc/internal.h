@@ -92,7 +92,7 @@ struct DeviceCopy {
     cudaStream_t ws_stream[2] = {nullptr, nullptr};
     cudaEvent_t ws_event[4] = {nullptr, nullptr, nullptr, nullptr};
     // gather pipeline shape chosen per TMA mode (index: rows 16-B aligned), -1 = not chosen yet
-    mutable int shape_cache[2] = {-1, -1};
+    mutable int shape_cache[4] = {-1, -1, -1, -1};  // [tma + 2 * fused keys]
 };
 
 }  // namespace fastlsh
@@ -108,6 +108,7 @@ struct fastlsh_params {
     fastlsh::TPacking tpack;
     bool packed = false;
     int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 shared-memory K1, 2 TMEM K1t
+    int32_t table_align = 1;   // hash blocks hold whole tables of this many hashes (fused keys)
     fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
     std::mutex mu;
 };
@@ -125,8 +126,17 @@ namespace fastlsh {
 void build_packing(const fastlsh_params& p, Packing& out);
 
 // gather.cu
+struct FusedKeys {            // compound keys built in the hashing kernel's epilogue
+    const uint64_t* r;        // device multipliers [L][K+1]
+    int L, K;
+    uint64_t* keys;           // device [L][ldk]
+    int64_t ldk;
+};
 fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const float* X,
-                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+                             int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
+                             const FusedKeys* fk = nullptr);
+// true when every hash block of the packing holds whole tables of `keys`
+bool keys_fusable(const fastlsh_params* p, const fastlsh_keys* keys);
 // gather_tmem.cu
 void build_tmem_packing(const fastlsh_params& p, TPacking& out);
 fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, const float* X,

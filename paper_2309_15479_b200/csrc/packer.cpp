@@ -207,13 +207,20 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
     pk.stage_chunks = 4 * pk.nq + kPadChunks;
     const int dmax = (m + P - 1) / P;
     const int kb_cap = std::max(1, lanes_cap / P);
-    const int HB = (k + kb_cap - 1) / kb_cap;
+    // Hash blocks: k hashes split as evenly as possible into HB CTA blocks; with a table size T
+    // (fastlsh_params_set_table_size) blocks hold whole tables of T consecutive hashes (the hashes
+    // past the last whole table go to the last block), so keys can be built inside the kernel.
+    const int T = (p.table_align > 1 && p.table_align <= kb_cap) ? p.table_align : 1;
+    const int units = k / T, rem = k % T;
+    int HB = (k + kb_cap - 1) / kb_cap;
+    while (((units + HB - 1) / HB) * T + rem > kb_cap) ++HB;
+    if (units > 0 && HB > units) HB = units;
     pk.hash_blocks = HB;
     pk.block_h0.resize(HB);
     pk.block_kb.resize(HB);
     int h0 = 0;
     for (int bl = 0; bl < HB; ++bl) {
-        pk.block_kb[bl] = k / HB + (bl < k % HB ? 1 : 0);
+        pk.block_kb[bl] = (units / HB + (bl < units % HB ? 1 : 0)) * T + (bl == HB - 1 ? rem : 0);
         pk.block_h0[bl] = h0;
         h0 += pk.block_kb[bl];
     }

@@ -186,9 +186,30 @@ def test_identity_plan_matches_e2lsh_oracle():
     check_codes(codes, p, s, code, b, w)
 
 
-def test_host_entry_point_matches_device_path():
+@pytest.mark.parametrize("name,L,K,N,extra_k", [("C1", 50, 10, 3001, 0), ("C4", 200, 10, 1203, 0),
+                                                ("C3", 16, 16, 4097, 0), ("C0", 5, 12, 999, 4)])
+def test_fused_keys_equal_separate_kernels(name, L, K, N, extra_k):
+    """Keys built in K1's epilogue (whole tables per CTA) == codes + the standalone key kernel."""
+    c = configs.get(name)
+    k = L * K + extra_k if name == "C0" else c.k
+    idx, a, b = fastlsh_arrays(c.n, c.m, k, c.w, 3)
+    P_fused = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(K)
+    P_plain = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    Kobj = fl.Keys.from_arrays(philox.key_multipliers(L, K, seed=4))
+    X = data.generate(c.data, c.n, 0, N, seed=5, device="cuda")
+    codes_f, keys_f = fl.hash_keys(P_fused, Kobj, X)
+    codes_p = fl.fastlsh_hash(P_plain, X)
+    keys_p = fl.build_keys(Kobj, codes_p)
+    assert torch.equal(codes_f, codes_p)
+    assert torch.equal(keys_f, keys_p)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_host_entry_point_matches_device_path(fused):
     c = configs.get("C4")
     P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    if fused:
+        P.set_table_size(c.K)
     K = fl.Keys.create(c.L, c.K, seed=1)
     X = data.generate(c.data, c.n, 0, 10_000, seed=1, device="cuda")
     codes_d, keys_d = fl.hash_keys(P, K, X)
