@@ -16,7 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [*os.environ.get("FASTLSH_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
-SOURCES = ["api.cu", "gather.cu", "gather_tmem.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
+SOURCES = ["api.cu", "gather.cu", "gather_inst0.cu", "gather_inst1.cu", "gather_inst2.cu", "gather_inst3.cu",
+           "gather_tmem.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
 
 
 def _stale(out: str, deps) -> bool:
@@ -28,7 +29,7 @@ def _stale(out: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "fastlsh.h"))
     objs, jobs = [], []
     for src in SOURCES:
