@@ -70,12 +70,106 @@ __global__ void __launch_bounds__(kKeyThreads) keys_kernel(const uint64_t* __res
     }
 }
 
+
+// Fast path (K <= 16): a warp owns a group of 32 consecutive tables (lane = table, its K+1
+// multipliers in registers as three 21-bit limbs r = r2*2^42 + r1*2^21 + r0) and a block of 32
+// rows. Per term, three IMAD.WIDE.U32 accumulate limb*u32(c) (< 2^53) into 64-bit sums
+// S0, S1, S2 (K <= 2^10 terms cannot overflow); then
+//   key = (r_0 + S0 + S1*2^21 + S2*2^42) mod (2^61-1),
+// where x*2^j mod (2^61-1) is a 61-bit rotation — all exact. The 32x32 keys of a (group, row
+// block) go through shared memory so each table's 32 rows are written as one 256-byte run.
+__device__ __forceinline__ uint64_t mod61(uint64_t x) {  // x < 2^64 -> x mod (2^61 - 1)
+    x = (x & P61) + (x >> 61);
+    return x >= P61 ? x - P61 : x;
+}
+__device__ __forceinline__ uint64_t rotl61(uint64_t x, int j) {  // x < 2^61: x * 2^j mod (2^61 - 1)
+    return ((x << j) & P61) | (x >> (61 - j));
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) keys_kernel_fast(const uint64_t* __restrict__ rmul,
+                                                        const int32_t* __restrict__ codes, long long N,
+                                                        int k, int L, uint64_t* __restrict__ out,
+                                                        long long ldk) {
+    __shared__ uint64_t s_key[4][32][33];  // [warp][table][row] (+1 pad)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int groups = (L + 31) / 32;
+    const long long rblocks = (N + 31) / 32;
+    const long long items = rblocks * groups;
+    for (long long it = (long long)blockIdx.x * 4 + warp; it < items; it += (long long)gridDim.x * 4) {
+        const int g = (int)(it % groups);
+        const long long v0 = (it / groups) * 32;
+        const int l = g * 32 + lane;
+        const bool live_l = l < L;
+        uint32_t r0[K], r1[K], r2[K];
+        uint64_t rc = 0;
+        if (live_l) {
+            rc = rmul[(size_t)l * (K + 1)];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const uint64_t r = rmul[(size_t)l * (K + 1) + j + 1];
+                r0[j] = (uint32_t)(r & 0x1fffff);
+                r1[j] = (uint32_t)((r >> 21) & 0x1fffff);
+                r2[j] = (uint32_t)(r >> 42);
+            }
+        }
+        const int rows = (int)min(32LL, N - v0);
+#pragma unroll 4
+        for (int rr = 0; rr < rows; ++rr) {
+            uint64_t key = 0;
+            if (live_l) {
+                const int32_t* c = codes + (v0 + rr) * (long long)k + l * K;
+                uint64_t s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const uint32_t u = (uint32_t)__ldg(c + j);
+                    s0 += (uint64_t)r0[j] * u;
+                    s1 += (uint64_t)r1[j] * u;
+                    s2 += (uint64_t)r2[j] * u;
+                }
+                key = mod61(rc + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
+            }
+            s_key[warp][lane][rr] = key;
+        }
+        __syncwarp();
+        for (int t = 0; t < 32; ++t) {
+            const int lt = g * 32 + t;
+            if (lt < L && lane < rows) out[(long long)lt * ldk + v0 + lane] = s_key[warp][t][lane];
+        }
+        __syncwarp();
+    }
+}
+
+typedef void (*FastKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long);
+FastKeysFn fast_keys_for(int K) {
+    switch (K) {
+#define FASTLSH_KCASE(X) case X: return keys_kernel_fast<X>;
+        FASTLSH_KCASE(1) FASTLSH_KCASE(2) FASTLSH_KCASE(3) FASTLSH_KCASE(4) FASTLSH_KCASE(5) FASTLSH_KCASE(6)
+        FASTLSH_KCASE(7) FASTLSH_KCASE(8) FASTLSH_KCASE(9) FASTLSH_KCASE(10) FASTLSH_KCASE(11) FASTLSH_KCASE(12)
+        FASTLSH_KCASE(13) FASTLSH_KCASE(14) FASTLSH_KCASE(15) FASTLSH_KCASE(16)
+#undef FASTLSH_KCASE
+        default: return nullptr;
+    }
+}
+
 }  // namespace
 
 fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r,
                                  const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
                                  int64_t ldk, cudaStream_t stream) {
     const int L = keys->L, K = keys->K;
+    if (FastKeysFn fk = fast_keys_for(K)) {  // K <= 16: register-resident limbs (above)
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long items = ((N + 31) / 32) * ((L + 31) / 32);
+        long long blocks = (items + 3) / 4;
+        const long long cap = (long long)sms * 16;
+        if (blocks > cap) blocks = cap;
+        fk<<<(unsigned)blocks, 128, 0, stream>>>(dev_r, codes, N, k, L, out, ldk);
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? FASTLSH_OK : set_cuda_error(e);
+    }
     const int TL = L < kTablesPerTile ? L : kTablesPerTile;  // tables per tile
     const size_t smem = (size_t)L * (K + 1) * 8 + (size_t)TL * kKeyRows * 8;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(keys_kernel),
