@@ -339,34 +339,62 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
             int u = 0, h = it;
             while (h >= kb) { h -= kb; ++u; }  // it / kb without a division (it < RG * kb)
             const float bh = s_b[h];
-            {
-                const float4* pb = part + (d * RG + u) * W * 32;
-                float4 s = pb[s_unit[h * P]];
+            const float4* pb = part + (d * RG + u) * W * 32;
+            float4 s;
+            if (P == 2) {  // the common packing: two parts, summed in part order
+                s = pb[s_unit[2 * h]];
+                const float4 v = pb[s_unit[2 * h + 1]];
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            } else {
+                s = pb[s_unit[h * P]];
                 for (int q = 1; q < P; ++q) {
                     const float4 v = pb[s_unit[h * P + q]];
                     s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
                 }
-                const float pr[4] = {s.x, s.y, s.z, s.w};
-                const long long o0 = (row0 + 4 * u) * a.k + h0 + h;
+            }
+            const float pr[4] = {s.x, s.y, s.z, s.w};
+            const long long o0 = (row0 + 4 * u) * a.k + h0 + h;
+            if (a.proj) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (4 * u + r < nrows) a.proj[o0 + (long long)r * a.k] = pr[r];
+                continue;
+            }
+            int code[4];
+            bool bad = false;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
+                const float num = __fadd_rn(pr[r], bh);
+                const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                const float f = floorf(qv);
+                code[r] = (int)f;
+                bad |= !(f > -2147483648.0f && f < 2147483648.0f);
+            }
+            if (bad) {  // rare: sentinel + count (rows past N are not counted)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    if (4 * u + r >= nrows) break;
-                    if (a.proj) {
-                        a.proj[o0 + (long long)r * a.k] = pr[r];
-                        continue;
-                    }
-                    // w a power of two: x * (1/w) is exact, so it equals the IEEE quotient
                     const float num = __fadd_rn(pr[r], bh);
                     const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
                     const float f = floorf(qv);
-                    int code = (int)f;
                     if (!(f > -2147483648.0f && f < 2147483648.0f)) {
-                        code = INT_MIN;
-                        atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                        code[r] = INT_MIN;
+                        if (4 * u + r < nrows) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
                     }
-                    a.codes[o0 + (long long)r * a.k] = code;
-                    if (fused) cb[(4 * u + r) * a.kb_max + h] = code;
                 }
+            }
+            if (4 * u + 4 <= nrows) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a.codes[o0 + (long long)r * a.k] = code[r];
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (4 * u + r < nrows) a.codes[o0 + (long long)r * a.k] = code[r];
+            }
+            if (fused) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (4 * u + r < nrows) cb[(4 * u + r) * a.kb_max + h] = code[r];
             }
         }
         mbar_arrive(PEMPTY(d));

@@ -1,9 +1,8 @@
+# round evidence: bench line, launch list (same command under ncu), ncu --set full of K1 and K3
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/r1_pytest_gpu.log
-timeout 300 python __graft_entry__.py smoke > gpurun_out/r1_smoke.log 2>&1; echo smoke=$?
 timeout 600 python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err; echo bench=$?
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/r1_bench_short.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/r1_ncu_launch.log 2>&1; echo ncu1=$?
 timeout 300 python tools/prof_gather.py --config C1 --rows 262144 --iters 3 --keys > gpurun_out/r1_prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^gather_kernel" -s 1 -c 1 -o gpurun_out/r1_gather_c1 python tools/prof_gather.py --config C1 --rows 262144 --iters 3 --keys > gpurun_out/r1_ncu_full.log 2>&1; echo ncu2=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:^gather_kernel" -s 1 -c 1 -o gpurun_out/r1_gather_c1 python tools/prof_gather.py --config C1 --rows 262144 --iters 3 --keys > gpurun_out/r1_ncu_full.log 2>&1; echo ncu2=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:keys_kernel" -s 1 -c 1 -o gpurun_out/r1_keys_c1 python tools/prof_gather.py --config C1 --rows 262144 --iters 3 --keys > gpurun_out/r1_ncu_keys.log 2>&1; echo ncu3=$?
