@@ -335,9 +335,14 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         int32_t* cb = cbuf + cs * 4 * RG * a.kb_max;
         if (fused && je >= 2) mbar_wait(CEMPTY(cs), (uint32_t)(((je - 2) >> 1) & 1));
         // items (hash, sub-stage) spread over all threads so every warp does an equal share
-        for (int it = tid; it < kb * RG; it += nthreads) {
+        // item it = (sub-stage u, hash h) with a per-sub-stage stride kbp = kb rounded up to 8, so a
+        // quarter-warp takes 8 consecutive hashes, whose parts the packer placed in distinct bank
+        // groups (conflict-free partial reads)
+        const int kbp = (kb + 7) & ~7;
+        for (int it = tid; it < kbp * RG; it += nthreads) {
             int u = 0, h = it;
-            while (h >= kb) { h -= kb; ++u; }  // it / kb without a division (it < RG * kb)
+            while (h >= kbp) { h -= kbp; ++u; }  // it / kbp without a division (it < RG * kbp)
+            if (h >= kb) continue;
             const float bh = s_b[h];
             const float4* pb = part + (d * RG + u) * W * 32;
             float4 s;

@@ -14,6 +14,8 @@
 //     position at which every lane and every bank group is used at most once.
 //  4. Free (lane, position) pairs become padding slots: coefficient 0 reading a zero chunk of a
 //     bank group unused at that position.
+//  5. Lane positions inside a quarter are free for the schedule; they are chosen (König colouring
+//     of quarters x (hash octet, part)) so that the epilogue's partial-sum reads are conflict-free.
 //
 // Everything is deterministic, so every rank derives the identical packing (and hence the
 // identical fp32 summation order) from the same params.
@@ -194,6 +196,46 @@ bool color_quarter(std::vector<Edge>& edges, int nlanes, int ncol) {
     return true;
 }
 
+// König edge colouring of a general bipartite multigraph (left x right nodes) with ncol >= max
+// degree colours. Edge e joins left[e] and right[e]; returns the colour of every edge (-1 = failed).
+std::vector<int> color_bipartite(const std::vector<int>& left, const std::vector<int>& right, int nleft,
+                                 int nright, int ncol) {
+    const int E = (int)left.size();
+    std::vector<int> col(E, -1), lc((size_t)nleft * ncol, -1), rc((size_t)nright * ncol, -1);
+    auto Lc = [&](int v, int t) -> int& { return lc[(size_t)v * ncol + t]; };
+    auto Rc = [&](int v, int t) -> int& { return rc[(size_t)v * ncol + t]; };
+    for (int e = 0; e < E; ++e) {
+        const int l = left[e], r = right[e];
+        int alpha = -1, beta = -1;
+        for (int t = 0; t < ncol && alpha < 0; ++t) if (Lc(l, t) < 0) alpha = t;
+        for (int t = 0; t < ncol && beta < 0; ++t) if (Rc(r, t) < 0) beta = t;
+        if (alpha < 0 || beta < 0) return std::vector<int>(E, -1);
+        if (Rc(r, alpha) >= 0) {  // flip the alpha/beta alternating path starting at r
+            std::vector<int> path;
+            bool at_right = true;
+            int v = r, c = alpha;
+            for (;;) {
+                const int e2 = at_right ? Rc(v, c) : Lc(v, c);
+                if (e2 < 0) break;
+                path.push_back(e2);
+                v = at_right ? left[e2] : right[e2];
+                at_right = !at_right;
+                c = (c == alpha) ? beta : alpha;
+            }
+            for (int e2 : path) { Lc(left[e2], col[e2]) = -1; Rc(right[e2], col[e2]) = -1; }
+            for (int e2 : path) {
+                col[e2] = (col[e2] == alpha) ? beta : alpha;
+                Lc(left[e2], col[e2]) = e2;
+                Rc(right[e2], col[e2]) = e2;
+            }
+        }
+        col[e] = alpha;
+        Lc(l, alpha) = e;
+        Rc(r, alpha) = e;
+    }
+    return col;
+}
+
 struct Trial {
     Packing pk;
     double cost = 1e300;
@@ -285,7 +327,51 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
     int64_t conflicts = 0;
     if (MS > kMaxSlots) MS = kMaxSlots;
     MS = (MS + 1) & ~1;  // the gather loop issues slots in pairs
+    if (const char* e = std::getenv("FASTLSH_MS_CAP")) {  // experiment knob: fold colours beyond a cap
+        const int cap = std::atoi(e) & ~1;
+        if (cap >= dmax && cap < MS) MS = cap;
+    }
     pk.slots = MS;
+
+    // Lane positions inside each quarter are free for the gather schedule (it is per lane). Choose
+    // them so that the epilogue, which reads the partials of 8 consecutive hashes per quarter-warp
+    // (one part at a time), hits 8 distinct bank groups: edge-colour the bipartite multigraph
+    // quarters x (hash octet, part) with 8 colours (degrees <= 8, König) and use the colour as the
+    // position. perm[bl][q][li] = position of member li (free lanes take the unused positions).
+    std::vector<std::vector<std::array<int, 8>>> perm(HB, std::vector<std::array<int, 8>>(Q));
+    for (int bl = 0; bl < HB; ++bl) {
+        const auto& units = block_units[bl];
+        std::vector<int> le, ri;
+        const int octs = (pk.block_kb[bl] + 7) / 8;
+        for (int q = 0; q < Q; ++q)
+            for (int li : plans[bl][q].members) {
+                le.push_back(q);
+                ri.push_back((units[li].hash / 8) * P + units[li].part);
+            }
+        std::vector<int> col = color_bipartite(le, ri, Q, std::max(1, octs * P), 8);
+        size_t e = 0;
+        for (int q = 0; q < Q; ++q) {
+            std::array<int, 8>& pm = perm[bl][q];
+            bool used[8] = {false, false, false, false, false, false, false, false};
+            const int nm = (int)plans[bl][q].members.size();
+            bool ok = true;
+            for (int li = 0; li < nm; ++li, ++e) {
+                pm[li] = col[e];
+                if (col[e] < 0 || used[col[e]]) ok = false;
+                else used[col[e]] = true;
+            }
+            if (!ok) {  // cannot happen (König); keep the identity order
+                for (int li = 0; li < 8; ++li) pm[li] = li;
+                continue;
+            }
+            int nxt = 0;
+            for (int li = nm; li < 8; ++li) {
+                while (used[nxt]) ++nxt;
+                pm[li] = nxt;
+                used[nxt] = true;
+            }
+        }
+    }
 
     const size_t lanes_total = (size_t)HB * Wn * 32;
     pk.offp.assign(lanes_total * MS, 0);
@@ -336,7 +422,7 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
                 }
             }
             for (int l = 0; l < 8; ++l) {
-                const int lane = qi * 8 + l;
+                const int lane = qi * 8 + perm[bl][q][l];
                 const size_t wl = ((size_t)bl * Wn + w);
                 for (int t = 0; t < MS; ++t) {
                     const uint32_t off = (uint32_t)tpos[(size_t)t * 8 + l] * 16u;

@@ -172,3 +172,20 @@ def test_kernel_selection_rules(lib):
     with pytest.raises(fl.FastLSHError):
         Q.set_kernel("tmem")
     assert Q.info()["kernel"] == 1
+
+
+@pytest.mark.parametrize("n,m,k", [(960, 60, 500), (784, 64, 2000), (128, 16, 256), (4096, 32, 1000), (96, 40, 37)])
+def test_epilogue_partial_reads_conflict_free(lib, n, m, k):
+    """The 8 consecutive hashes an epilogue quarter-warp reads have their part-q partials in 8
+    distinct bank groups (lane % 8) for every part q (packer.cpp: König colouring of positions)."""
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import fastlsh_arrays
+    idx, a, b = fastlsh_arrays(n, m, k, 1.0, 2)
+    pk = fl.Params.from_arrays(n, 1.0, idx, a, b).packing()
+    for bl in range(pk["hash_blocks"]):
+        kb = int(pk["block_kb"][bl])
+        ul = pk["unit_lane"][bl, :kb, :].astype(np.int64)
+        for o in range(0, kb, 8):
+            for q in range(pk["parts"]):
+                pos = ul[o:o + 8, q] % 8
+                assert len(set(pos.tolist())) == len(pos), (bl, o, q, pos)

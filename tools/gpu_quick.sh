@@ -1,4 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/q_pytest.log
+cat gpurun_out/q_pytest.log
 timeout 300 python bench.py --steps 10 --no-cpu-baseline --no-dense --e2e-steps 1 > gpurun_out/q.json 2>gpurun_out/q.err; echo bench=$?
 python - <<'PY'
 import json
