@@ -1,0 +1,106 @@
+"""Per-config measurement: K1 (and K1t where it applies) and the dense tcgen05
+E2LSH comparator on every BASELINE.json config, with the north-star roofline fraction
+t_roof / t_kernel, t_roof = max((4Nn + 4Nk)/BW_HBM, N*k*m/G_s). One JSON object per line.
+
+  python tools/measure_configs.py [--out profiles/r01_configs.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2309_15479_b200 as fl  # noqa: E402
+from fastlsh_inputs import configs, data  # noqa: E402
+
+G_S = 148 * 32 * 1.965e9
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+    except Exception:
+        return 6.65e12
+
+
+def timed(fn, iters):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+CASES = [  # name, m override, rows, note
+    ("C0", None, None, "full config (10^4 rows, L2-resident)"),
+    ("C1", None, None, "full config"),
+    ("C2", 32, None, "full config, m sweep"),
+    ("C2", 128, None, "m sweep"),
+    ("C2", 512, 250_000, "m sweep, 250k-row sample"),
+    ("C2", 4096, 20_000, "m = n (i.i.d. sampling), 20k-row sample"),
+    ("C3", None, 25_000_000, "one GPU's shard at G = 8 (2e8 / 8 rows)"),
+    ("C4", None, None, "one streaming batch (1e5 rows)"),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.jsonl"))
+    args = ap.parse_args()
+    bw = hbm_peak()
+    out = open(args.out, "w")
+    for name, m_over, rows, note in CASES:
+        c = configs.get(name)
+        m = m_over or c.m
+        N = rows or c.N
+        P = fl.Params.create(c.n, m, c.k, c.w, seed=c.seed)
+        X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
+        codes = torch.empty((N, c.k), dtype=torch.int32, device="cuda")
+        gathers = N * c.k * m
+        iters = max(3, min(20, int(2e11 / max(gathers, 1))))
+        t_hbm = (4.0 * N * c.n + 4.0 * N * c.k) / bw
+        t_smem = gathers / G_S
+        t_roof = max(t_hbm, t_smem)
+        rec = {"config": name, "m": m, "rows": N, "n": c.n, "k": c.k, "note": note,
+               "t_roof_ms": t_roof * 1e3, "bound": "smem" if t_smem >= t_hbm else "hbm"}
+        info = P.info()
+        rec["packing"] = {kk: info[kk] for kk in ("parts", "slots", "warps_per_block", "hash_blocks",
+                                                  "bank_efficiency")}
+        for kern in ("smem", "tmem"):
+            try:
+                P.set_kernel(kern)
+                ms = timed(lambda: fl.fastlsh_hash(P, X, out=codes), iters)
+                rec[f"K1{'t' if kern == 'tmem' else ''}"] = {
+                    "ms": ms, "hashes_per_s": N * c.k / (ms / 1e3), "roofline_frac": t_roof / (ms / 1e3),
+                    "smem_frac": t_smem / (ms / 1e3)}
+            except fl.FastLSHError as ex:
+                rec[f"K1{'t' if kern == 'tmem' else ''}"] = {"unavailable": str(ex)}
+        P.set_kernel("auto")
+        try:
+            Pd = fl.Params.e2lsh(c.n, c.k, c.w, seed=c.seed)
+            for prec in (3, 1):
+                ms = timed(lambda: fl.e2lsh_hash(Pd, X, out=codes, precision=prec), 3)
+                rec[f"dense_tf32x{prec}"] = {"ms": ms, "hashes_per_s": N * c.k / (ms / 1e3),
+                                             "K1_speedup": ms / rec["K1"]["ms"]}
+            del Pd
+        except fl.FastLSHError as ex:
+            rec["dense"] = {"unavailable": str(ex)}
+        print(json.dumps(rec), flush=True)
+        out.write(json.dumps(rec) + "\n")
+        del X, codes, P
+        torch.cuda.empty_cache()
+    out.close()
+
+
+if __name__ == "__main__":
+    main()
