@@ -140,19 +140,24 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "hashes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in steps),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.name == "C3" else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_dict(cfg, world),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "hashes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def _config_dict(cfg, world):
-    return {"workload": f"{cfg.name}: N={cfg.N} rows/GPU, n={cfg.n}, k={cfg.k}, m={cfg.m}, w={cfg.w}, "
-                        f"keys L={cfg.L} x K={cfg.K}, recipe {cfg.data}",
-            "N_per_gpu": cfg.N, "n": cfg.n, "k": cfg.k, "m": cfg.m, "w": cfg.w, "L": cfg.L, "K": cfg.K,
-            "global_rows": cfg.N * world, "parallelism": f"row-sharded x{world}, params replicated",
-            "l2": f"inputs {cfg.N * cfg.n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
+def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1):
+    n_rank = cfg.N if n_rank is None else n_rank
+    n_total = cfg.N * world if n_total is None else n_total
+    d = {"workload": f"{cfg.name}: N={n_rank} rows/GPU, n={cfg.n}, k={cfg.k}, m={cfg.m}, w={cfg.w}, "
+                     f"keys L={cfg.L} x K={cfg.K}, recipe {cfg.data}",
+         "N_per_gpu": n_rank, "n": cfg.n, "k": cfg.k, "m": cfg.m, "w": cfg.w, "L": cfg.L, "K": cfg.K,
+         "global_rows": n_total, "parallelism": f"row-sharded x{world}, params replicated",
+         "l2": f"inputs {n_rank * cfg.n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
+    if chunks > 1:
+        d["chunks_per_step"] = chunks
+    return d
 
 
 def _traffic_from_profiles(cfg, rows: int):
@@ -183,6 +188,7 @@ def main():
     ap.add_argument("--fused-keys", action="store_true",
                     help="build keys in K1's epilogue (measured slower on C1: 6.80 vs 6.42 ms/step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -210,38 +216,58 @@ def main():
     if Kobj is not None and args.fused_keys:
         P.set_table_size(cfg.K)  # whole tables per CTA: keys are built in K1's epilogue
     info = P.info()
-    N = cfg.N
-    X = data.generate(cfg.data, cfg.n, rank * N, (rank + 1) * N, seed=cfg.seed, device=dev)
-    codes = torch.empty((N, cfg.k), dtype=torch.int32, device=dev)
+    # C3 is a fixed 2e8-row dataset sharded over the ranks (strong scaling) and hashed in chunks:
+    # its codes (204.8 GB) do not fit one GPU, so only a chunk of codes lives at a time while the
+    # keys of all rows are built into [L][N]. Other configs are per-GPU workloads.
+    from paper_2309_15479_b200.distributed import shard_rows
+    strong = cfg.name == "C3"
+    if strong:
+        N_total = cfg.N
+        lo, hi = shard_rows(N_total, world, rank)
+    else:
+        lo, hi = rank * cfg.N, (rank + 1) * cfg.N
+        N_total = world * cfg.N
+    N = hi - lo
+    chunk = min(N, args.chunk_rows) if strong else N
+    bounds = [(c0, min(N, c0 + chunk)) for c0 in range(0, N, chunk)]
+    X = data.generate(cfg.data, cfg.n, lo, hi, seed=cfg.seed, device=dev)
+    codes = torch.empty((chunk, cfg.k), dtype=torch.int32, device=dev)
     keys = torch.empty((cfg.L, N), dtype=torch.int64, device=dev) if Kobj else None
     gathered = torch.empty((cfg.L, world * N), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
     stream = torch.cuda.current_stream()
 
     fused_keys = bool(Kobj) and args.fused_keys
-    launches_per_step = 1 + (1 if (Kobj and not fused_keys) else 0)
+    launches_per_step = len(bounds) * (1 + (1 if (Kobj and not fused_keys) else 0))
     ev = []
 
     def step(record: bool):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
-        if record:
-            e[0].record(stream)
-        if Kobj and args.fused_keys:
-            fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
+        marks = []  # per chunk: (before hash, after hash, after keys)
+        for c0, c1 in bounds:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
             if record:
-                e[1].record(stream)
-        else:
-            fl.fastlsh_hash(P, X, out=codes)
+                e[0].record(stream)
+            cb = codes[:c1 - c0]
+            if Kobj and args.fused_keys and not strong:
+                fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
+                if record:
+                    e[1].record(stream)
+            else:
+                fl.fastlsh_hash(P, X[c0:c1], out=cb)
+                if record:
+                    e[1].record(stream)
+                if Kobj:
+                    fl.build_keys(Kobj, cb, out=keys, col0=c0)
             if record:
-                e[1].record(stream)
-            if Kobj:
-                fl.build_keys(Kobj, codes, out=keys)
+                e[2].record(stream)
+                marks.append(e)
+        ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if record else None
         if record:
-            e[2].record(stream)
+            ea[0].record(stream)
         if gathered is not None:
             allgather_keys(keys, out=gathered)
         if record:
-            e[3].record(stream)
-            ev.append(e)
+            ea[1].record(stream)
+            ev.append((marks, ea))
 
     smi_index = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -269,15 +295,15 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
-    hash_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    keys_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    ag_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    hash_ms = [sum(m[0].elapsed_time(m[1]) for m in marks) for marks, _ in ev]
+    keys_ms = [sum(m[1].elapsed_time(m[2]) for m in marks) for marks, _ in ev]
+    ag_ms = [ea[0].elapsed_time(ea[1]) for _, ea in ev]
     tt = torch.tensor([total_ms, statistics.mean(hash_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_ms_max, hash_ms_max = float(tt[0]), float(tt[1])
     ms_per_step = total_ms_max / args.steps
-    hashes_per_step = world * N * cfg.k
+    hashes_per_step = N_total * cfg.k
     value = hashes_per_step / (ms_per_step / 1e3)
 
     # roofline of the dominant kernel (K1): smem gathers vs the north_star bound
@@ -303,28 +329,32 @@ def main():
     if not args.no_dense:
         Pd = fl.Params.e2lsh(cfg.n, cfg.k, cfg.w, seed=cfg.seed)
         dense = {}
+        Nd = min(N, chunk)  # C3: the comparator runs on one chunk of rows
+        Xd, cd = X[:Nd], codes[:Nd]
         for prec in (3, 1):
-            fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+            fl.e2lsh_hash(Pd, Xd, out=cd, precision=prec)
             d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             d0.record(stream)
             for _ in range(3):
-                fl.e2lsh_hash(Pd, X, out=codes, precision=prec)
+                fl.e2lsh_hash(Pd, Xd, out=cd, precision=prec)
             d1.record(stream)
             torch.cuda.synchronize()
             ms = d0.elapsed_time(d1) / 3
             kpad = (cfg.k + 255) // 256 * 256
-            dense[f"tf32x{prec}"] = {"ms": ms, "hashes_per_s": N * cfg.k / (ms / 1e3),
-                                     "mma_tflops": 2.0 * N * cfg.n * kpad * prec / (ms / 1e3) / 1e12,
-                                     "fastlsh_hash_speedup": ms / statistics.mean(hash_ms)}
+            dense[f"tf32x{prec}"] = {"ms": ms, "rows": Nd, "hashes_per_s": Nd * cfg.k / (ms / 1e3),
+                                     "mma_tflops": 2.0 * Nd * cfg.n * kpad * prec / (ms / 1e3) / 1e12,
+                                     "fastlsh_hash_speedup": (ms / Nd) / (statistics.mean(hash_ms) / N)}
         dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows; tf32x3 is the "
                          "parity-gated comparator (3xTF32), tf32x1 the ungated reference point")
         del Pd
 
     # end to end through the public host-buffer API: H2D of X, hash + keys, D2H of codes + keys
-    Xh = X.cpu().pin_memory()
-    codes_h = torch.empty((N, cfg.k), dtype=torch.int32).pin_memory()
-    keys_h = torch.empty((cfg.L, N), dtype=torch.int64).pin_memory() if Kobj else None
+    # (C3: on a 2M-row sample of each shard; the host would need 307 GB for the whole shard at G=1)
+    Ne = N if not strong else min(N, 2_097_152)
+    Xh = X[:Ne].cpu().pin_memory()
+    codes_h = torch.empty((Ne, cfg.k), dtype=torch.int32).pin_memory()
+    keys_h = torch.empty((cfg.L, Ne), dtype=torch.int64).pin_memory() if Kobj else None
     fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=131072)  # warm (workspace allocation)
     if world > 1:
         dist.barrier()
@@ -335,10 +365,11 @@ def main():
     et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e = {"value": hashes_per_step / float(et[0]), "unit": "hashes/s",
+    e2e = {"value": world * Ne * cfg.k / float(et[0]), "unit": "hashes/s",
            "h2d_bytes_per_step": int(Xh.numel() * 4),
            "d2h_bytes_per_step": int(codes_h.numel() * 4 + (keys_h.numel() * 8 if keys_h is not None else 0)),
-           "api": "fastlsh_hash_host (pinned host buffers, 2-stream chunked pipeline)", "steps": args.e2e_steps}
+           "api": "fastlsh_hash_host (pinned host buffers, 2-stream chunked pipeline)", "steps": args.e2e_steps,
+           "rows_per_gpu": Ne}
     del Xh, codes_h, keys_h
 
     cb = None
@@ -348,9 +379,10 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "hashes/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, resident in HBM)",
-                "config": _config_dict(cfg, world), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "config": _config_dict(cfg, world, N, N_total, len(bounds)), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks,
                 "keys_fused": fused_keys,

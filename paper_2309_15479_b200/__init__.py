@@ -319,16 +319,22 @@ def e2lsh_project(params: Params, X, out=None, precision: int = 3, stream=None):
     return out
 
 
-def build_keys(keys: Keys, codes, out=None, ldk=None, stream=None):
-    """keys[L, N] uint64 (stored in an int64 tensor) from codes[N, k] int32."""
+def build_keys(keys: Keys, codes, out=None, ldk=None, stream=None, col0: int = 0):
+    """keys[L, N] uint64 (stored in an int64 tensor) from codes[N, k] int32.
+
+    With `out` an [L, ldk] tensor and `col0` > 0, the N keys of each table go to columns
+    [col0, col0 + N) (chunked table builds)."""
     import torch
     N, k = codes.shape
-    ldk = N if ldk is None else ldk
     if out is None:
+        ldk = (N + col0) if ldk is None else ldk
         out = torch.empty((keys.L, ldk), dtype=torch.int64, device=codes.device)
-    _check(keys._lib.fastlsh_build_keys(keys._h, _dev_ptr(codes, torch.int32, "codes"), N, k,
-                                        _dev_ptr(out, torch.int64, "keys"), ldk, _stream_ptr(stream)),
-           "fastlsh_build_keys")
+    ldk = out.shape[1]
+    if out.shape[0] != keys.L or col0 < 0 or col0 + N > ldk:
+        raise ValueError("keys output must be [L, ldk] with col0 + N <= ldk")
+    ptr = ctypes.c_void_p(_dev_ptr(out, torch.int64, "keys").value + 8 * col0)
+    _check(keys._lib.fastlsh_build_keys(keys._h, _dev_ptr(codes, torch.int32, "codes"), N, k, ptr, ldk,
+                                        _stream_ptr(stream)), "fastlsh_build_keys")
     return out
 
 

@@ -90,16 +90,21 @@ template <int K>
 __global__ void __launch_bounds__(128) keys_kernel_fast(const uint64_t* __restrict__ rmul,
                                                         const int32_t* __restrict__ codes, long long N,
                                                         int k, int L, uint64_t* __restrict__ out,
-                                                        long long ldk) {
+                                                        long long ldk, int vec) {
     __shared__ uint64_t s_key[4][32][33];  // [warp][table][row] (+1 pad)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int groups = (L + 31) / 32;
+    // TPW tables per warp (lane % TPW), RPW = 32 / TPW rows per iteration (lane / TPW), so that
+    // every lane has work when L < 32
+    const int TPW = L >= 32 ? 32 : (L > 16 ? 32 : L > 8 ? 16 : L > 4 ? 8 : L > 2 ? 4 : L > 1 ? 2 : 1);
+    const int RPW = 32 / TPW;
+    const int tl = lane % TPW, rsub = lane / TPW;
+    const int groups = (L + TPW - 1) / TPW;
     const long long rblocks = (N + 31) / 32;
     const long long items = rblocks * groups;
     for (long long it = (long long)blockIdx.x * 4 + warp; it < items; it += (long long)gridDim.x * 4) {
         const int g = (int)(it % groups);
         const long long v0 = (it / groups) * 32;
-        const int l = g * 32 + lane;
+        const int l = g * TPW + tl;
         const bool live_l = l < L;
         uint32_t r0[K], r1[K], r2[K];
         uint64_t rc = 0;
@@ -115,32 +120,49 @@ __global__ void __launch_bounds__(128) keys_kernel_fast(const uint64_t* __restri
         }
         const int rows = (int)min(32LL, N - v0);
 #pragma unroll 4
-        for (int rr = 0; rr < rows; ++rr) {
+        for (int rb = 0; rb < 32; rb += RPW) {
+            const int rr = rb + rsub;
             uint64_t key = 0;
-            if (live_l) {
+            if (live_l && rr < rows) {
                 const int32_t* c = codes + (v0 + rr) * (long long)k + l * K;
+                uint32_t u[K];
+                if (K % 4 == 0 && vec == 4) {  // 16-byte aligned runs: 128-bit loads
+#pragma unroll
+                    for (int j = 0; j < K; j += 4) {
+                        const int4 q = __ldg(reinterpret_cast<const int4*>(c + j));
+                        u[j] = q.x; u[j + 1] = q.y; u[j + 2] = q.z; u[j + 3] = q.w;
+                    }
+                } else if (K % 2 == 0 && vec >= 2) {  // 8-byte aligned runs: 64-bit loads
+#pragma unroll
+                    for (int j = 0; j < K; j += 2) {
+                        const int2 q = __ldg(reinterpret_cast<const int2*>(c + j));
+                        u[j] = q.x; u[j + 1] = q.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < K; ++j) u[j] = (uint32_t)__ldg(c + j);
+                }
                 uint64_t s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
-                    const uint32_t u = (uint32_t)__ldg(c + j);
-                    s0 += (uint64_t)r0[j] * u;
-                    s1 += (uint64_t)r1[j] * u;
-                    s2 += (uint64_t)r2[j] * u;
+                    s0 += (uint64_t)r0[j] * u[j];
+                    s1 += (uint64_t)r1[j] * u[j];
+                    s2 += (uint64_t)r2[j] * u[j];
                 }
                 key = mod61(rc + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
             }
-            s_key[warp][lane][rr] = key;
+            s_key[warp][tl][rr] = key;
         }
         __syncwarp();
-        for (int t = 0; t < 32; ++t) {
-            const int lt = g * 32 + t;
+        for (int t = 0; t < TPW; ++t) {
+            const int lt = g * TPW + t;
             if (lt < L && lane < rows) out[(long long)lt * ldk + v0 + lane] = s_key[warp][t][lane];
         }
         __syncwarp();
     }
 }
 
-typedef void (*FastKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long);
+typedef void (*FastKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long, int);
 FastKeysFn fast_keys_for(int K) {
     switch (K) {
 #define FASTLSH_KCASE(X) case X: return keys_kernel_fast<X>;
@@ -166,7 +188,11 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
         long long blocks = (items + 3) / 4;
         const long long cap = (long long)sms * 16;
         if (blocks > cap) blocks = cap;
-        fk<<<(unsigned)blocks, 128, 0, stream>>>(dev_r, codes, N, k, L, out, ldk);
+        // vector width of the per-(row, table) code runs: 4 when every run is 16-byte aligned,
+        // 2 when 8-byte aligned, else 1
+        const uintptr_t base = reinterpret_cast<uintptr_t>(codes);
+        const int vec = (k % 4 == 0 && K % 4 == 0 && base % 16 == 0) ? 4 : (k % 2 == 0 && K % 2 == 0 && base % 8 == 0) ? 2 : 1;
+        fk<<<(unsigned)blocks, 128, 0, stream>>>(dev_r, codes, N, k, L, out, ldk, vec);
         cudaError_t e = cudaGetLastError();
         return e == cudaSuccess ? FASTLSH_OK : set_cuda_error(e);
     }

@@ -290,3 +290,20 @@ def test_tmem_kernel_determinism_and_flags():
     assert (codes[5] == -(2 ** 31)).all()
     nf, sat = fl.read_flags(P, reset=True)
     assert nf == c.k and sat == 0
+
+
+def test_chunked_key_build_equals_whole():
+    """Keys built chunk by chunk into columns [c0, c1) of one [L][N] table (the C3 bench path)."""
+    c = configs.get("C3")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1)
+    X = data.generate(c.data, c.n, 0, 10_007, seed=1, device="cuda")
+    whole = fl.build_keys(Kobj, fl.fastlsh_hash(P, X))
+    keys = torch.empty_like(whole)
+    codes = torch.empty((4096, c.k), dtype=torch.int32, device="cuda")
+    for c0 in range(0, 10_007, 4096):
+        c1 = min(10_007, c0 + 4096)
+        cb = codes[:c1 - c0]
+        fl.fastlsh_hash(P, X[c0:c1], out=cb)
+        fl.build_keys(Kobj, cb, out=keys, col0=c0)
+    assert torch.equal(keys, whole)
