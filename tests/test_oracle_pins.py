@@ -301,3 +301,36 @@ def _case(N, n, m, k, w, seed):
     X = rng.standard_normal((N, n)).astype(np.float32)
     idx, a, b = fastlsh_arrays(n, m, k, w, seed)
     return X, idx, a, b
+
+
+# ---- bucket tables (§3.2; reading R15) ----------------------------------------
+
+def test_tables_oracle_matches_brute_grouping():
+    """build_tables (library sort) == a pure-Python dictionary grouping of (key, id) per table."""
+    from oracle import tables
+    rng = np.random.default_rng(5)
+    L, N = 4, 600
+    keys = rng.integers(0, 40, size=(L, N), dtype=np.uint64)  # many collisions
+    keys[1] = rng.integers(0, 2 ** 61 - 1, size=N, dtype=np.uint64)  # (almost) all distinct
+    keys[2, :] = 7  # one bucket
+    sk, si, starts = tables.build_tables(keys)
+    for l in range(L):
+        ref = tables.buckets_brute(keys[l])
+        got = {}
+        bounds = list(starts[l]) + [N]
+        for b in range(len(starts[l])):
+            s, e = bounds[b], bounds[b + 1]
+            assert (sk[l][s:e] == sk[l][s]).all()
+            got[int(sk[l][s])] = [int(x) for x in si[l][s:e]]
+        assert got == ref
+        assert list(got.keys()) == sorted(ref.keys())  # buckets in ascending key order
+        assert sorted(si[l].tolist()) == list(range(N))  # a permutation of the rows
+
+
+def test_tables_oracle_hand_example():
+    """Hand-written table: keys (5, 3, 5, 9, 3) -> buckets {3: [1, 4], 5: [0, 2], 9: [3]}."""
+    from oracle import tables
+    sk, si, starts = tables.build_tables(np.array([[5, 3, 5, 9, 3]], dtype=np.uint64))
+    assert sk[0].tolist() == [3, 3, 5, 5, 9]
+    assert si[0].tolist() == [1, 4, 0, 2, 3]
+    assert starts[0].tolist() == [0, 2, 4]
