@@ -189,6 +189,7 @@ def main():
                     help="build keys in K1's epilogue (measured slower on C1: 6.80 vs 6.42 ms/step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
+    ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -324,6 +325,33 @@ def main():
                 "peak_source": peaks["source"] + f"; smem peak = 148 SM x 32 x {peaks['sm_max_mhz']:.0f} MHz",
                 "kernel_share_of_step": statistics.mean(hash_ms) / ms_per_step if ms_per_step else None}
 
+    # bucket tables of this rank's keys: stable radix sort of
+    # (key, id) per table + bucket starts — timed separately, not part of the hashing step
+    tables = None
+    if Kobj is not None and not args.no_tables:
+        ws = None
+        out_t = None
+        try:
+            out_t = fl.build_tables(keys)
+            need = out_t  # allocate once, then time re-builds into the same buffers
+            t_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            t_ev[0].record(stream)
+            for _ in range(3):
+                fl.build_tables(keys, out=out_t, workspace=ws)
+            t_ev[1].record(stream)
+            torch.cuda.synchronize()
+            tms = t_ev[0].elapsed_time(t_ev[1]) / 3
+            entries = cfg.L * N
+            tables = {"ms": tms, "entries": entries, "entries_per_s": entries / (tms / 1e3),
+                      "buckets_table0": int(out_t[3][0].item()),
+                      "hbm_bytes_algorithmic": entries * (8 * 8 + 8 * 24 + 8 + 4),
+                      "note": "8 LSD radix passes (hist 8 B + scatter 12 B in / 12 B out per entry) + bucket starts"}
+            tables["hbm_frac"] = tables["hbm_bytes_algorithmic"] / (tms / 1e3) / (_peaks()["hbm_gbs"] * 1e9)
+            del out_t, need
+        except Exception as ex:  # noqa: BLE001 (report, never hide a failure)
+            tables = {"error": str(ex)}
+
     # on-box comparator: the dense E2LSH GEMM (tcgen05, m = n) on the same rows, k and w
     dense = None
     if not args.no_dense:
@@ -389,7 +417,7 @@ def main():
                 "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},
-                "dense_e2lsh": dense,
+                "dense_e2lsh": dense, "tables": tables,
                 "packing": {k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
                                                  "bank_efficiency", "conflict_wavefronts")}}
         print(json.dumps(line))

@@ -170,6 +170,24 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ke
                                  const float* X, int64_t N, int32_t* codes, uint64_t* keys_out,
                                  int64_t ldk, fastlsh_stream_t stream);
 
+/* ---- bucket tables (§3.2; reading R15) ------------ */
+
+/* Table l is the multiset of pairs (key_l(v), v), v < N, built in canonical bulk form:
+ *   sorted_keys[l*N + j]  keys of table l in ascending unsigned order (device u64 [L][N]),
+ *   ids[l*N + j]          row id of entry j; equal keys (one bucket) in ascending id (u32 [L][N]),
+ *   bucket_start[l*(N+1) + b]  first entry of bucket b for b < nbuckets[l], then N for the rest
+ *                              of the row ([L][N+1] u32),
+ *   nbuckets[l]           number of distinct keys of table l (device i64 [L]).
+ * keys: device u64 [L][ldk] (e.g. fastlsh_build_keys output), ldk >= N. A stable LSD radix sort
+ * (8 passes of 8 bits over the 61-bit keys) per table, then bucket starts. `workspace` is a device
+ * buffer of >= fastlsh_tables_workspace(L, N) bytes (16-byte aligned), owned by the caller.
+ * EINVAL on bad sizes/pointers (N must be < 2^32 - 1); asynchronous on `stream`. */
+fastlsh_status fastlsh_tables_workspace(int32_t L, int64_t N, size_t* bytes);
+fastlsh_status fastlsh_build_tables(const uint64_t* keys, int32_t L, int64_t N, int64_t ldk,
+                                    uint64_t* sorted_keys, uint32_t* ids, uint32_t* bucket_start,
+                                    int64_t* nbuckets, void* workspace, size_t workspace_bytes,
+                                    fastlsh_stream_t stream);
+
 /* ---- host-buffer entry point (end-to-end; SURVEY.md §3 "config 4 streaming") ----------------- */
 
 /* Hash HOST rows: X_host f32[N*n] (pinned or pageable), codes_host int32[N*k], keys_host

@@ -22,7 +22,7 @@ EXPORTED = [
     "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
-    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_host", "fastlsh_read_flags",
+    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables", "fastlsh_hash_host", "fastlsh_read_flags",
     "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
 ]
 
@@ -79,6 +79,8 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_keys_export": [P, P],
         "fastlsh_build_keys": [P, P, i64, i32, P, i64, P],
         "fastlsh_hash_keys": [P, P, P, i64, P, P, i64, P],
+        "fastlsh_tables_workspace": [i32, i64, ctypes.POINTER(ctypes.c_size_t)],
+        "fastlsh_build_tables": [P, i32, i64, i64, P, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_hash_host": [P, P, P, i64, P, P, i64],
         "fastlsh_read_flags": [P, P, P, i32, P],
     }
@@ -336,6 +338,33 @@ def build_keys(keys: Keys, codes, out=None, ldk=None, stream=None, col0: int = 0
     _check(keys._lib.fastlsh_build_keys(keys._h, _dev_ptr(codes, torch.int32, "codes"), N, k, ptr, ldk,
                                         _stream_ptr(stream)), "fastlsh_build_keys")
     return out
+
+
+def build_tables(keys, N=None, out=None, workspace=None, stream=None):
+    """Bucket tables from keys [L, ldk] (int64 view of u64), rows [0, N).
+
+    Returns (sorted_keys int64 [L, N], ids int32 [L, N] (u32 bit patterns), bucket_start int32
+    [L, N+1], nbuckets int64 [L]); see fastlsh_build_tables."""
+    import torch
+    lib = load_library()
+    L, ldk = keys.shape
+    N = ldk if N is None else N
+    dev = keys.device
+    if out is None:
+        out = (torch.empty((L, N), dtype=torch.int64, device=dev), torch.empty((L, N), dtype=torch.int32, device=dev),
+               torch.empty((L, N + 1), dtype=torch.int32, device=dev), torch.empty((L,), dtype=torch.int64, device=dev))
+    sk, ids, starts, nb = out
+    need = ctypes.c_size_t()
+    _check(lib.fastlsh_tables_workspace(L, N, ctypes.byref(need)), "fastlsh_tables_workspace")
+    if workspace is None or workspace.numel() < need.value:
+        workspace = torch.empty((max(1, need.value),), dtype=torch.uint8, device=dev)
+    _check(lib.fastlsh_build_tables(_dev_ptr(keys, torch.int64, "keys"), L, N, ldk,
+                                    _dev_ptr(sk, torch.int64, "sorted_keys") if N else None,
+                                    _dev_ptr(ids, torch.int32, "ids") if N else None,
+                                    _dev_ptr(starts, torch.int32, "bucket_start"), _dev_ptr(nb, torch.int64, "nbuckets"),
+                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_ptr(stream)),
+           "fastlsh_build_tables")
+    return sk, ids, starts, nb
 
 
 def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None):

@@ -474,6 +474,39 @@ fastlsh_status fastlsh_build_keys(const fastlsh_keys* ks, const int32_t* codes, 
     return launch_build_keys(ks, dr, codes, N, k, keys_out, ldk, reinterpret_cast<cudaStream_t>(stream));
 }
 
+fastlsh_status fastlsh_tables_workspace(int32_t L, int64_t N, size_t* bytes) {
+    if (L < 1 || N < 0 || N >= 0xffffffffLL || !bytes) return FASTLSH_EINVAL;
+    *bytes = tables_workspace_bytes(L, N);
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_build_tables(const uint64_t* keys, int32_t L, int64_t N, int64_t ldk,
+                                    uint64_t* sorted_keys, uint32_t* ids, uint32_t* bucket_start,
+                                    int64_t* nbuckets, void* workspace, size_t workspace_bytes,
+                                    fastlsh_stream_t stream) {
+    if (L < 1 || N < 0 || N >= 0xffffffffLL || ldk < N) return FASTLSH_EINVAL;
+    if (!bucket_start || !nbuckets || (reinterpret_cast<uintptr_t>(nbuckets) & 7) ||
+        (reinterpret_cast<uintptr_t>(bucket_start) & 3))
+        return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    st = check_sm100(dev);
+    if (st != FASTLSH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (N == 0) {  // empty tables: no buckets, bucket_start[l][0] = 0
+        FL_CUDA(cudaMemsetAsync(nbuckets, 0, (size_t)L * sizeof(int64_t), s));
+        FL_CUDA(cudaMemsetAsync(bucket_start, 0, (size_t)L * sizeof(uint32_t), s));
+        return FASTLSH_OK;
+    }
+    if (!keys || !sorted_keys || !ids || !workspace || workspace_bytes < tables_workspace_bytes(L, N) ||
+        (reinterpret_cast<uintptr_t>(keys) & 7) || (reinterpret_cast<uintptr_t>(sorted_keys) & 7) ||
+        (reinterpret_cast<uintptr_t>(ids) & 3) || (reinterpret_cast<uintptr_t>(workspace) & 15))
+        return FASTLSH_EINVAL;
+    return launch_build_tables(keys, L, N, ldk, sorted_keys, ids, bucket_start,
+                               reinterpret_cast<long long*>(nbuckets), workspace, s);
+}
+
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
                                  int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
                                  fastlsh_stream_t stream) {

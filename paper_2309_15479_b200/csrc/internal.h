@@ -148,6 +148,11 @@ fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const f
 fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r,
                                  const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
                                  int64_t ldk, cudaStream_t stream);
+// tables.cu
+size_t tables_workspace_bytes(int L, long long N);
+fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, long long ldk, uint64_t* sorted_keys,
+                                   uint32_t* ids, uint32_t* starts, long long* nbuckets, void* ws,
+                                   cudaStream_t stream);
 // e2lsh_tcgen05.cu
 fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N,
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);

@@ -307,3 +307,45 @@ def test_chunked_key_build_equals_whole():
         fl.fastlsh_hash(P, X[c0:c1], out=cb)
         fl.build_keys(Kobj, cb, out=keys, col0=c0)
     assert torch.equal(keys, whole)
+
+
+# ---- bucket tables (R15): bit-exact vs the oracle --------------------------
+
+def _check_tables(keys_np, sk, ids, starts, nb):
+    from oracle import tables as otables
+    L, N = keys_np.shape
+    rsk, rsi, rst = otables.build_tables(keys_np)
+    assert np.array_equal(sk.cpu().numpy().view(np.uint64), rsk)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), rsi)
+    nbh = nb.cpu().numpy()
+    st = starts.cpu().numpy().view(np.uint32)
+    for l in range(L):
+        assert nbh[l] == len(rst[l])
+        assert np.array_equal(st[l, :nbh[l]].astype(np.int64), rst[l])
+        assert (st[l, nbh[l]:] == N).all()
+
+
+@pytest.mark.parametrize("L,N,hi", [(3, 10_000, 50), (2, 4096, 2 ** 61 - 1), (5, 4097, 3), (1, 1, 9), (4, 77_777, 1000),
+                                    (2, 300_001, 2 ** 61 - 1)])
+def test_tables_bit_exact(L, N, hi):
+    rng = np.random.default_rng(L * 1000 + N)
+    keys_np = rng.integers(0, hi, size=(L, N), dtype=np.uint64)
+    keys = torch.as_tensor(keys_np.view(np.int64)).cuda()
+    _check_tables(keys_np, *fl.build_tables(keys))
+
+
+def test_tables_from_hashed_keys_and_ldk():
+    """Tables from real C1 keys (the bench path), keys read with ldk > N."""
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1)
+    X = data.generate(c.data, c.n, 0, 20_000, seed=1, device="cuda")
+    keys = fl.build_keys(Kobj, fl.fastlsh_hash(P, X), ldk=20_011)
+    keys_np = keys[:, :20_000].cpu().numpy().view(np.uint64)
+    _check_tables(keys_np, *fl.build_tables(keys, N=20_000))
+
+
+def test_tables_empty():
+    keys = torch.zeros((3, 0), dtype=torch.int64, device="cuda")
+    sk, ids, starts, nb = fl.build_tables(keys)
+    assert nb.cpu().tolist() == [0, 0, 0] and starts.cpu().numpy()[:, 0].tolist() == [0, 0, 0]
