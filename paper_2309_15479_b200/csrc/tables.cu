@@ -9,9 +9,11 @@
 //               equal digits with __match_any_sync and keep warp-private running counts; warps'
 //               counts are prefixed in shared memory, so the order of equal digits is the input
 //               order (stability, which makes the row id the tie-break).
-// Then one CTA per table marks bucket starts (key differs from its predecessor) and compacts
-// their positions with a block scan. Bound: HBM (per pass each element is read twice and written
-// once: 8 B key + 4 B id).
+//               The tile is reordered by digit in shared memory first, so global writes are
+//               contiguous runs per digit.
+// Then bucket starts (key differs from its predecessor): per-tile flag counts, a per-table scan
+// over tiles, and per-tile block-scanned writes. Bound: HBM (per pass each element is read twice
+// and written once: 8 B key + 4 B id).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,12 +48,10 @@ __global__ void __launch_bounds__(256) radix_hist(const uint64_t* __restrict__ k
     for (int d = threadIdx.x; d < kBins; d += blockDim.x) hl[(size_t)d * T + t] = h[d];
 }
 
-// in-place exclusive scan of hist[l][*][*] (digit-major) for every table: one CTA per table
-__global__ void __launch_bounds__(1024) radix_scan(uint32_t* __restrict__ hist, int T) {
+// in-place exclusive scan of `per_table` consecutive values per table: one CTA per table
+__device__ __forceinline__ void scan_rows(uint32_t* __restrict__ hl, long long total) {
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t carry;
-    uint32_t* hl = hist + (size_t)blockIdx.x * kBins * T;
-    const long long total = (long long)kBins * T;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -84,113 +84,211 @@ __global__ void __launch_bounds__(1024) radix_scan(uint32_t* __restrict__ hist, 
     }
 }
 
-// stable scatter of one tile; ids_in == nullptr means ids are the row indices (first pass)
-__global__ void __launch_bounds__(kSortWarps * 32) radix_scatter(const uint64_t* __restrict__ keys_in, long long ldk_in,
+// hist[l][*][*] (digit-major, kBins * T values per table)
+__global__ void __launch_bounds__(1024) radix_scan(uint32_t* __restrict__ hist, int T) {
+    scan_rows(hist + (size_t)blockIdx.x * kBins * T, (long long)kBins * T);
+}
+
+// cnt[l][*] (T values per table)
+__global__ void __launch_bounds__(1024) radix_scan_rows(uint32_t* __restrict__ cnt, int T) {
+    scan_rows(cnt + (size_t)blockIdx.x * T, (long long)T);
+}
+
+// stable scatter of one tile; ids_in == nullptr means ids are the row indices (first pass).
+// The tile is first reordered by digit in shared memory (stable), then written out so that
+// consecutive threads write consecutive entries of each digit's run (coalesced stores).
+__global__ void __launch_bounds__(kSortWarps * 32, 3) radix_scatter(const uint64_t* __restrict__ keys_in, long long ldk_in,
                                                                const uint32_t* __restrict__ ids_in,
                                                                uint64_t* __restrict__ keys_out,
                                                                uint32_t* __restrict__ ids_out, long long N, int T,
                                                                int shift, const uint32_t* __restrict__ offs) {
     __shared__ uint32_t wcnt[kSortWarps][kBins];
+    __shared__ uint32_t dstart[kBins];  // tile-local first position of each digit
+    __shared__ uint32_t gbase[kBins];   // global position of the digit's first element of this tile
+    extern __shared__ __align__(16) unsigned char tile_smem[];  // dynamic: the tile in digit order
+    uint64_t* sk = reinterpret_cast<uint64_t*>(tile_smem);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + kTile);
     const int l = blockIdx.y, t = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kBins; i += blockDim.x) (&wcnt[0][0])[i] = 0;
     __syncthreads();
     const uint64_t* kl = keys_in + (long long)l * ldk_in;
     const uint32_t* il = ids_in ? ids_in + (long long)l * N : nullptr;
-    const long long w0 = (long long)t * kTile + (long long)warp * kItems * 32;
+    const long long tile0 = (long long)t * kTile;
+    const long long w0 = tile0 + (long long)warp * kItems * 32;
     uint64_t k[kItems];
     uint32_t id[kItems], loc[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {  // all loads first: kItems independent loads in flight
+        const long long e = w0 + r * 32 + lane;
+        const bool live = e < N;
+        k[r] = live ? __ldg(kl + e) : 0ull;
+        id[r] = live ? (il ? __ldg(il + e) : (uint32_t)e) : 0u;
+    }
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const long long e = w0 + r * 32 + lane;
         const bool live = e < N;
-        k[r] = live ? kl[e] : 0ull;
-        id[r] = live ? (il ? il[e] : (uint32_t)e) : 0u;
         const uint32_t d = digit_of(k[r], shift);
-        // dead lanes (past N) are the last ones of the tile, after every live element: their
-        // digit ranks do not disturb live ones; they are masked out of the counts below
+        // dead lanes (past N) are the tile's last elements: masked out of every count
         const unsigned live_mask = __ballot_sync(0xffffffffu, live);
         const unsigned peers = __match_any_sync(0xffffffffu, live ? d : 0xffffffffu) & live_mask;
-        const uint32_t before = wcnt[warp][d & (kBins - 1)];
+        const uint32_t before = wcnt[warp][d];
         __syncwarp();
         loc[r] = before + __popc(peers & ((1u << lane) - 1u));
         if (live && (peers & ((1u << lane) - 1u)) == 0) wcnt[warp][d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    // exclusive prefix over warps, per digit
-    for (int d = threadIdx.x; d < kBins; d += blockDim.x) {
-        uint32_t s = 0;
+    // per digit: exclusive prefix over warps, and the tile total
+    uint32_t total = 0;
+    const int d_mine = threadIdx.x;  // blockDim.x == kBins
+    {
+        uint32_t sacc = 0;
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t c = wcnt[w][d];
-            wcnt[w][d] = s;
-            s += c;
+            const uint32_t c = wcnt[w][d_mine];
+            wcnt[w][d_mine] = sacc;
+            sacc += c;
         }
+        total = sacc;
     }
-    __syncthreads();
-    const uint32_t* ol = offs + (size_t)l * kBins * T;
-    uint64_t* ko = keys_out + (long long)l * N;
-    uint32_t* io = ids_out + (long long)l * N;
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const long long e = w0 + r * 32 + lane;
-        if (e >= N) continue;
-        const uint32_t d = digit_of(k[r], shift);
-        const uint32_t pos = ol[(size_t)d * T + t] + wcnt[warp][d] + loc[r];
-        ko[pos] = k[r];
-        io[pos] = id[r];
-    }
-}
-
-// bucket starts of every table: positions j with j == 0 or key[j] != key[j-1], then N
-__global__ void __launch_bounds__(1024) bucket_starts(const uint64_t* __restrict__ sk, long long N,
-                                                     uint32_t* __restrict__ starts, long long* __restrict__ nbuckets) {
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry;
-    const int l = blockIdx.x;
-    const uint64_t* kl = sk + (long long)l * N;
-    uint32_t* sl = starts + (long long)l * (N + 1);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (long long base = 0; base < N; base += blockDim.x) {
-        const long long j = base + threadIdx.x;
-        const uint32_t f = (j < N && (j == 0 || kl[j] != kl[j - 1])) ? 1u : 0u;
-        uint32_t x = f;
+    // exclusive scan of the digit totals across the block (256 threads = 8 warps)
+    {
+        __shared__ uint32_t wsum[kSortWarps];
+        uint32_t x = total;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        if (lane == 31) warp_sums[warp] = x;
+        if (lane == 31) wsum[warp] = x;
         __syncthreads();
-        if (warp == 0) {
-            uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sums[lane] = s;
-        }
-        __syncthreads();
-        const uint32_t idx = carry + (warp ? warp_sums[warp - 1] : 0u) + x - f;
-        if (f) sl[idx] = (uint32_t)j;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = idx + f;
-        __syncthreads();
+        uint32_t base = 0;
+        for (int w = 0; w < warp; ++w) base += wsum[w];
+        dstart[d_mine] = base + x - total;
+        gbase[d_mine] = offs[((size_t)l * kBins + d_mine) * T + t] - (base + x - total);
     }
-    const uint32_t nb = carry;
-    for (long long j = nb + threadIdx.x; j <= N; j += blockDim.x) sl[j] = (uint32_t)N;  // sentinel + fill
-    if (threadIdx.x == 0) nbuckets[l] = nb;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const long long e = w0 + r * 32 + lane;
+        if (e >= N) continue;
+        const uint32_t d = digit_of(k[r], shift);
+        const uint32_t p = dstart[d] + wcnt[warp][d] + loc[r];
+        sk[p] = k[r];
+        si[p] = id[r];
+    }
+    __syncthreads();
+    const int live_n = (int)min((long long)kTile, N - tile0);
+    uint64_t* ko = keys_out + (long long)l * N;
+    uint32_t* io = ids_out + (long long)l * N;
+    for (int j = threadIdx.x; j < live_n; j += blockDim.x) {
+        const uint64_t kk = sk[j];
+        const uint32_t pos = gbase[digit_of(kk, shift)] + (uint32_t)j;
+        ko[pos] = kk;
+        io[pos] = si[j];
+    }
+}
+
+// bucket starts of every table: positions j with j == 0 or key[j] != key[j-1], then N.
+// (1) per-tile flag counts, (2) per-table exclusive scan over tiles (radix_scan with one "bin"),
+// (3) per tile: block scan of the flags, positions written at the tile's offset.
+__device__ __forceinline__ uint32_t is_start(const uint64_t* kl, long long j) {
+    return (j == 0 || kl[j] != kl[j - 1]) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256) bucket_count(const uint64_t* __restrict__ sk, long long N, int T,
+                                                   uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t tot;
+    const int l = blockIdx.y, t = blockIdx.x;
+    const uint64_t* kl = sk + (long long)l * N;
+    if (threadIdx.x == 0) tot = 0;
+    __syncthreads();
+    uint32_t c = 0;
+    const long long e0 = (long long)t * kTile, e1 = min(N, e0 + kTile);
+    for (long long j = e0 + threadIdx.x; j < e1; j += blockDim.x) c += is_start(kl, j);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[(size_t)l * T + t] = tot;
+}
+
+__global__ void __launch_bounds__(256) bucket_write(const uint64_t* __restrict__ sk, long long N, int T,
+                                                   const uint32_t* __restrict__ cnt_scanned,
+                                                   const uint32_t* __restrict__ cnt_raw,
+                                                   uint32_t* __restrict__ starts, long long* __restrict__ nbuckets) {
+    __shared__ uint32_t wsum[8];
+    const int l = blockIdx.y, t = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t* kl = sk + (long long)l * N;
+    uint32_t* sl = starts + (long long)l * (N + 1);
+    __shared__ uint64_t tk[kTile + 1];  // tk[0] = key before the tile
+    const long long e0 = (long long)t * kTile;
+    uint32_t base = cnt_scanned[(size_t)l * T + t];
+    for (int i = threadIdx.x; i <= kTile; i += blockDim.x) {
+        const long long j = e0 - 1 + i;
+        tk[i] = (j >= 0 && j < N) ? kl[j] : 0ull;
+    }
+    __syncthreads();
+    // flags with a coalesced mapping (thread i: entries i, i + 256, ...) into bytes, then each
+    // thread takes 16 consecutive flags with one 16-byte load: local count, block scan, write
+    __shared__ __align__(16) uint8_t tf[kTile];
+    for (int i = threadIdx.x; i < kTile; i += blockDim.x) {
+        const long long j = e0 + i;
+        tf[i] = (j < N && (j == 0 || tk[i + 1] != tk[i])) ? 1 : 0;
+    }
+    __syncthreads();
+    const long long j0 = e0 + (long long)threadIdx.x * (kTile / 256);
+    const uint4 fw = reinterpret_cast<const uint4*>(tf)[threadIdx.x];
+    const uint32_t fwords[4] = {fw.x, fw.y, fw.z, fw.w};
+    uint32_t f[kTile / 256], c = 0;
+#pragma unroll
+    for (int i = 0; i < kTile / 256; ++i) {
+        f[i] = (fwords[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        c += f[i];
+    }
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t local = 0;  // this thread's first slot inside the tile's run of bucket starts
+    for (int w = 0; w < warp; ++w) local += wsum[w];
+    local += x - c;
+    uint32_t tile_n = 0;
+    for (int w = 0; w < 8; ++w) tile_n += wsum[w];
+    // positions go to shared memory first (tk is free again), then out with coalesced stores
+    __syncthreads();
+    uint32_t* tpos = reinterpret_cast<uint32_t*>(tk);
+#pragma unroll
+    for (int i = 0; i < kTile / 256; ++i)
+        if (f[i]) tpos[local++] = (uint32_t)(j0 + i);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tile_n; i += blockDim.x) sl[base + i] = tpos[i];
+    if (t == T - 1 && threadIdx.x == 0) {
+        const uint32_t nb = cnt_scanned[(size_t)l * T + t] + cnt_raw[(size_t)l * T + t];
+        nbuckets[l] = nb;
+    }
+}
+
+// bucket_start[l][nb .. N] = N (sentinel and fill)
+__global__ void bucket_fill(long long N, uint32_t* __restrict__ starts, const long long* __restrict__ nbuckets) {
+    const int l = blockIdx.y;
+    const long long nb = nbuckets[l];
+    uint32_t* sl = starts + (long long)l * (N + 1);
+    for (long long j = nb + (long long)blockIdx.x * blockDim.x + threadIdx.x; j <= N; j += (long long)gridDim.x * blockDim.x)
+        sl[j] = (uint32_t)N;
 }
 
 }  // namespace
 
 size_t tables_workspace_bytes(int L, long long N) {
     const long long T = (N + kTile - 1) / kTile;
-    return (size_t)L * N * 12 + (size_t)L * kBins * T * 4 + 256;
+    return (size_t)L * N * 12 + (size_t)L * kBins * T * 4 + (size_t)2 * L * T * 4 + 512;
 }
 
 fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, long long ldk, uint64_t* sorted_keys,
@@ -204,6 +302,9 @@ fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, lon
     hp = (hp + 255) & ~(uintptr_t)255;
     uint32_t* hist = reinterpret_cast<uint32_t*>(hp);
     const dim3 grid(T, L);
+    cudaError_t ae = cudaFuncSetAttribute(reinterpret_cast<const void*>(radix_scatter),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * 12);
+    if (ae != cudaSuccess) return set_cuda_error(ae);
     for (int p = 0; p < kPasses; ++p) {
         const int shift = p * kRadixBits;
         // pass 0 reads the caller's keys (ids = row indices); then ping-pong so the last pass
@@ -215,9 +316,15 @@ fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, lon
         uint32_t* iout = p % 2 ? ids : alt_i;
         radix_hist<<<grid, 256, 0, stream>>>(kin, ldin, N, T, shift, hist);
         radix_scan<<<L, 1024, 0, stream>>>(hist, T);
-        radix_scatter<<<grid, kSortWarps * 32, 0, stream>>>(kin, ldin, iin, kout, iout, N, T, shift, hist);
+        radix_scatter<<<grid, kSortWarps * 32, kTile * 12, stream>>>(kin, ldin, iin, kout, iout, N, T, shift, hist);
     }
-    bucket_starts<<<L, 1024, 0, stream>>>(sorted_keys, N, starts, nbuckets);
+    uint32_t* cnt = hist + (size_t)L * kBins * T;     // [L][T] flag counts (scanned in place)
+    uint32_t* cnt_raw = cnt + (size_t)L * T;           // [L][T] copy before the scan
+    bucket_count<<<grid, 256, 0, stream>>>(sorted_keys, N, T, cnt);
+    cudaMemcpyAsync(cnt_raw, cnt, (size_t)L * T * 4, cudaMemcpyDeviceToDevice, stream);
+    radix_scan_rows<<<L, 1024, 0, stream>>>(cnt, T);
+    bucket_write<<<grid, 256, 0, stream>>>(sorted_keys, N, T, cnt, cnt_raw, starts, nbuckets);
+    bucket_fill<<<dim3(64, L), 256, 0, stream>>>(N, starts, nbuckets);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FASTLSH_OK : set_cuda_error(e);
 }
