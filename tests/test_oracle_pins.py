@@ -334,3 +334,42 @@ def test_tables_oracle_hand_example():
     assert sk[0].tolist() == [3, 3, 5, 5, 9]
     assert si[0].tolist() == [1, 4, 0, 2, 3]
     assert starts[0].tolist() == [0, 2, 4]
+
+
+# ---- query with exact re-ranking (reading R16) -------------------------
+
+def test_query_oracle_candidates_and_ranking():
+    """Candidates == points sharing a key with the query in some table (computed from the keys, no
+    tables); the top-k == a brute-force sort of those candidates by (distance, id)."""
+    from oracle import query as oq
+    from oracle import tables as otables
+    rng = np.random.default_rng(9)
+    N, n, L, nq, topk = 400, 6, 3, 12, 5
+    X = rng.standard_normal((N, n)).astype(np.float32)
+    keys = rng.integers(0, 25, size=(L, N), dtype=np.uint64)
+    Q = rng.standard_normal((nq, n)).astype(np.float32)
+    qkeys = rng.integers(0, 30, size=(L, nq), dtype=np.uint64)  # some keys absent from every table
+    sk, si, _ = otables.build_tables(keys)
+    ids, dist, ncand = oq.query(X, Q, sk, si, qkeys, topk)
+    for q in range(nq):
+        cand = oq.candidates_brute(keys, qkeys, q)
+        assert ncand[q] == len(cand)
+        ref = sorted(((float(((X[c].astype(np.float64) - Q[q]) ** 2).sum()), c) for c in cand))[:topk]
+        got = [(d, i) for d, i in zip(dist[q], ids[q]) if i >= 0]
+        assert [i for _, i in got] == [c for _, c in ref]
+        assert np.allclose([d for d, _ in got], [d for d, _ in ref], rtol=0, atol=1e-12)
+        assert (ids[q][len(ref):] == -1).all() and np.isinf(dist[q][len(ref):]).all()
+
+
+def test_query_oracle_point_finds_itself():
+    """A query equal to a data point shares all its keys, so the point is a candidate at distance 0
+    and comes first (ties at distance 0 by id)."""
+    from oracle import query as oq
+    from oracle import tables as otables
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((200, 4)).astype(np.float32)
+    keys = rng.integers(0, 1 << 40, size=(4, 200), dtype=np.uint64)
+    sk, si, _ = otables.build_tables(keys)
+    sel = np.array([0, 17, 199])
+    ids, dist, ncand = oq.query(X, X[sel], sk, si, keys[:, sel], 3)
+    assert ids[:, 0].tolist() == sel.tolist() and (dist[:, 0] == 0).all()
