@@ -189,7 +189,8 @@ def main():
                     help="build keys in K1's epilogue (measured slower on C1: 6.80 vs 6.42 ms/step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
-    ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build measurement")
+    ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build and query measurements")
+    ap.add_argument("--queries", type=int, default=10_000, help="queries answered in the query measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -352,6 +353,52 @@ def main():
         except Exception as ex:  # noqa: BLE001 (report, never hide a failure)
             tables = {"error": str(ex)}
 
+    # queries: fresh rows of the same distribution are hashed,
+    # keyed and answered against the tables (exact re-ranking, top-10); recall@10 against exact
+    # nearest neighbours on a 100-query sample (rank 0). Timed separately from the hashing step.
+    queries = None
+    if Kobj is not None and not args.no_tables and not strong and rank == 0:
+        try:
+            nq = args.queries
+            Qd = data.generate(cfg.data, cfg.n, N_total + 10_000_000, N_total + 10_000_000 + nq, seed=cfg.seed,
+                               device=dev)
+            tabs = fl.build_tables(keys)
+            qcodes = torch.empty((nq, cfg.k), dtype=torch.int32, device=dev)
+
+            def qstep():
+                fl.fastlsh_hash(P, Qd, out=qcodes)
+                qk = fl.build_keys(Kobj, qcodes)
+                return fl.query(X, tabs, Qd, qk, topk=10)
+            qstep()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            q0.record(stream)
+            res = qstep()
+            q1.record(stream)
+            torch.cuda.synchronize()
+            qms = q0.elapsed_time(q1)
+            qids = res[0].cpu().numpy()
+            ncand = res[2].double().cpu().numpy()
+            # exact 10-NN of the first 100 queries (fp64 on the host) for recall@10
+            ns = min(100, nq)
+            Xh64 = X.cpu().numpy()
+            Qh = Qd[:ns].cpu().numpy().astype(np.float64)
+            xx = (Xh64.astype(np.float64) ** 2).sum(1)
+            hits = 0
+            for i in range(ns):
+                dd = xx - 2.0 * (Xh64 @ Qh[i]) + (Qh[i] ** 2).sum()
+                truth = set(np.argpartition(dd, 10)[:10].tolist())
+                hits += len(truth & set(qids[i][qids[i] >= 0].tolist()))
+            del Xh64
+            queries = {"queries": nq, "ms": qms, "queries_per_s": nq / (qms / 1e3),
+                       "mean_candidates": float(ncand.mean()), "max_candidates": float(ncand.max()),
+                       "recall_at_10": hits / (10.0 * ns), "recall_sample": ns,
+                       "note": "hash + keys + bucket probes + exact re-rank (top 10) of fresh rows; "
+                               "recall vs exact 10-NN (fp64 host) on the first queries"}
+            del tabs, Qd, qcodes, res
+        except Exception as ex:  # noqa: BLE001
+            queries = {"error": str(ex)}
+
     # on-box comparator: the dense E2LSH GEMM (tcgen05, m = n) on the same rows, k and w
     dense = None
     if not args.no_dense:
@@ -417,7 +464,7 @@ def main():
                 "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},
-                "dense_e2lsh": dense, "tables": tables,
+                "dense_e2lsh": dense, "tables": tables, "queries": queries,
                 "packing": {k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
                                                  "bank_efficiency", "conflict_wavefronts")}}
         print(json.dumps(line))

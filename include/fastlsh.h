@@ -188,6 +188,23 @@ fastlsh_status fastlsh_build_tables(const uint64_t* keys, int32_t L, int64_t N, 
                                     int64_t* nbuckets, void* workspace, size_t workspace_bytes,
                                     fastlsh_stream_t stream);
 
+/* ---- query with exact re-ranking (§3.2; reading R16) ------ */
+
+/* For every query q < nq (rows of Q f32 [nq][n], device): the candidates are the DISTINCT rows v of
+ * the tables (fastlsh_build_tables output for the data X f32 [N][n]) whose key equals the query's
+ * key qkeys[l*ldq + q] in at least one table l (qkeys from fastlsh_hash + fastlsh_build_keys with
+ * the same params and keys objects); they are ranked by the exact squared l2 distance in fp32
+ * (lane-strided sums, fixed warp reduction) and the first `topk` (1..32) by (distance, id) are
+ * written to out_ids[q*topk + r] (int32) / out_dist (f32); fewer candidates pad with -1 / +inf.
+ * out_ncand[q] (int64) = number of distinct candidates. workspace: >= fastlsh_query_workspace(N,
+ * nq) bytes of device memory (visited bitmaps; zeroed by the call). EINVAL on bad arguments,
+ * EUNSUPPORTED if n and L do not fit shared memory. Asynchronous on `stream`. */
+fastlsh_status fastlsh_query_workspace(int64_t N, int64_t nq, size_t* bytes);
+fastlsh_status fastlsh_query(const float* X, int64_t N, int32_t n, const uint64_t* sorted_keys,
+                             const uint32_t* ids, int32_t L, const float* Q, const uint64_t* qkeys, int64_t nq,
+                             int64_t ldq, int32_t topk, int32_t* out_ids, float* out_dist, int64_t* out_ncand,
+                             void* workspace, size_t workspace_bytes, fastlsh_stream_t stream);
+
 /* ---- host-buffer entry point (end-to-end; SURVEY.md §3 "config 4 streaming") ----------------- */
 
 /* Hash HOST rows: X_host f32[N*n] (pinned or pageable), codes_host int32[N*k], keys_host

@@ -22,7 +22,8 @@ EXPORTED = [
     "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
-    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables", "fastlsh_hash_host", "fastlsh_read_flags",
+    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables",
+    "fastlsh_query_workspace", "fastlsh_query", "fastlsh_hash_host", "fastlsh_read_flags",
     "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
 ]
 
@@ -81,6 +82,8 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_hash_keys": [P, P, P, i64, P, P, i64, P],
         "fastlsh_tables_workspace": [i32, i64, ctypes.POINTER(ctypes.c_size_t)],
         "fastlsh_build_tables": [P, i32, i64, i64, P, P, P, P, P, ctypes.c_size_t, P],
+        "fastlsh_query_workspace": [i64, i64, ctypes.POINTER(ctypes.c_size_t)],
+        "fastlsh_query": [P, i64, i32, P, P, i32, P, P, i64, i64, i32, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_hash_host": [P, P, P, i64, P, P, i64],
         "fastlsh_read_flags": [P, P, P, i32, P],
     }
@@ -365,6 +368,33 @@ def build_tables(keys, N=None, out=None, workspace=None, stream=None):
                                     ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_ptr(stream)),
            "fastlsh_build_tables")
     return sk, ids, starts, nb
+
+
+def query(X, tables, Q, qkeys, topk: int = 10, workspace=None, stream=None):
+    """LSH query with exact re-ranking: tables = build_tables(...) output for X,
+    qkeys [L, >= nq] the queries' keys. Returns (ids int32 [nq, topk], dist f32 [nq, topk],
+    ncand int64 [nq])."""
+    import torch
+    lib = load_library()
+    sk, ids, _starts, _nb = tables
+    N, n = X.shape
+    nq = Q.shape[0]
+    L, ldq = qkeys.shape
+    dev = Q.device
+    out_i = torch.empty((nq, topk), dtype=torch.int32, device=dev)
+    out_d = torch.empty((nq, topk), dtype=torch.float32, device=dev)
+    out_c = torch.empty((nq,), dtype=torch.int64, device=dev)
+    need = ctypes.c_size_t()
+    _check(lib.fastlsh_query_workspace(N, nq, ctypes.byref(need)), "fastlsh_query_workspace")
+    if workspace is None or workspace.numel() < need.value:
+        workspace = torch.empty((max(1, need.value),), dtype=torch.uint8, device=dev)
+    _check(lib.fastlsh_query(_dev_ptr(X, torch.float32, "X"), N, n, _dev_ptr(sk, torch.int64, "sorted_keys"),
+                             _dev_ptr(ids, torch.int32, "ids"), L, _dev_ptr(Q, torch.float32, "Q"),
+                             _dev_ptr(qkeys, torch.int64, "qkeys"), nq, ldq, topk,
+                             _dev_ptr(out_i, torch.int32, "out_ids"), _dev_ptr(out_d, torch.float32, "out_dist"),
+                             _dev_ptr(out_c, torch.int64, "out_ncand"), ctypes.c_void_p(workspace.data_ptr()),
+                             workspace.numel(), _stream_ptr(stream)), "fastlsh_query")
+    return out_i, out_d, out_c
 
 
 def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None):

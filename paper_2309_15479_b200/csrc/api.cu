@@ -507,6 +507,36 @@ fastlsh_status fastlsh_build_tables(const uint64_t* keys, int32_t L, int64_t N, 
                                reinterpret_cast<long long*>(nbuckets), workspace, s);
 }
 
+fastlsh_status fastlsh_query_workspace(int64_t N, int64_t nq, size_t* bytes) {
+    if (N < 0 || nq < 0 || !bytes) return FASTLSH_EINVAL;
+    *bytes = query_workspace_bytes(N, query_grid(nq));
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_query(const float* X, int64_t N, int32_t n, const uint64_t* sorted_keys,
+                             const uint32_t* ids, int32_t L, const float* Q, const uint64_t* qkeys, int64_t nq,
+                             int64_t ldq, int32_t topk, int32_t* out_ids, float* out_dist, int64_t* out_ncand,
+                             void* workspace, size_t workspace_bytes, fastlsh_stream_t stream) {
+    if (N < 0 || N >= 0xffffffffLL || n < 1 || L < 1 || L > 4096 || nq < 0 || ldq < nq || topk < 1 ||
+        topk > 32)
+        return FASTLSH_EINVAL;
+    if (nq == 0) return FASTLSH_OK;
+    if (!Q || !qkeys || !out_ids || !out_dist || !out_ncand || (N > 0 && (!X || !sorted_keys || !ids)) ||
+        (reinterpret_cast<uintptr_t>(qkeys) & 7) || (reinterpret_cast<uintptr_t>(sorted_keys) & 7) ||
+        (reinterpret_cast<uintptr_t>(out_ncand) & 7) || (reinterpret_cast<uintptr_t>(X) & 3) ||
+        (reinterpret_cast<uintptr_t>(Q) & 3))
+        return FASTLSH_EINVAL;
+    if ((size_t)((n + 3) & ~3) * 4 + (size_t)L * 16 > 200 * 1024) return FASTLSH_EUNSUPPORTED;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    st = check_sm100(dev);
+    if (st != FASTLSH_OK) return st;
+    if (!workspace || workspace_bytes < query_workspace_bytes(N, query_grid(nq))) return FASTLSH_EINVAL;
+    return launch_query(X, N, n, sorted_keys, ids, L, Q, qkeys, nq, ldq, topk, out_ids, out_dist,
+                        reinterpret_cast<long long*>(out_ncand), workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
                                  int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
                                  fastlsh_stream_t stream) {

@@ -153,6 +153,12 @@ size_t tables_workspace_bytes(int L, long long N);
 fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, long long ldk, uint64_t* sorted_keys,
                                    uint32_t* ids, uint32_t* starts, long long* nbuckets, void* ws,
                                    cudaStream_t stream);
+// query.cu
+size_t query_workspace_bytes(long long N, int grid);
+int query_grid(long long nq);
+fastlsh_status launch_query(const float* X, long long N, int n, const uint64_t* sk, const uint32_t* ids, int L,
+                            const float* Q, const uint64_t* qkeys, long long nq, long long ldq, int topk,
+                            int32_t* out_ids, float* out_dist, long long* out_ncand, void* ws, cudaStream_t stream);
 // e2lsh_tcgen05.cu
 fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N,
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);

@@ -349,3 +349,59 @@ def test_tables_empty():
     keys = torch.zeros((3, 0), dtype=torch.int64, device="cuda")
     sk, ids, starts, nb = fl.build_tables(keys)
     assert nb.cpu().tolist() == [0, 0, 0] and starts.cpu().numpy()[:, 0].tolist() == [0, 0, 0]
+
+
+# ---- query with exact re-ranking (R16) ----------------------------------
+
+def _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o):
+    ids_g, d_g, nc_g = ids_g.cpu().numpy(), d_g.cpu().numpy().astype(np.float64), nc_g.cpu().numpy()
+    assert np.array_equal(nc_g, nc_o)  # the distinct candidate counts are integers: exact
+    assert np.array_equal(ids_g < 0, ids_o < 0)
+    tol = 1e-5 * np.maximum(1.0, np.abs(d_o))  # fp32 distance vs the double oracle
+    live = ids_o >= 0
+    assert (np.abs(d_g[live] - d_o[live]) <= tol[live]).all()
+    # ids may differ only where the oracle's distances are tied within that tolerance
+    for q in range(ids_o.shape[0]):
+        for r in np.flatnonzero((ids_g[q] != ids_o[q]) & live[q]):
+            near = np.abs(d_o[q] - d_o[q, r]) <= 2 * tol[q, r]
+            assert ids_g[q, r] in set(ids_o[q][near].tolist()) or r >= 1 and near[-1], (q, r)
+
+
+@pytest.mark.parametrize("n,N,k,m,w,L,K,topk", [(64, 6000, 24, 8, 2.0, 6, 4, 10), (128, 3000, 16, 16, 8.0, 4, 4, 32),
+                                                (32, 1, 8, 4, 1.0, 2, 4, 5)])
+def test_query_matches_oracle(n, N, k, m, w, L, K, topk):
+    """GPU tables + query on keys from the oracle's codes (so both sides see identical keys) vs
+    oracle/query.py; half the queries are data rows (they must find themselves)."""
+    from oracle import query as oq
+    from oracle import tables as otables
+    idx, a, b = fastlsh_arrays(n, m, k, w, 3)
+    g = torch.Generator().manual_seed(N + n)
+    X = torch.randn((N, n), generator=g) * 2
+    Qn = max(1, min(40, N))
+    Q = torch.cat([X[torch.arange(Qn) * max(1, N // Qn) % N], torch.randn((40, n), generator=g) * 2])
+    r = philox.key_multipliers(L, K, seed=5)
+    _, _, cx = oracle.fastlsh(X.numpy(), idx, a, b, w, threads=THREADS)
+    _, _, cq = oracle.fastlsh(Q.numpy(), idx, a, b, w, threads=THREADS)
+    keys_o = okeys.build_keys(cx, r, L, K)
+    qkeys_o = okeys.build_keys(cq, r, L, K)
+    sk, si, _ = otables.build_tables(keys_o)
+    ids_o, d_o, nc_o = oq.query(X.numpy(), Q.numpy(), sk, si, qkeys_o, topk)
+    tables = fl.build_tables(torch.as_tensor(keys_o.view(np.int64)).cuda())
+    ids_g, d_g, nc_g = fl.query(X.cuda(), tables, Q.cuda(), torch.as_tensor(qkeys_o.view(np.int64)).cuda(), topk)
+    _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o)
+    assert (ids_g.cpu().numpy()[:Qn, 0] >= 0).all()
+
+
+def test_query_end_to_end_c1_sample():
+    """The product path on C1 data: hash + keys + tables + query on the GPU; queries that are data
+    rows find themselves first at distance 0 (exact property, no oracle needed)."""
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1)
+    X = data.generate(c.data, c.n, 0, 50_000, seed=1, device="cuda")
+    keys = fl.build_keys(Kobj, fl.fastlsh_hash(P, X))
+    tables = fl.build_tables(keys)
+    sel = torch.arange(0, 50_000, 997, device="cuda")
+    qk = keys[:, sel].contiguous()
+    ids, dist, nc = fl.query(X, tables, X[sel].contiguous(), qk, topk=10)
+    assert torch.equal(ids[:, 0].long(), sel) and (dist[:, 0] == 0).all() and (nc >= 1).all()
