@@ -373,3 +373,28 @@ def test_query_oracle_point_finds_itself():
     sel = np.array([0, 17, 199])
     ids, dist, ncand = oq.query(X, X[sel], sk, si, keys[:, sel], 3)
     assert ids[:, 0].tolist() == sel.tolist() and (dist[:, 0] == 0).all()
+
+
+# ---- extensions: angular and MIPS transforms (reading R17) --------
+
+def test_transforms_oracle_pins():
+    from oracle import transforms as ot
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((300, 7)) * rng.uniform(0.1, 3, size=(300, 1))
+    X[5] = 0.0
+    Xn = ot.normalize(X)
+    nz = np.arange(300) != 5
+    assert np.allclose(np.linalg.norm(Xn[nz], axis=1), 1.0) and (Xn[5] == 0).all()
+    # hand case: (3, 4) -> (0.6, 0.8)
+    assert np.allclose(ot.normalize(np.array([[3.0, 4.0]])), [[0.6, 0.8]])
+    kappa = ot.max_norm(X)
+    P = ot.mips_data(X, kappa)
+    assert np.allclose(np.linalg.norm(P, axis=1), kappa)  # every transformed row has norm kappa
+    U = rng.standard_normal((40, 7))
+    U /= np.linalg.norm(U, axis=1, keepdims=True)
+    Qt = ot.mips_query(U)
+    # the paper's identity: argmax inner product == argmin l2 distance after P / Q (||u|| = 1)
+    d = ((P[None, :, :] - Qt[:, None, :]) ** 2).sum(-1)
+    assert (np.argmin(d, axis=1) == np.argmax(U @ X.T, axis=1)).all()
+    # ||P(v) - Q(u)||^2 = kappa^2 + 1 - 2 v.u exactly (closed form)
+    assert np.allclose(d, kappa ** 2 + 1 - 2 * (U @ X.T))
