@@ -205,6 +205,19 @@ fastlsh_status fastlsh_query(const float* X, int64_t N, int32_t n, const uint64_
                              int64_t ldq, int32_t topk, int32_t* out_ids, float* out_dist, int64_t* out_ncand,
                              void* workspace, size_t workspace_bytes, fastlsh_stream_t stream);
 
+/* ---- extensions (§5, 830-834 App. B; reading R17) ------------- */
+
+/* Angular similarity: out[r] = X[r] / ||X[r]||_2 (a zero row stays zero); out may equal X.
+ * Device f32 [N][n], fp32 sums of squares, IEEE sqrt and division. */
+fastlsh_status fastlsh_normalize_rows(const float* X, int64_t N, int32_t n, float* out, fastlsh_stream_t stream);
+/* *kappa (device f32) = max_r ||X[r]||_2 (0 for N = 0). */
+fastlsh_status fastlsh_max_row_norm(const float* X, int64_t N, int32_t n, float* kappa, fastlsh_stream_t stream);
+/* MIPS transforms: data (is_query = 0) out[r] = (sqrt(max(kappa^2 - ||X[r]||^2, 0)), X[r]); queries
+ * (is_query = 1) out[r] = (0, X[r]). out: device f32 [N][n+1] (kappa: device f32, data only);
+ * hash the results with params of dimension n + 1. */
+fastlsh_status fastlsh_mips_transform(const float* X, int64_t N, int32_t n, const float* kappa, int32_t is_query,
+                                      float* out, fastlsh_stream_t stream);
+
 /* ---- host-buffer entry point (end-to-end; SURVEY.md §3 "config 4 streaming") ----------------- */
 
 /* Hash HOST rows: X_host f32[N*n] (pinned or pageable), codes_host int32[N*k], keys_host

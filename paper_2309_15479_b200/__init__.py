@@ -23,7 +23,8 @@ EXPORTED = [
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables",
-    "fastlsh_query_workspace", "fastlsh_query", "fastlsh_hash_host", "fastlsh_read_flags",
+    "fastlsh_query_workspace", "fastlsh_query", "fastlsh_normalize_rows", "fastlsh_max_row_norm",
+    "fastlsh_mips_transform", "fastlsh_hash_host", "fastlsh_read_flags",
     "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
 ]
 
@@ -83,6 +84,9 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_tables_workspace": [i32, i64, ctypes.POINTER(ctypes.c_size_t)],
         "fastlsh_build_tables": [P, i32, i64, i64, P, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_query_workspace": [i64, i64, ctypes.POINTER(ctypes.c_size_t)],
+        "fastlsh_normalize_rows": [P, i64, i32, P, P],
+        "fastlsh_max_row_norm": [P, i64, i32, P, P],
+        "fastlsh_mips_transform": [P, i64, i32, P, i32, P, P],
         "fastlsh_query": [P, i64, i32, P, P, i32, P, P, i64, i64, i32, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_hash_host": [P, P, P, i64, P, P, i64],
         "fastlsh_read_flags": [P, P, P, i32, P],
@@ -395,6 +399,42 @@ def query(X, tables, Q, qkeys, topk: int = 10, workspace=None, stream=None):
                              _dev_ptr(out_c, torch.int64, "out_ncand"), ctypes.c_void_p(workspace.data_ptr()),
                              workspace.numel(), _stream_ptr(stream)), "fastlsh_query")
     return out_i, out_d, out_c
+
+
+def normalize_rows(X, out=None, stream=None):
+    """Angular similarity preprocessing: rows scaled to unit l2 norm."""
+    import torch
+    lib = load_library()
+    N, n = X.shape
+    out = torch.empty_like(X) if out is None else out
+    _check(lib.fastlsh_normalize_rows(_dev_ptr(X, torch.float32, "X"), N, n, _dev_ptr(out, torch.float32, "out"),
+                                      _stream_ptr(stream)), "fastlsh_normalize_rows")
+    return out
+
+
+def max_row_norm(X, stream=None):
+    """kappa = max_r ||X[r]||_2 as a 1-element device tensor."""
+    import torch
+    lib = load_library()
+    N, n = X.shape
+    k = torch.empty((1,), dtype=torch.float32, device=X.device)
+    _check(lib.fastlsh_max_row_norm(_dev_ptr(X, torch.float32, "X"), N, n, _dev_ptr(k, torch.float32, "kappa"),
+                                    _stream_ptr(stream)), "fastlsh_max_row_norm")
+    return k
+
+
+def mips_transform(X, kappa=None, query: bool = False, stream=None):
+    """MIPS transforms: P(v) = (sqrt(kappa^2 - ||v||^2), v) for data,
+    Q(u) = (0, u) for queries; returns f32 [N, n+1]."""
+    import torch
+    lib = load_library()
+    N, n = X.shape
+    out = torch.empty((N, n + 1), dtype=torch.float32, device=X.device)
+    kp = _dev_ptr(kappa, torch.float32, "kappa") if kappa is not None else ctypes.c_void_p(0)
+    _check(lib.fastlsh_mips_transform(_dev_ptr(X, torch.float32, "X"), N, n, kp, 1 if query else 0,
+                                      _dev_ptr(out, torch.float32, "out"), _stream_ptr(stream)),
+           "fastlsh_mips_transform")
+    return out
 
 
 def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None):

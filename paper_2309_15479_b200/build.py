@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [*os.environ.get("FASTLSH_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 SOURCES = ["api.cu", "gather.cu", "gather_inst0.cu", "gather_inst1.cu", "gather_inst2.cu", "gather_inst3.cu",
-           "gather_tmem.cu", "tables.cu", "query.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
+           "gather_tmem.cu", "tables.cu", "query.cu", "transforms.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
 
 
 def _stale(out: str, deps) -> bool:

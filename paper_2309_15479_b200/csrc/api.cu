@@ -537,6 +537,37 @@ fastlsh_status fastlsh_query(const float* X, int64_t N, int32_t n, const uint64_
                         reinterpret_cast<long long*>(out_ncand), workspace, reinterpret_cast<cudaStream_t>(stream));
 }
 
+static fastlsh_status transform_checks(const float* X, int64_t N, int32_t n, const void* out) {
+    if (N < 0 || n < 1) return FASTLSH_EINVAL;
+    if (N > 0 && (!X || !out || (reinterpret_cast<uintptr_t>(X) & 3) || (reinterpret_cast<uintptr_t>(out) & 3)))
+        return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = current_device(&dev);
+    if (st != FASTLSH_OK) return st;
+    return check_sm100(dev);
+}
+
+fastlsh_status fastlsh_normalize_rows(const float* X, int64_t N, int32_t n, float* out, fastlsh_stream_t stream) {
+    fastlsh_status st = transform_checks(X, N, n, out);
+    if (st != FASTLSH_OK || N == 0) return st;
+    return launch_normalize(X, N, n, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status fastlsh_max_row_norm(const float* X, int64_t N, int32_t n, float* kappa, fastlsh_stream_t stream) {
+    if (!kappa || (reinterpret_cast<uintptr_t>(kappa) & 3)) return FASTLSH_EINVAL;
+    fastlsh_status st = transform_checks(X, N, n, kappa);
+    if (st != FASTLSH_OK) return st;
+    return launch_max_norm(X, N, n, kappa, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fastlsh_status fastlsh_mips_transform(const float* X, int64_t N, int32_t n, const float* kappa, int32_t is_query,
+                                      float* out, fastlsh_stream_t stream) {
+    if (!is_query && (!kappa || (reinterpret_cast<uintptr_t>(kappa) & 3))) return FASTLSH_EINVAL;
+    fastlsh_status st = transform_checks(X, N, n, out);
+    if (st != FASTLSH_OK || N == 0) return st;
+    return launch_mips(X, N, n, kappa, is_query ? 1 : 0, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
                                  int64_t N, int32_t* codes, uint64_t* keys_out, int64_t ldk,
                                  fastlsh_stream_t stream) {

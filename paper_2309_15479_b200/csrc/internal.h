@@ -159,6 +159,11 @@ int query_grid(long long nq);
 fastlsh_status launch_query(const float* X, long long N, int n, const uint64_t* sk, const uint32_t* ids, int L,
                             const float* Q, const uint64_t* qkeys, long long nq, long long ldq, int topk,
                             int32_t* out_ids, float* out_dist, long long* out_ncand, void* ws, cudaStream_t stream);
+// transforms.cu
+fastlsh_status launch_normalize(const float* X, long long N, int n, float* out, cudaStream_t s);
+fastlsh_status launch_max_norm(const float* X, long long N, int n, float* kappa, cudaStream_t s);
+fastlsh_status launch_mips(const float* X, long long N, int n, const float* kappa, int is_query, float* out,
+                           cudaStream_t s);
 // e2lsh_tcgen05.cu
 fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N,
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);

@@ -405,3 +405,57 @@ def test_query_end_to_end_c1_sample():
     qk = keys[:, sel].contiguous()
     ids, dist, nc = fl.query(X, tables, X[sel].contiguous(), qk, topk=10)
     assert torch.equal(ids[:, 0].long(), sel) and (dist[:, 0] == 0).all() and (nc >= 1).all()
+
+
+# ---- extensions (R17) ------------------------------------------------
+
+def test_transforms_match_oracle():
+    from oracle import transforms as ot
+    g = torch.Generator().manual_seed(4)
+    X = torch.randn((3001, 37), generator=g) * torch.rand((3001, 1), generator=g) * 5
+    X[7] = 0.0
+    Xd = X.cuda()
+    Xn = fl.normalize_rows(Xd).cpu().numpy()
+    assert np.allclose(Xn, ot.normalize(X.numpy()), rtol=2e-6, atol=1e-7)
+    kap = fl.max_row_norm(Xd)
+    kref = ot.max_norm(X.numpy())
+    assert abs(kap.item() - kref) <= 1e-6 * kref
+    P = fl.mips_transform(Xd, kap).cpu().numpy().astype(np.float64)
+    Pr = ot.mips_data(X.numpy(), kap.item())
+    assert np.array_equal(P[:, 1:], Pr[:, 1:])  # copied coordinates are exact
+    assert np.allclose(P[:, 0] ** 2, Pr[:, 0] ** 2, rtol=0, atol=2e-6 * kref ** 2)  # cancellation-aware bound
+    Qt = fl.mips_transform(Xd[:50], query=True).cpu().numpy()
+    assert (Qt[:, 0] == 0).all() and np.array_equal(Qt[:, 1:], X[:50].numpy())
+
+
+def test_mips_pipeline_finds_max_inner_product():
+    """End to end on the GPU: P/Q transforms + FastLSH keys + tables + query. Since
+    ||P(v) - Q(u)||^2 = kappa^2 + 1 - 2 v.u for ||u|| = 1, the top-1 of the
+    distance re-rank must be the candidate with the largest inner product (candidates recomputed
+    here from the keys with torch)."""
+    g = torch.Generator().manual_seed(6)
+    X = (torch.randn((4000, 31), generator=g) * (1 + torch.rand((4000, 1), generator=g))).cuda()
+    kap = fl.max_row_norm(X)
+    PX = fl.mips_transform(X, kap)
+    U = fl.normalize_rows(torch.randn((25, 31), generator=g).cuda())
+    QU = fl.mips_transform(U, query=True)
+    P = fl.Params.create(32, 16, 8, 2.0, seed=3)
+    Kobj = fl.Keys.create(4, 2, seed=3)
+    keys = fl.build_keys(Kobj, fl.fastlsh_hash(P, PX))
+    qkeys = fl.build_keys(Kobj, fl.fastlsh_hash(P, QU))
+    ids, dist, nc = fl.query(PX, fl.build_tables(keys), QU, qkeys, topk=1)
+    ip = (U.double() @ X.double().T)
+    checked = 0
+    for q in range(U.shape[0]):
+        cand = (keys == qkeys[:, q:q + 1]).any(dim=0).nonzero().flatten()
+        assert nc[q].item() == cand.numel()
+        if cand.numel() == 0:
+            assert ids[q, 0].item() == -1
+            continue
+        best = ip[q, cand].max().item()
+        got = ids[q, 0].long().item()
+        assert ip[q, got].item() >= best - 1e-4 * max(1.0, abs(best))
+        d_ref = kap.double().item() ** 2 + 1 - 2 * ip[q, got].item()
+        assert abs(dist[q, 0].item() - d_ref) <= 1e-4 * max(1.0, d_ref)
+        checked += 1
+    assert checked >= 5
