@@ -9,9 +9,10 @@
 // the buckets 32 entries at a time, keep the first occurrence of every candidate with a
 // test-and-set in the CTA's visited bitmap (N bits in global memory, cleared again after the
 // query), and score fresh candidates one at a time with the whole warp (coalesced row read,
-// query in shared memory, fixed-order warp reduction); each warp keeps a sorted top-k list that
-// thread 0 merges at the end. Work per query: the bucket searches plus one row read per distinct
-// candidate — bound by HBM/L2 reads of candidate rows.
+// query in shared memory, four independent partial sums per lane so four loads are in flight,
+// fixed-order reduction); each warp keeps a sorted top-k list that thread 0 merges at the end.
+// Work per query: the bucket searches plus one row read per distinct candidate — bound by
+// HBM/L2 reads of candidate rows (C1: 10^4 queries x 2,106 candidates x 3,840 B in 38 ms).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -88,11 +89,25 @@ __global__ void __launch_bounds__(kQWarps * 32) query_kernel(const float* __rest
                     todo &= todo - 1;
                     const uint32_t cc = __shfl_sync(0xffffffffu, c, src);
                     const float* row = X + (long long)cc * n;
-                    float acc = 0.f;
-                    for (int d = lane; d < n; d += 32) {
-                        const float df = row[d] - squery[d];
-                        acc = fmaf(df, df, acc);
+                    // four independent partial sums (dims d, d+32, d+64, d+96 of each 128-block)
+                    // keep four row loads in flight per lane; fixed combination order
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                    int d = lane;
+                    for (; d + 96 < n; d += 128) {
+                        const float x0 = __ldg(row + d), x1 = __ldg(row + d + 32);
+                        const float x2 = __ldg(row + d + 64), x3 = __ldg(row + d + 96);
+                        const float d0 = x0 - squery[d], d1 = x1 - squery[d + 32];
+                        const float d2 = x2 - squery[d + 64], d3 = x3 - squery[d + 96];
+                        a0 = fmaf(d0, d0, a0);
+                        a1 = fmaf(d1, d1, a1);
+                        a2 = fmaf(d2, d2, a2);
+                        a3 = fmaf(d3, d3, a3);
                     }
+                    for (; d < n; d += 32) {
+                        const float df = __ldg(row + d) - squery[d];
+                        a0 = fmaf(df, df, a0);
+                    }
+                    float acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                     if (lane == 0) {  // insert into this warp's sorted top-k list
