@@ -25,7 +25,7 @@ def allgather_keys(keys_local, out=None, group=None):
     """All-gather table-major keys [L][N_local] (int64 view of u64) into [L][world * N_local].
 
     Equal shard sizes are required (all_gather_into_tensor semantics); the per-table calls are
-    issued back to back so NCCL can pipeline them. Returns `out`.
+    issued asynchronously back to back and waited on together, so NCCL pipelines them. Returns `out`.
     """
     import torch
     import torch.distributed as dist
@@ -36,8 +36,10 @@ def allgather_keys(keys_local, out=None, group=None):
         out = torch.empty((L, world * n_local), dtype=keys_local.dtype, device=keys_local.device)
     if out.shape != (L, world * n_local):
         raise ValueError("output must be [L, world * N_local]")
-    for l in range(L):
-        dist.all_gather_into_tensor(out[l], keys_local[l].contiguous(), group=group)
+    works = [dist.all_gather_into_tensor(out[l], keys_local[l].contiguous(), group=group, async_op=True)
+             for l in range(L)]
+    for w in works:
+        w.wait()
     return out
 
 
