@@ -189,3 +189,23 @@ def test_epilogue_partial_reads_conflict_free(lib, n, m, k):
             for q in range(pk["parts"]):
                 pos = ul[o:o + 8, q] % 8
                 assert len(set(pos.tolist())) == len(pos), (bl, o, q, pos)
+
+
+def test_table_query_transform_argument_checks(lib):
+    """Size/pointer validation of the table, query and transform entry points happens before any
+    device work (EINVAL, no crash); valid calls without a B200 fail loudly, never on the CPU."""
+    c_size = ctypes.c_size_t()
+    assert lib.fastlsh_tables_workspace(0, 10, ctypes.byref(c_size)) == fl.EINVAL
+    assert lib.fastlsh_tables_workspace(3, -1, ctypes.byref(c_size)) == fl.EINVAL
+    assert lib.fastlsh_tables_workspace(50, 1_000_000, ctypes.byref(c_size)) == fl.OK and c_size.value > 50 * 12e6
+    V = ctypes.c_void_p(256)
+    assert lib.fastlsh_build_tables(V, 0, 10, 10, V, V, V, V, V, 1 << 30, None) == fl.EINVAL   # L = 0
+    assert lib.fastlsh_build_tables(V, 2, 10, 5, V, V, V, V, V, 1 << 30, None) == fl.EINVAL    # ldk < N
+    assert lib.fastlsh_query_workspace(-1, 3, ctypes.byref(c_size)) == fl.EINVAL
+    assert lib.fastlsh_query(V, 10, 4, V, V, 2, V, V, 3, 3, 0, V, V, V, V, 1 << 30, None) == fl.EINVAL   # topk 0
+    assert lib.fastlsh_query(V, 10, 4, V, V, 2, V, V, 3, 3, 33, V, V, V, V, 1 << 30, None) == fl.EINVAL  # topk > 32
+    assert lib.fastlsh_query(V, 10, 4, V, V, 2, V, V, 3, 2, 5, V, V, V, V, 1 << 30, None) == fl.EINVAL   # ldq < nq
+    assert lib.fastlsh_normalize_rows(V, -1, 4, V, None) == fl.EINVAL
+    assert lib.fastlsh_mips_transform(V, 5, 4, None, 0, V, None) == fl.EINVAL  # data transform needs kappa
+    rc = lib.fastlsh_normalize_rows(V, 5, 4, V, None)
+    assert rc in (fl.ECUDA, fl.EUNSUPPORTED)
