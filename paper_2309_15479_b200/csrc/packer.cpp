@@ -16,6 +16,10 @@
 //     bank group unused at that position.
 //  5. Lane positions inside a quarter are free for the schedule; they are chosen (König colouring
 //     of quarters x (hash octet, part)) so that the epilogue's partial-sum reads are conflict-free.
+//  Between 2 and 3, single slots move between the parts of a hash (the split into parts is free
+//  too) to flatten each quarter's bank-group loads towards m/parts; each parts choice is then
+//  costed with the padded slot count and with slots capped at the (even) part size, folding the
+//  few remaining colours into conflicts.
 //
 // Everything is deterministic, so every rank derives the identical packing (and hence the
 // identical fp32 summation order) from the same params.
@@ -236,12 +240,65 @@ std::vector<int> color_bipartite(const std::vector<int>& left, const std::vector
     return col;
 }
 
+// Slot exchange between the parts of a hash (P >= 2): which of a hash's slots go to which part is
+// free (addition commutes), so single slots are swapped between partner units in different
+// quarters when that lowers F = sum over (quarter, bank group) of max(0, load - T)^2 with T = the
+// part size (strict descent). Unit sizes do not change.
+void exchange_slots(std::vector<Unit>& units, std::vector<QuarterState>& qs, int P, int T) {
+    if (P < 2) return;
+    std::vector<int> uq(units.size(), -1);
+    for (int q = 0; q < (int)qs.size(); ++q)
+        for (int u : qs[q].members) uq[u] = q;
+    auto e2 = [T](int v) { return v > T ? (v - T) * (v - T) : 0; };
+    for (int sweep = 0; sweep < 200; ++sweep) {
+        bool improved = false;
+        for (int q = 0; q < (int)qs.size(); ++q) {
+            for (int g = 0; g < 8; ++g) {
+                while (qs[q].load[g] > T) {
+                    int best = 0, bu = -1, bu2 = -1, bg2 = -1;
+                    for (int u : qs[q].members) {
+                        if (units[u].cnt[g] == 0) continue;
+                        const int base = u - units[u].part;  // units of a hash are consecutive
+                        for (int pp = 0; pp < P; ++pp) {
+                            const int u2 = base + pp;
+                            const int q2 = uq[u2];
+                            if (u2 == u || q2 < 0 || q2 == q) continue;
+                            for (int g2 = 0; g2 < 8; ++g2) {
+                                if (g2 == g || units[u2].cnt[g2] == 0) continue;
+                                const auto& A = qs[q].load;
+                                const auto& B = qs[q2].load;
+                                const int d = e2(A[g] - 1) - e2(A[g]) + e2(A[g2] + 1) - e2(A[g2]) +
+                                              e2(B[g] + 1) - e2(B[g]) + e2(B[g2] - 1) - e2(B[g2]);
+                                if (d < best) { best = d; bu = u; bu2 = u2; bg2 = g2; }
+                            }
+                        }
+                    }
+                    if (bu < 0) break;
+                    const int q2 = uq[bu2];
+                    auto& sa = units[bu].slots;
+                    auto& sb = units[bu2].slots;
+                    int ia = -1, ib = -1;
+                    for (int i = 0; i < (int)sa.size() && ia < 0; ++i) if ((sa[i].first & 7) == g) ia = i;
+                    for (int i = 0; i < (int)sb.size() && ib < 0; ++i) if ((sb[i].first & 7) == bg2) ib = i;
+                    std::swap(sa[ia], sb[ib]);
+                    units[bu].cnt[g]--; units[bu].cnt[bg2]++;
+                    units[bu2].cnt[bg2]--; units[bu2].cnt[g]++;
+                    qs[q].load[g]--; qs[q].load[bg2]++;
+                    qs[q2].load[bg2]--; qs[q2].load[g]++;
+                    improved = true;
+                }
+            }
+        }
+        if (!improved) break;
+    }
+}
+
 struct Trial {
     Packing pk;
     double cost = 1e300;
 };
 
-void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
+void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out, int ms_cap) {
     const int n = p.n, m = p.m, k = p.k;
     Packing pk;
     pk.parts = P;
@@ -297,6 +354,7 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
             }
         }
         auto qs = group_units(units, Q, dmax);
+        if (P <= 4) exchange_slots(units, qs, P, dmax);  // matters (and is cheap) for few parts
         plans[bl].resize(Q);
         for (int q = 0; q < Q; ++q) {
             auto& qp = plans[bl][q];
@@ -327,7 +385,11 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out) {
     int64_t conflicts = 0;
     if (MS > kMaxSlots) MS = kMaxSlots;
     MS = (MS + 1) & ~1;  // the gather loop issues slots in pairs
-    if (const char* e = std::getenv("FASTLSH_MS_CAP")) {  // experiment knob: fold colours beyond a cap
+    // ms_cap > 0: fold colours beyond the cap into existing positions (a few bank conflicts instead
+    // of padding slots every lane pays); the cost model below compares both choices
+    if (ms_cap < 0) ms_cap = (dmax + 1) & ~1;  // the even part size
+    if (ms_cap > 0 && (ms_cap & ~1) >= dmax && (ms_cap & ~1) < MS) MS = ms_cap & ~1;
+    if (const char* e = std::getenv("FASTLSH_MS_CAP")) {  // experiment knob: force a cap
         const int cap = std::atoi(e) & ~1;
         if (cap >= dmax && cap < MS) MS = cap;
     }
@@ -475,13 +537,16 @@ void build_packing(const fastlsh_params& p, Packing& out) {
         // beyond 256 lanes per hash the block holds a single hash; keep P <= 256
         if (P > 256) break;
         // 16 warps per CTA when the slots fit 128 registers per lane (MS <= 32), else 8
-        Trial t;
-        try_parts(p, P, (warps_force ? warps_force : 16) * 32, t);
-        if (!warps_force && t.pk.slots > 32) {
-            t = Trial();
-            try_parts(p, P, 8 * 32, t);
+        for (int cap : {0, -1}) {  // padded slots, or slots capped at the part size with folding
+            if (cap < 0 && P > 8) break;  // many parts: padding is already small
+            Trial t;
+            try_parts(p, P, (warps_force ? warps_force : 16) * 32, t, cap);
+            if (!warps_force && t.pk.slots > 32) {
+                t = Trial();
+                try_parts(p, P, 8 * 32, t, cap);
+            }
+            if (t.cost < best.cost) best = std::move(t);
         }
-        if (t.cost < best.cost) best = std::move(t);
     }
     out = std::move(best.pk);
 }

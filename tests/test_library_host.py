@@ -150,8 +150,10 @@ def test_bench_config_packing_quality(lib):
     c = configs.get("C1")
     p = fl.Params.create(c.n, c.m, c.k, c.w, seed=1)
     info = p.info()
-    # the cost model splits m=60 into 2 parts so that 16 warps/SM fit (MS <= 32 registers)
-    assert info["conflict_wavefronts"] == 0
+    # the cost model splits m=60 into 2 parts so that 16 warps/SM fit (MS <= 32 registers); slots
+    # capped at the part size leave only a few folded bank conflicts (< 2% of the wavefronts)
+    stage_wavefronts = info["hash_blocks"] * info["warps_per_block"] * 4 * info["slots"]
+    assert info["conflict_wavefronts"] <= 0.02 * stage_wavefronts
     assert info["slots"] <= 32 and info["warps_per_block"] == 16
     assert info["bank_efficiency"] >= 0.9
 
