@@ -249,8 +249,11 @@ def main():
             if record:
                 e[0].record(stream)
             cb = codes[:c1 - c0]
-            if Kobj and args.fused_keys and not strong:
-                fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
+            if Kobj and args.fused_keys:
+                if strong:  # keys only: the codes of the 2e8 rows never reach HBM
+                    fl.hash_keys(P, Kobj, X[c0:c1], keys_out=keys, with_codes=False, col0=c0)
+                else:
+                    fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
                 if record:
                     e[1].record(stream)
             else:

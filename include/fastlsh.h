@@ -164,8 +164,11 @@ fastlsh_status fastlsh_build_keys(const fastlsh_keys* keys, const int32_t* codes
                                   int32_t k, uint64_t* keys_out, int64_t ldk,
                                   fastlsh_stream_t stream);
 
-/* Fused: codes (as fastlsh_hash) and keys (as fastlsh_build_keys) for the same rows in one call
- * sequence on `stream`; keys may be NULL (codes only). */
+/* Codes (as fastlsh_hash) and keys (as fastlsh_build_keys) for the same rows on `stream`; keys may
+ * be NULL (codes only). When the params were packed with fastlsh_params_set_table_size(p, K) so that
+ * every CTA hash block holds whole tables, the keys are built in the hashing kernel's epilogue
+ * (codes never re-read); then `codes` may be NULL too — keys only, codes never written to HBM
+ * (SURVEY.md §8(f)1). Otherwise codes == NULL is EINVAL. */
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* keys,
                                  const float* X, int64_t N, int32_t* codes, uint64_t* keys_out,
                                  int64_t ldk, fastlsh_stream_t stream);

@@ -437,21 +437,31 @@ def mips_transform(X, kappa=None, query: bool = False, stream=None):
     return out
 
 
-def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None):
-    """One step of the hot path: codes (Eq. 5) then compound keys, on the same stream."""
+def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, stream=None,
+              with_codes: bool = True, col0: int = 0):
+    """One step of the hot path: codes (Eq. 5) then compound keys, on the same stream.
+
+    with_codes=False (params packed with set_table_size(K)): keys only, built in the hashing
+    kernel's epilogue; codes are never written. keys_out may be a wider [L, ldk] table with the
+    N keys of each table written to columns [col0, col0 + N)."""
     import torch
     params._ready()
     N = X.shape[0]
-    if codes is None:
+    if with_codes and codes is None:
         codes = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
     kp = ctypes.c_void_p(0)
+    ldk = N
     if keys is not None:
         if keys_out is None:
-            keys_out = torch.empty((keys.L, N), dtype=torch.int64, device=X.device)
-        kp = _dev_ptr(keys_out, torch.int64, "keys")
+            keys_out = torch.empty((keys.L, N + col0), dtype=torch.int64, device=X.device)
+        ldk = keys_out.shape[1]
+        if keys_out.shape[0] != keys.L or col0 < 0 or col0 + N > ldk:
+            raise ValueError("keys_out must be [L, ldk] with col0 + N <= ldk")
+        kp = ctypes.c_void_p(_dev_ptr(keys_out, torch.int64, "keys").value + 8 * col0)
+    cp = _dev_ptr(codes, torch.int32, "codes") if codes is not None else ctypes.c_void_p(0)
     _check(params._lib.fastlsh_hash_keys(params._h, keys._h if keys is not None else None,
-                                         _dev_ptr(X, torch.float32, "X"), N, _dev_ptr(codes, torch.int32, "codes"),
-                                         kp, N, _stream_ptr(stream)), "fastlsh_hash_keys")
+                                         _dev_ptr(X, torch.float32, "X"), N, cp, kp, ldk, _stream_ptr(stream)),
+           "fastlsh_hash_keys")
     return codes, keys_out
 
 

@@ -574,13 +574,15 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     if (!ks || !keys_out) return fastlsh_hash(p, X, N, codes, stream);
     if (!p || N < 0 || (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
     if (N == 0) return FASTLSH_OK;
-    if (!X || !codes || ldk < N || (reinterpret_cast<uintptr_t>(X) & 3) ||
-        (reinterpret_cast<uintptr_t>(codes) & 3) || (reinterpret_cast<uintptr_t>(keys_out) & 7))
+    if (!X || ldk < N || (reinterpret_cast<uintptr_t>(X) & 3) || (reinterpret_cast<uintptr_t>(codes) & 3) ||
+        (reinterpret_cast<uintptr_t>(keys_out) & 7))
         return FASTLSH_EINVAL;
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
     if (st != FASTLSH_OK) return st;
-    if (keys_fusable(p, ks) && !tmem_selected(p)) {  // keys built in K1's epilogue
+    const bool fusable = keys_fusable(p, ks) && !tmem_selected(p);
+    if (!codes && !fusable) return FASTLSH_EINVAL;  // keys only needs the fused kernel
+    if (fusable) {  // keys built in K1's epilogue (codes not written when codes == NULL)
         const uint64_t* dr = nullptr;
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;

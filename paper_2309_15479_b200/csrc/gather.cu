@@ -71,7 +71,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     const Packing& pk = p->pack;
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    const int fused = (fk && fk->keys && codes) ? 1 : 0;
+    const int fused = (fk && fk->keys) ? 1 : 0;  // codes may be null: keys only
     const int tables_max = fused ? pk.kb_max / fk->K + 1 : 0;
     const int keys_words = fused ? tables_max * (fk->K + 1) : 0;
     // Pipeline shape: among the shapes whose shared memory fits (with the TMA landing ring when

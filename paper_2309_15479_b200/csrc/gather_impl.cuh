@@ -390,11 +390,12 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
             }
             if (4 * u + 4 <= nrows) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) a.codes[o0 + (long long)r * a.k] = code[r];
+                for (int r = 0; r < 4; ++r)
+                    if (!FUSED || a.codes) a.codes[o0 + (long long)r * a.k] = code[r];
             } else {
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                    if (4 * u + r < nrows) a.codes[o0 + (long long)r * a.k] = code[r];
+                    if (4 * u + r < nrows && (!FUSED || a.codes)) a.codes[o0 + (long long)r * a.k] = code[r];
             }
             if (fused) {
 #pragma unroll

@@ -459,3 +459,22 @@ def test_mips_pipeline_finds_max_inner_product():
         assert abs(dist[q, 0].item() - d_ref) <= 1e-4 * max(1.0, d_ref)
         checked += 1
     assert checked >= 5
+
+
+def test_fused_keys_only_chunked_equals_separate():
+    """Keys-only fused path (codes never written), chunked into one [L][N] table with col0 offsets,
+    equals codes + the key kernel (C3 shape: 16 tables of 16 codes)."""
+    c = configs.get("C3")
+    idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 2)
+    Pf = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(c.K)
+    Pp = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    Kobj = fl.Keys.create(c.L, c.K, seed=7)
+    N = 20_011
+    X = data.generate(c.data, c.n, 0, N, seed=3, device="cuda")
+    ref = fl.build_keys(Kobj, fl.fastlsh_hash(Pp, X))
+    keys = torch.full_like(ref, -1)
+    for c0 in range(0, N, 8192):
+        c1 = min(N, c0 + 8192)
+        codes, _ = fl.hash_keys(Pf, Kobj, X[c0:c1], keys_out=keys, with_codes=False, col0=c0)
+        assert codes is None
+    assert torch.equal(keys, ref)

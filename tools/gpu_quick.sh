@@ -1,7 +1,9 @@
-timeout 1200 python tools/measure_configs.py --out gpurun_out/configs3.jsonl > gpurun_out/configs3.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "fused or keys or host_entry" 2>&1 | tail -2 > gpurun_out/qq.log
+timeout 900 python bench.py --config C3 --steps 3 --e2e-steps 1 --no-dense --no-cpu-baseline --fused-keys > gpurun_out/c3f.json 2>gpurun_out/c3f.err; echo c3f=$?
+tail -2 gpurun_out/c3f.err
 python - <<'PY'
 import json
-for l in open('gpurun_out/configs3.jsonl'):
-    d=json.loads(l); k1=d.get('K1',{}); k1t=d.get('K1t',{}); d3=d.get('dense_tf32x3',{}); d1=d.get('dense_tf32x1',{})
-    print(f"{d['config']} m={d['m']} N={d['rows']}: roof {d['t_roof_ms']:.3f} | K1 {k1.get('ms',float('nan')):.3f}ms frac {k1.get('roofline_frac',float('nan')):.3f} | K1t {k1t.get('ms',float('nan')):.3f} | x3 {d3.get('ms',float('nan')):.3f} x1 {d1.get('ms',float('nan')):.3f} | {d['packing']}")
+d = json.loads(open("gpurun_out/c3f.json").read().strip().splitlines()[-1])
+print("C3 fused: ms/step %.3f" % d["ms_per_step"], "value %.3e" % d["value"], d["breakdown_ms"], "frac %.3f" % d["roofline"]["frac"], d["gpu_launches"])
 PY
+cat gpurun_out/qq.log
