@@ -35,6 +35,7 @@
 namespace fastlsh {
 namespace k1 {
 
+// partial-sum ring depth: 2 (a depth of 3, measured, was slower: less stage/landing room)
 constexpr int kPartSlots = 2;
 constexpr int kBars = 2 * 4 + 2 * kPartSlots + 2 * 2 + 4;  // up to 4 stages, 2 landings, 2 code slots
 
