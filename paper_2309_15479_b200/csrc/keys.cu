@@ -71,13 +71,34 @@ __global__ void __launch_bounds__(kKeyThreads) keys_kernel(const uint64_t* __res
 }
 
 
-// Fast path (K <= 16): a warp owns a group of 32 consecutive tables (lane = table, its K+1
-// multipliers in registers as three 21-bit limbs r = r2*2^42 + r1*2^21 + r0) and a block of 32
-// rows. Per term, three IMAD.WIDE.U32 accumulate limb*u32(c) (< 2^53) into 64-bit sums
-// S0, S1, S2 (K <= 2^10 terms cannot overflow); then
+// Fast path (K <= 16): a warp owns a group of TPW consecutive tables (lane % TPW = table, its
+// K+1 multipliers in registers as three 21-bit limbs r = r2*2^42 + r1*2^21 + r0) and RPW =
+// 32 / TPW rows at a time (lane / TPW), over a block of RB rows. Per term, three IMAD.WIDE.U32
+// accumulate limb*u32(c) (< 2^53) into 64-bit sums S0, S1, S2 (K <= 2^10 terms cannot
+// overflow); then
 //   key = (r_0 + S0 + S1*2^21 + S2*2^42) mod (2^61-1),
-// where x*2^j mod (2^61-1) is a 61-bit rotation — all exact. The 32x32 keys of a (group, row
-// block) go through shared memory so each table's 32 rows are written as one 256-byte run.
+// where x*2^j mod (2^61-1) is a 61-bit rotation — all exact. HBM streaming: the codes of B row
+// steps are loaded before any of them is reduced (addresses clamped into the valid range, so
+// the loads are unconditional and ptxas issues them back to back: B*K*4 bytes in flight per
+// lane). TPW is chosen so that few lanes idle (C1, L = 50: TPW = 10, 30 of 32 lanes busy). The
+// keys of a (group, row block) go through shared memory so each table's RB rows leave as one
+// contiguous run.
+constexpr int kKeySlots = 32 * 33 + 64;  // per warp: TPW * (RB + 1) u64 keys
+
+// row steps per load batch (measured on C1/C4, K = 10: 2 -> 0.72 ms, 3 -> 0.60 ms, 4 -> 0.64 ms;
+// more rows per batch means more bytes in flight but more registers, hence fewer warps; K = 16
+// on C3: the 8M-row microbenchmark has 1 -> 2.07 ms, 2 -> 2.16 ms, 3 -> 2.41 ms, but the chunked
+// 2e8-row bench build 2 -> 45.5 ms vs 1 -> 51.8 ms: 2 is kept)
+#ifndef FASTLSH_KEYS_B10
+#define FASTLSH_KEYS_B10 3
+#endif
+#ifndef FASTLSH_KEYS_B16
+#define FASTLSH_KEYS_B16 2
+#endif
+__host__ __device__ constexpr int keys_batch(int K) {
+    return K <= 5 ? 8 : K <= 10 ? FASTLSH_KEYS_B10 : FASTLSH_KEYS_B16;
+}
+
 __device__ __forceinline__ uint64_t mod61(uint64_t x) {  // x < 2^64 -> x mod (2^61 - 1)
     x = (x & P61) + (x >> 61);
     return x >= P61 ? x - P61 : x;
@@ -86,86 +107,123 @@ __device__ __forceinline__ uint64_t rotl61(uint64_t x, int j) {  // x < 2^61: x 
     return ((x << j) & P61) | (x >> (61 - j));
 }
 
-template <int K>
-__global__ void __launch_bounds__(128) keys_kernel_fast(const uint64_t* __restrict__ rmul,
+struct KeysShape {
+    int TPW, RPW, RB;
+};
+
+inline KeysShape keys_shape(int L, int K) {
+    // lanes busy = TPW * RPW of 32, table slots used = L / (groups * TPW): maximise the product
+    // (ties: larger TPW, fewer multiplier reloads)
+    const int B = keys_batch(K);
+    KeysShape best{1, 32, 32};
+    double best_eff = -1;
+    for (int tpw = 32; tpw >= 1; --tpw) {
+        const int rpw = 32 / tpw;
+        const int groups = (L + tpw - 1) / tpw;
+        const int step = rpw * B;
+        const int rb = step * ((32 + step - 1) / step);
+        const double eff = (double)(tpw * rpw) / 32.0 * (double)L / (double)(groups * tpw);
+        if (tpw * (rb + 1) <= kKeySlots && eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = KeysShape{tpw, rpw, rb};
+        }
+    }
+    return best;
+}
+
+template <int K, int V>
+__device__ __forceinline__ void load_codes(const int32_t* c, uint32_t (&u)[K]) {
+    if (K % 4 == 0 && V == 4) {  // 16-byte aligned runs: 128-bit loads
+#pragma unroll
+        for (int j = 0; j < K; j += 4) {
+            const int4 q = __ldg(reinterpret_cast<const int4*>(c + j));
+            u[j] = q.x; u[j + 1] = q.y; u[j + 2] = q.z; u[j + 3] = q.w;
+        }
+    } else if (K % 2 == 0 && V >= 2) {  // 8-byte aligned runs: 64-bit loads
+#pragma unroll
+        for (int j = 0; j < K; j += 2) {
+            const int2 q = __ldg(reinterpret_cast<const int2*>(c + j));
+            u[j] = q.x; u[j + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) u[j] = (uint32_t)__ldg(c + j);
+    }
+}
+
+#ifndef FASTLSH_KEYS_MINB
+#define FASTLSH_KEYS_MINB 1
+#endif
+template <int K, int V>
+__global__ void __launch_bounds__(128, FASTLSH_KEYS_MINB) keys_kernel_fast(const uint64_t* __restrict__ rmul,
                                                         const int32_t* __restrict__ codes, long long N,
                                                         int k, int L, uint64_t* __restrict__ out,
-                                                        long long ldk, int vec) {
-    __shared__ uint64_t s_key[4][32][33];  // [warp][table][row] (+1 pad)
+                                                        long long ldk, int TPW, int RB) {
+    constexpr int B = keys_batch(K);
+    __shared__ uint64_t s_key[4][kKeySlots];  // [warp][table * (RB + 1) + row]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // TPW tables per warp (lane % TPW), RPW = 32 / TPW rows per iteration (lane / TPW), so that
-    // every lane has work when L < 32
-    const int TPW = L >= 32 ? 32 : (L > 16 ? 32 : L > 8 ? 16 : L > 4 ? 8 : L > 2 ? 4 : L > 1 ? 2 : 1);
     const int RPW = 32 / TPW;
+    const bool lane_busy = lane < TPW * RPW;
     const int tl = lane % TPW, rsub = lane / TPW;
     const int groups = (L + TPW - 1) / TPW;
-    const long long rblocks = (N + 31) / 32;
+    const long long rblocks = (N + RB - 1) / RB;
     const long long items = rblocks * groups;
+    uint64_t* sk = s_key[warp];
     for (long long it = (long long)blockIdx.x * 4 + warp; it < items; it += (long long)gridDim.x * 4) {
         const int g = (int)(it % groups);
-        const long long v0 = (it / groups) * 32;
+        const long long v0 = (it / groups) * RB;
         const int l = g * TPW + tl;
-        const bool live_l = l < L;
+        const bool live_l = lane_busy && l < L;
+        const int lc = l < L ? l : L - 1;  // clamped: loads stay in range, results are dropped
         uint32_t r0[K], r1[K], r2[K];
-        uint64_t rc = 0;
-        if (live_l) {
-            rc = rmul[(size_t)l * (K + 1)];
+        const uint64_t rc = rmul[(size_t)lc * (K + 1)];
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const uint64_t r = rmul[(size_t)l * (K + 1) + j + 1];
-                r0[j] = (uint32_t)(r & 0x1fffff);
-                r1[j] = (uint32_t)((r >> 21) & 0x1fffff);
-                r2[j] = (uint32_t)(r >> 42);
-            }
+        for (int j = 0; j < K; ++j) {
+            const uint64_t r = rmul[(size_t)lc * (K + 1) + j + 1];
+            r0[j] = (uint32_t)(r & 0x1fffff);
+            r1[j] = (uint32_t)((r >> 21) & 0x1fffff);
+            r2[j] = (uint32_t)(r >> 42);
         }
-        const int rows = (int)min(32LL, N - v0);
-#pragma unroll 4
-        for (int rb = 0; rb < 32; rb += RPW) {
-            const int rr = rb + rsub;
-            uint64_t key = 0;
-            if (live_l && rr < rows) {
-                const int32_t* c = codes + (v0 + rr) * (long long)k + l * K;
-                uint32_t u[K];
-                if (K % 4 == 0 && vec == 4) {  // 16-byte aligned runs: 128-bit loads
+        const int rows = (int)min((long long)RB, N - v0);
+        for (int rb = 0; rb < RB; rb += RPW * B) {
+            uint32_t u[B][K];
 #pragma unroll
-                    for (int j = 0; j < K; j += 4) {
-                        const int4 q = __ldg(reinterpret_cast<const int4*>(c + j));
-                        u[j] = q.x; u[j + 1] = q.y; u[j + 2] = q.z; u[j + 3] = q.w;
-                    }
-                } else if (K % 2 == 0 && vec >= 2) {  // 8-byte aligned runs: 64-bit loads
+            for (int bb = 0; bb < B; ++bb) {
+                const int rr = rb + bb * RPW + rsub;
+                const int rcl = rr < rows ? rr : rows - 1;
+                load_codes<K, V>(codes + (v0 + rcl) * (long long)k + lc * K, u[bb]);
+            }
 #pragma unroll
-                    for (int j = 0; j < K; j += 2) {
-                        const int2 q = __ldg(reinterpret_cast<const int2*>(c + j));
-                        u[j] = q.x; u[j + 1] = q.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < K; ++j) u[j] = (uint32_t)__ldg(c + j);
-                }
+            for (int bb = 0; bb < B; ++bb) {
+                const int rr = rb + bb * RPW + rsub;
                 uint64_t s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
-                    s0 += (uint64_t)r0[j] * u[j];
-                    s1 += (uint64_t)r1[j] * u[j];
-                    s2 += (uint64_t)r2[j] * u[j];
+                    s0 += (uint64_t)r0[j] * u[bb][j];
+                    s1 += (uint64_t)r1[j] * u[bb][j];
+                    s2 += (uint64_t)r2[j] * u[bb][j];
                 }
-                key = mod61(rc + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
+                const uint64_t key = mod61(rc + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
+                if (live_l && rr < rows) sk[tl * (RB + 1) + rr] = key;
             }
-            s_key[warp][tl][rr] = key;
         }
         __syncwarp();
         for (int t = 0; t < TPW; ++t) {
             const int lt = g * TPW + t;
-            if (lt < L && lane < rows) out[(long long)lt * ldk + v0 + lane] = s_key[warp][t][lane];
+            if (lt >= L) break;
+            for (int r = lane; r < rows; r += 32) out[(long long)lt * ldk + v0 + r] = sk[t * (RB + 1) + r];
         }
         __syncwarp();
     }
 }
 
-typedef void (*FastKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long, int);
-FastKeysFn fast_keys_for(int K) {
+typedef void (*FastKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long, int, int);
+// vector width V of the per-(row, table) code runs: 4 when every run is 16-byte aligned, 2 when
+// 8-byte aligned, else 1
+FastKeysFn fast_keys_for(int K, int V) {
     switch (K) {
-#define FASTLSH_KCASE(X) case X: return keys_kernel_fast<X>;
+#define FASTLSH_KCASE(X) \
+    case X: return V == 4 && X % 4 == 0 ? keys_kernel_fast<X, 4> : V >= 2 && X % 2 == 0 ? keys_kernel_fast<X, 2> : keys_kernel_fast<X, 1>;
         FASTLSH_KCASE(1) FASTLSH_KCASE(2) FASTLSH_KCASE(3) FASTLSH_KCASE(4) FASTLSH_KCASE(5) FASTLSH_KCASE(6)
         FASTLSH_KCASE(7) FASTLSH_KCASE(8) FASTLSH_KCASE(9) FASTLSH_KCASE(10) FASTLSH_KCASE(11) FASTLSH_KCASE(12)
         FASTLSH_KCASE(13) FASTLSH_KCASE(14) FASTLSH_KCASE(15) FASTLSH_KCASE(16)
@@ -180,19 +238,18 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
                                  const int32_t* codes, int64_t N, int32_t k, uint64_t* out,
                                  int64_t ldk, cudaStream_t stream) {
     const int L = keys->L, K = keys->K;
-    if (FastKeysFn fk = fast_keys_for(K)) {  // K <= 16: register-resident limbs (above)
+    const uintptr_t base = reinterpret_cast<uintptr_t>(codes);
+    const int vec = (k % 4 == 0 && K % 4 == 0 && base % 16 == 0) ? 4 : (k % 2 == 0 && K % 2 == 0 && base % 8 == 0) ? 2 : 1;
+    if (FastKeysFn fk = fast_keys_for(K, vec)) {  // K <= 16: register-resident limbs (above)
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const long long items = ((N + 31) / 32) * ((L + 31) / 32);
+        const KeysShape sh = keys_shape(L, K);
+        const long long items = ((N + sh.RB - 1) / sh.RB) * ((L + sh.TPW - 1) / sh.TPW);
         long long blocks = (items + 3) / 4;
         const long long cap = (long long)sms * 16;
         if (blocks > cap) blocks = cap;
-        // vector width of the per-(row, table) code runs: 4 when every run is 16-byte aligned,
-        // 2 when 8-byte aligned, else 1
-        const uintptr_t base = reinterpret_cast<uintptr_t>(codes);
-        const int vec = (k % 4 == 0 && K % 4 == 0 && base % 16 == 0) ? 4 : (k % 2 == 0 && K % 2 == 0 && base % 8 == 0) ? 2 : 1;
-        fk<<<(unsigned)blocks, 128, 0, stream>>>(dev_r, codes, N, k, L, out, ldk, vec);
+        fk<<<(unsigned)blocks, 128, 0, stream>>>(dev_r, codes, N, k, L, out, ldk, sh.TPW, sh.RB);
         cudaError_t e = cudaGetLastError();
         return e == cudaSuccess ? FASTLSH_OK : set_cuda_error(e);
     }
