@@ -132,6 +132,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.w = p->w;
     a.k = p->k;
     a.P = pk.parts;
+    a.direct = (pk.direct && !fused) ? 1 : 0;
     a.W = pk.warps;
     a.HB = pk.hash_blocks;
     a.kb_max = pk.kb_max;

@@ -62,6 +62,7 @@ struct GatherArgs {
     int L, K, tables_max;
     uint64_t* keys;      // [L][ldk]
     long long ldk;
+    int direct;          // P == 1 with warp-contiguous hashes: quantise straight from the registers
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -324,6 +325,14 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
     const float w = a.w;
     const float inv_w = 1.0f / w;
     const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
+    // direct epilogue: this lane's hash (-1: padding lane) and its offset b
+    int my_h = -1;
+    float my_b = 0.f;
+    if (!fused && a.direct) {
+        for (int h = 0; h < kb; ++h)
+            if (s_unit[h] == tid) my_h = h;
+        if (my_h >= 0) my_b = s_b[my_h];
+    }
 
     // epilogue of iteration je: sum parts, quantise, store (one hash per thread, 4*RG rows)
     auto epilogue = [&](long long je) {
@@ -477,6 +486,48 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
                 issue_group<RG>(a, group_of(jn), land0 + l * land_bytes, LFULL(l));
             }
         }
+        if (!fused && a.direct) {  // P == 1: this lane holds whole projections, quantise them here
+            const long long row0 = group_of(j) * (4 * RG);
+            const int nrows = live_rows(a.N, row0, 4 * RG);
+            if (my_h >= 0) {
+                const long long o0 = row0 * a.k + h0 + my_h;
+#pragma unroll
+                for (int u = 0; u < RG; ++u) {
+                    if (a.proj) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            if (4 * u + r < nrows) a.proj[o0 + (long long)(4 * u + r) * a.k] = acc[u][r];
+                        continue;
+                    }
+                    int code[4];
+                    bool bad = false;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const float num = __fadd_rn(acc[u][r], my_b);
+                        const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                        const float f = floorf(qv);
+                        code[r] = (int)f;
+                        bad |= !(f > -2147483648.0f && f < 2147483648.0f);
+                    }
+                    if (bad) {  // rare: sentinel + count (rows past N are not counted)
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const float num = __fadd_rn(acc[u][r], my_b);
+                            const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                            const float f = floorf(qv);
+                            if (!(f > -2147483648.0f && f < 2147483648.0f)) {
+                                code[r] = INT_MIN;
+                                if (4 * u + r < nrows) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (4 * u + r < nrows) a.codes[o0 + (long long)(4 * u + r) * a.k] = code[r];
+                }
+            }
+            continue;
+        }
         // 4. publish this lane's partials for group j
         const int d = (int)(j % kPartSlots);
         if (j >= kPartSlots) mbar_wait(PEMPTY(d), (uint32_t)(((j - kPartSlots) / kPartSlots) & 1));
@@ -489,7 +540,7 @@ __global__ void __launch_bounds__((MS <= 32 ? 512 : 256), 1) gather_kernel(const
         // 6. fused keys of group j-2 (its codes are complete in shared memory)
         if (fused && j >= 2) build_keys(j - 2);
     }
-    if (iters >= 1) epilogue(iters - 1);
+    if (iters >= 1 && (fused || !a.direct)) epilogue(iters - 1);
     if (fused) {
         if (iters >= 2) build_keys(iters - 2);
         if (iters >= 1) build_keys(iters - 1);

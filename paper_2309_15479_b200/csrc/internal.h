@@ -42,6 +42,10 @@ struct Packing {
     std::vector<uint16_t> unit_lane;  // [HB][kb_max][parts]: lane id (warp*32+lane) of each part
     double efficiency = 0;       // useful slots / (lanes * MS) over all warps
     int64_t conflict_wavefronts = 0;  // extra wavefronts per stage (all blocks) beyond 4 per LDS
+    // direct epilogue (parts == 1): warp w of a block holds hashes [32w, 32w+32) of the block, so
+    // each lane quantises its own sums and the warp's code stores are contiguous runs (no
+    // partial-sum round trip through shared memory)
+    int direct = 0;
 };
 
 // GPU packing for the TMEM kernel K1t (gather_tmem.cu). Hash block hb serves

@@ -298,7 +298,8 @@ struct Trial {
     double cost = 1e300;
 };
 
-void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out, int ms_cap) {
+void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out, int ms_cap, bool direct = false) {
+    direct = direct && P == 1;
     const int n = p.n, m = p.m, k = p.k;
     Packing pk;
     pk.parts = P;
@@ -353,8 +354,23 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out, int ms
                 units.push_back(std::move(u));
             }
         }
-        auto qs = group_units(units, Q, dmax);
-        if (P <= 4) exchange_slots(units, qs, P, dmax);  // matters (and is cheap) for few parts
+        std::vector<QuarterState> qs;
+        if (direct) {  // quarters of warp w take units (= hashes, P = 1) [32w, 32w+32) only
+            qs.resize(Q);
+            for (int w = 0; w < Wn; ++w) {
+                const int u0 = 32 * w, u1 = std::min<int>((int)units.size(), u0 + 32);
+                if (u0 >= u1) continue;
+                std::vector<Unit> sub(units.begin() + u0, units.begin() + u1);
+                auto sq = group_units(sub, 4, dmax);
+                for (int qi = 0; qi < 4; ++qi) {
+                    for (int& mbr : sq[qi].members) mbr += u0;
+                    qs[4 * w + qi] = std::move(sq[qi]);
+                }
+            }
+        } else {
+            qs = group_units(units, Q, dmax);
+            if (P <= 4) exchange_slots(units, qs, P, dmax);  // matters (and is cheap) for few parts
+        }
         plans[bl].resize(Q);
         for (int q = 0; q < Q; ++q) {
             auto& qp = plans[bl][q];
@@ -506,7 +522,11 @@ void try_parts(const fastlsh_params& p, int P, int lanes_cap, Trial& out, int ms
     // rows -> HB*W*MS per row (+ scheduler conflicts); staging = landing read + transposed write of
     // the row per hash block -> HB*n/16; epilogue partial traffic ~ k*P/4. The pipe reaches ~98%
     // with 16 warps/SM (MS <= 32: <= 128 registers) but ~75% with 8 warps/SM (MS > 32).
-    const double wf = (double)HB * Wn * MS + (double)conflicts / 4.0 + (double)HB * p.n / 16.0 + p.k * P / 4.0;
+    // The direct epilogue (P = 1) replaces the partial-sum traffic and item loop by one store per
+    // lane and row.
+    pk.direct = direct ? 1 : 0;
+    const double epi = direct ? p.k / 16.0 : p.k * P / 4.0;
+    const double wf = (double)HB * Wn * MS + (double)conflicts / 4.0 + (double)HB * p.n / 16.0 + epi;
     const double rate = MS <= 32 ? 0.98 : 0.75;
     out.cost = wf / rate;
     out.pk = std::move(pk);
@@ -532,6 +552,7 @@ void build_packing(const fastlsh_params& p, Packing& out) {
         int v = std::atoi(e);
         if (v >= 1 && v <= 16) warps_force = v;
     }
+    const bool no_direct = std::getenv("FASTLSH_NO_DIRECT") != nullptr;  // experiment knob
     Trial best;
     for (int P : cands) {
         // beyond 256 lanes per hash the block holds a single hash; keep P <= 256
@@ -539,13 +560,15 @@ void build_packing(const fastlsh_params& p, Packing& out) {
         // 16 warps per CTA when the slots fit 128 registers per lane (MS <= 32), else 8
         for (int cap : {0, -1}) {  // padded slots, or slots capped at the part size with folding
             if (cap < 0 && P > 8) break;  // many parts: padding is already small
-            Trial t;
-            try_parts(p, P, (warps_force ? warps_force : 16) * 32, t, cap);
-            if (!warps_force && t.pk.slots > 32) {
-                t = Trial();
-                try_parts(p, P, 8 * 32, t, cap);
+            for (int direct = 0; direct <= (P == 1 && !no_direct ? 1 : 0); ++direct) {
+                Trial t;
+                try_parts(p, P, (warps_force ? warps_force : 16) * 32, t, cap, direct);
+                if (!warps_force && t.pk.slots > 32) {
+                    t = Trial();
+                    try_parts(p, P, 8 * 32, t, cap, direct);
+                }
+                if (t.cost < best.cost) best = std::move(t);
             }
-            if (t.cost < best.cost) best = std::move(t);
         }
     }
     out = std::move(best.pk);
