@@ -193,6 +193,30 @@ def test_epilogue_partial_reads_conflict_free(lib, n, m, k):
                 assert len(set(pos.tolist())) == len(pos), (bl, o, q, pos)
 
 
+@pytest.mark.parametrize("n,m,k", [(128, 16, 256), (128, 16, 64), (128, 16, 77)])
+def test_direct_packing_warp_contiguous(lib, n, m, k):
+    """One-part packings take the direct epilogue (packer.cpp, gather_impl.cuh): warp w of a block
+    holds exactly the hashes [32w, 32w+32) of the block, so its code stores are contiguous runs;
+    with FASTLSH_NO_DIRECT the packer may place hashes in any warp."""
+    import os
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import fastlsh_arrays
+    idx, a, b = fastlsh_arrays(n, m, k, 1.0, 3)
+    pk = fl.Params.from_arrays(n, 1.0, idx, a, b).packing()
+    assert pk["parts"] == 1
+    for bl in range(pk["hash_blocks"]):
+        kb = int(pk["block_kb"][bl])
+        lanes = pk["unit_lane"][bl, :kb, 0].astype(np.int64)
+        assert (lanes // 32 == np.arange(kb) // 32).all()
+        assert len(set(lanes.tolist())) == kb
+    os.environ["FASTLSH_NO_DIRECT"] = "1"
+    try:
+        pk2 = fl.Params.from_arrays(n, 1.0, idx, a, b).packing()
+    finally:
+        del os.environ["FASTLSH_NO_DIRECT"]
+    assert pk2["slots"] <= pk["slots"]  # the unconstrained grouping never needs more slots
+
+
 def test_table_query_transform_argument_checks(lib):
     """Size/pointer validation of the table, query and transform entry points happens before any
     device work (EINVAL, no crash); valid calls without a B200 fail loudly, never on the CPU."""
