@@ -57,7 +57,8 @@ typedef struct {
     double bank_efficiency;    /* useful gathers / (lanes * slots) over all warps                 */
     int64_t conflict_wavefronts; /* extra smem wavefronts per row left by the scheduler          */
     int32_t kernel;            /* hashing kernel for 16-B aligned X: 1 = shared-memory gather K1,
-                                  2 = tensor-memory gather K1t                 */
+                                  2 = tensor-memory gather K1t,
+                                  3 = row-major gather K1r                     */
     int32_t tmem_hash_blocks;  /* K1t: CTAs hash blocks (0 when K1t does not apply)              */
     int32_t tmem_hashes_per_warp; /* K1t: hashes (register accumulator pairs) per warp           */
 } fastlsh_params_info_t;
@@ -101,6 +102,16 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* p, int32_t* sizes, u
                                       float* coef, uint16_t* unit_lane, int32_t* block_h0,
                                       int32_t* block_kb);
 
+/* Diagnostic: copy the K1r packing out (rpacker.cpp).
+ * sizes[0..7] = {ok, parts P, slots MS, warps W, hash_blocks HB, kb_max, staged row stride S
+ * (words), conflict wavefronts per row}. When ok == 0 nothing else is written. Arrays (any may be
+ * NULL): offp u32[HB*W*(MS/2)*32] (two 16-bit byte offsets into a staged row: bits 0-15 slot 2t,
+ * bits 16-31 slot 2t+1), coef f32[HB*W*MS*32], lane_hash int16[HB*W*32] (block-local hash of the
+ * lane's part, -1 idle; parts of hash slot j sit in lanes j + (32/P)q), block_h0/block_kb int32[HB]. */
+fastlsh_status fastlsh_params_row_packing(const fastlsh_params* p, int32_t* sizes, uint32_t* offp,
+                                          float* coef, int16_t* lane_hash, int32_t* block_h0,
+                                          int32_t* block_kb);
+
 /* Hint that keys of K consecutive codes will be built from these params: the GPU
  * packing then keeps whole tables inside each CTA hash block, which lets fastlsh_hash_keys build
  * the keys in the hashing kernel's epilogue (codes are still written). Must be called before the
@@ -113,13 +124,14 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 /* ---- hashing ----------------------------------------------------------- */
 
-/* Choose the hashing kernel of these params (both compute Eq. 5, with the same
+/* Choose the hashing kernel of these params (all compute Eq. 5, with the same
  * epilogue; only the summation order of the fp32 projection differs, within the same bound):
- *   0 = automatic (default): the tensor-memory gather K1t when it applies — n % 4 == 0, m <= 128,
- *       the packed records fit in shared memory, X 16-byte aligned — else the shared-memory K1;
- *   1 = always the shared-memory gather K1;
- *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED).
- * EINVAL for other values; EUNSUPPORTED for 2 when K1t cannot serve the params at all. */
+ *   0 = automatic (default): the row-major gather K1r when its packing exists and its cost model
+ *       beats K1's, for calls with n % 4 == 0 and X 16-byte aligned; else the shared-memory K1;
+ *   1 = always the shared-memory gather K1 (column-interleaved stages, LDS.128);
+ *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED);
+ *   3 = always K1r (row-major stages, LDS.32; likewise EUNSUPPORTED when it cannot serve).
+ * EINVAL for other values; EUNSUPPORTED for 2 or 3 when that kernel cannot serve the params. */
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
 
 /* codes[r*k + i] = floor((a_i . S_i(X[r]) + b_i) / w) as int32, for r < N, i < k — Eq. 5.

@@ -19,6 +19,7 @@ OK, EINVAL, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5
 EXPORTED = [
     "fastlsh_params_create", "fastlsh_params_create_from_arrays", "e2lsh_params_create",
     "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
+    "fastlsh_params_row_packing",
     "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
@@ -72,6 +73,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_params_set_kernel": [P, i32],
         "fastlsh_params_set_table_size": [P, i32],
         "fastlsh_params_packing": [P, P, P, P, P, P, P],
+        "fastlsh_params_row_packing": [P, P, P, P, P, P, P],
         "fastlsh_hash": [P, P, i64, P, P],
         "fastlsh_project": [P, P, i64, P, P],
         "e2lsh_hash": [P, P, i64, P, i32, P],
@@ -198,10 +200,29 @@ class Params:
                     offp=offp.reshape(HB, W, MS, 32), coef=coef.reshape(HB, W, MS, 32),
                     unit_lane=unit.reshape(HB, kbm, P), block_h0=h0, block_kb=kb)
 
+    def row_packing(self) -> dict | None:
+        """The K1r layout (diagnostic; see fastlsh_params_row_packing); None when K1r does not apply."""
+        sz = np.zeros(8, np.int32)
+        _check(self._lib.fastlsh_params_row_packing(self._h, _np_ptr(sz), None, None, None, None, None),
+               "fastlsh_params_row_packing")
+        ok, P, MS, W, HB, kbm, S, conf = (int(x) for x in sz)
+        if not ok:
+            return None
+        offp = np.zeros(HB * W * (MS // 2) * 32, np.uint32)
+        coef = np.zeros(HB * W * MS * 32, np.float32)
+        lh = np.zeros(HB * W * 32, np.int16)
+        h0 = np.zeros(HB, np.int32)
+        kb = np.zeros(HB, np.int32)
+        _check(self._lib.fastlsh_params_row_packing(self._h, _np_ptr(sz), _np_ptr(offp), _np_ptr(coef), _np_ptr(lh),
+                                                    _np_ptr(h0), _np_ptr(kb)), "fastlsh_params_row_packing")
+        return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, S=S, conflicts=conf,
+                    offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
+                    lane_hash=lh.reshape(HB, W, 32), block_h0=h0, block_kb=kb)
+
     def set_kernel(self, kernel):
-        """Pin the hashing kernel: "auto" (0), "smem" (1, K1) or "tmem" (2, K1t); see
-        fastlsh_params_set_kernel. Returns self."""
-        code = {"auto": 0, "smem": 1, "tmem": 2}.get(kernel, kernel)
+        """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t) or "rows" (3, K1r);
+        see fastlsh_params_set_kernel. Returns self."""
+        code = {"auto": 0, "smem": 1, "tmem": 2, "rows": 3}.get(kernel, kernel)
         _check(self._lib.fastlsh_params_set_kernel(self._h, int(code)), "fastlsh_params_set_kernel")
         return self
 

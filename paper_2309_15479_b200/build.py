@@ -17,7 +17,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [*os.environ.get("FASTLSH_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 SOURCES = ["api.cu", "gather.cu", "gather_inst0.cu", "gather_inst1.cu", "gather_inst2.cu", "gather_inst3.cu",
-           "gather_tmem.cu", "tables.cu", "query.cu", "transforms.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp"]
+           "gather_tmem.cu", "tables.cu", "query.cu", "transforms.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp",
+           "gather_rows.cu", "gather_rows_inst0.cu", "gather_rows_inst1.cu", "gather_rows_inst2.cu",
+           "gather_rows_inst3.cu", "gather_rows_inst4.cu", "gather_rows_inst5.cu", "rpacker.cpp"]
 
 
 def _stale(out: str, deps) -> bool:
@@ -27,16 +29,29 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _deps(path: str, seen=None) -> list:
+    """The file and every local header it includes (transitively)."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return []
+    seen.add(path)
+    out = [path]
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("#include \""):
+            inc = line.split('"')[1]
+            out += _deps(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
-    headers.append(os.path.join(ROOT, "include", "fastlsh.h"))
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
-        if force or _stale(o, [s] + headers):
+        if force or _stale(o, _deps(s)):
             lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
             jobs.append([NVCC, *ARCH, *COMMON, *lang, "-c", s, "-o", o] +
                         (["-Xptxas", "-v"] if verbose and src.endswith(".cu") else []))

@@ -82,6 +82,7 @@ fastlsh_status ensure_packed(fastlsh_params* p) {
     if (p->pack.slots <= 0) return FASTLSH_EUNSUPPORTED;
     try {
         if (!p->is_e2lsh) build_tmem_packing(*p, p->tpack);
+        build_row_packing(*p, p->rpack);
     } catch (...) {
         return FASTLSH_ENOMEM;
     }
@@ -104,6 +105,7 @@ void free_device_copy(DeviceCopy& d) {
     cudaFree(d.block_h0); cudaFree(d.block_kb); cudaFree(d.flags);
     cudaFree(d.dense_hi); cudaFree(d.dense_lo);
     cudaFree(d.t_recs); cudaFree(d.t_counts); cudaFree(d.t_offs); cudaFree(d.t_hinfo); cudaFree(d.t_groups);
+    cudaFree(d.r_offp); cudaFree(d.r_coef); cudaFree(d.r_lane_hash); cudaFree(d.r_block_h0); cudaFree(d.r_block_kb);
     for (int i = 0; i < 2; ++i) {
         cudaFree(d.ws_x[i]); cudaFree(d.ws_codes[i]); cudaFree(d.ws_keys[i]);
         if (d.ws_stream[i]) cudaStreamDestroy(d.ws_stream[i]);
@@ -120,11 +122,25 @@ constexpr bool kAutoTmem = false;  // K1t is still slower than K1 on the bench w
 bool tmem_selected(const fastlsh_params* p) {
     return p->kernel == 2 || (p->kernel == 0 && kAutoTmem && p->tpack.ok);
 }
+// K1r (row-major stages) serves the call when pinned (kernel 3) or, in auto mode, when its packing
+// exists and its modelled cost is below K1's (K1's model omits its transposition stalls: the
+// measured ratio is applied). Calls K1r cannot serve (n % 4 != 0, X not 16-B aligned) go to K1.
+constexpr double kK1Derate = 1.25;
+bool rows_selected(const fastlsh_params* p) {
+    if (!p->rpack.ok) return false;
+    if (p->kernel == 3) return true;
+    if (p->n % 4) return false;  // rows are not 16-byte multiples: no bulk row copies
+    return p->kernel == 0 && p->rpack.cost <= p->pack.cost * kK1Derate;
+}
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
     if (tmem_selected(p)) {
         fastlsh_status st = launch_gather_tmem(p, d, X, N, codes, proj, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 2) return st;
+    }
+    if (p->kernel == 3 || rows_selected(p)) {
+        fastlsh_status st = launch_gather_rows(p, d, X, N, codes, proj, stream);
+        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 3) return st;
     }
     return launch_gather(p, d, X, N, codes, proj, stream);
 }
@@ -244,7 +260,7 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
-    info->kernel = tmem_selected(p) ? 2 : 1;
+    info->kernel = tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
     info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
     info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
@@ -269,6 +285,30 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* cp, int32_t* sizes, 
     if (offp) std::memcpy(offp, pk.offp.data(), pk.offp.size() * sizeof(uint32_t));
     if (coef) std::memcpy(coef, pk.coef.data(), pk.coef.size() * sizeof(float));
     if (unit_lane) std::memcpy(unit_lane, pk.unit_lane.data(), pk.unit_lane.size() * sizeof(uint16_t));
+    if (block_h0) for (size_t i = 0; i < pk.block_h0.size(); ++i) block_h0[i] = pk.block_h0[i];
+    if (block_kb) for (size_t i = 0; i < pk.block_kb.size(); ++i) block_kb[i] = pk.block_kb[i];
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_row_packing(const fastlsh_params* cp, int32_t* sizes, uint32_t* offp, float* coef,
+                                          int16_t* lane_hash, int32_t* block_h0, int32_t* block_kb) {
+    if (!cp) return FASTLSH_EINVAL;
+    fastlsh_params* p = const_cast<fastlsh_params*>(cp);
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        fastlsh_status st = ensure_packed(p);
+        if (st != FASTLSH_OK) return st;
+    }
+    const RPacking& pk = p->rpack;
+    if (sizes) {
+        sizes[0] = pk.ok ? 1 : 0; sizes[1] = pk.parts; sizes[2] = pk.slots; sizes[3] = pk.warps;
+        sizes[4] = pk.hash_blocks; sizes[5] = pk.kb_max; sizes[6] = pk.S;
+        sizes[7] = (int32_t)pk.conflict_wavefronts;
+    }
+    if (!pk.ok) return FASTLSH_OK;
+    if (offp) std::memcpy(offp, pk.offp.data(), pk.offp.size() * sizeof(uint32_t));
+    if (coef) std::memcpy(coef, pk.coef.data(), pk.coef.size() * sizeof(float));
+    if (lane_hash) std::memcpy(lane_hash, pk.lane_hash.data(), pk.lane_hash.size() * sizeof(int16_t));
     if (block_h0) for (size_t i = 0; i < pk.block_h0.size(); ++i) block_h0[i] = pk.block_h0[i];
     if (block_kb) for (size_t i = 0; i < pk.block_kb.size(); ++i) block_kb[i] = pk.block_kb[i];
     return FASTLSH_OK;
@@ -314,7 +354,12 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
                          (st = upload_vec(&d.t_counts, p->tpack.counts, s)) != FASTLSH_OK ||
                          (st = upload_vec(&d.t_offs, p->tpack.offs, s)) != FASTLSH_OK ||
                          (st = upload_vec(&d.t_hinfo, p->tpack.hinfo, s)) != FASTLSH_OK ||
-                         (st = upload_vec(&d.t_groups, p->tpack.groups, s)) != FASTLSH_OK))) {
+                         (st = upload_vec(&d.t_groups, p->tpack.groups, s)) != FASTLSH_OK)) ||
+        (p->rpack.ok && ((st = upload_vec(&d.r_offp, p->rpack.offp, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.r_coef, p->rpack.coef, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.r_lane_hash, p->rpack.lane_hash, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.r_block_h0, p->rpack.block_h0, s)) != FASTLSH_OK ||
+                         (st = upload_vec(&d.r_block_kb, p->rpack.block_kb, s)) != FASTLSH_OK))) {
         free_device_copy(d);
         return st;
     }
@@ -331,11 +376,12 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
-    if (!p || kernel < 0 || kernel > 2) return FASTLSH_EINVAL;
+    if (!p || kernel < 0 || kernel > 3) return FASTLSH_EINVAL;
     std::lock_guard<std::mutex> g(p->mu);
     fastlsh_status st = ensure_packed(p);
     if (st != FASTLSH_OK) return st;
     if (kernel == 2 && !p->tpack.ok) return FASTLSH_EUNSUPPORTED;
+    if (kernel == 3 && !p->rpack.ok) return FASTLSH_EUNSUPPORTED;
     p->kernel = kernel;
     return FASTLSH_OK;
 }

@@ -1,0 +1,98 @@
+// gather_rows.cu — launcher of K1r, the row-major FastLSH hashing kernel (gather_rows.cuh;
+// DESIGN.md "K1r", Eq. 5).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "internal.h"
+
+#include "gather_rows.cuh"
+
+namespace fastlsh {
+namespace k1r {
+
+RowKernelFn select_row_kernel(int MS, int cls) {
+    typedef RowKernelFn (*UnitFn)(int, int);
+    static const UnitFn units[] = {row_kernel_ms_0, row_kernel_ms_1, row_kernel_ms_2,
+                                   row_kernel_ms_3, row_kernel_ms_4, row_kernel_ms_5};
+    for (UnitFn u : units)
+        if (RowKernelFn f = u(MS, cls)) return f;
+    return nullptr;
+}
+
+// stages + kCodeBufs code buffers + barriers + b
+size_t row_smem_bytes(const RPacking& pk) {
+    const RClass c = kRClasses[pk.cls];
+    const int kbp = (pk.kb_max + 3) & ~3;
+    return (size_t)c.NS * c.R * c.S * 4 + (size_t)kCodeBufs * c.R * kbp * 4 + (size_t)(2 * c.NS + 2 * kCodeBufs) * 8 +
+           (size_t)kbp * 4;
+}
+
+}  // namespace k1r
+
+using namespace k1r;
+
+fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
+                                  int32_t* codes, float* proj, cudaStream_t stream) {
+    const RPacking& pk = p->rpack;
+    if (!pk.ok || !d.r_offp) return FASTLSH_EUNSUPPORTED;
+    // TMA bulk row copies need 16-byte aligned rows
+    if ((p->n % 4) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
+    constexpr size_t kSmemMax = 227 * 1024;
+    const int threads = pk.warps * 32;
+    const size_t smem = row_smem_bytes(pk);
+    if (smem > kSmemMax) return FASTLSH_EUNSUPPORTED;
+    const int R = kRClasses[pk.cls].R;
+    RowKernelFn fn = select_row_kernel(pk.slots, pk.cls);
+    if (!fn) return FASTLSH_EUNSUPPORTED;
+    RowArgs a;
+    a.X = X;
+    a.N = N;
+    a.n = p->n;
+    a.S = pk.S;
+    a.offp = d.r_offp;
+    a.coef = d.r_coef;
+    a.lane_hash = d.r_lane_hash;
+    a.b = d.b;
+    a.block_h0 = d.r_block_h0;
+    a.block_kb = d.r_block_kb;
+    a.w = p->w;
+    a.k = p->k;
+    a.P = pk.parts;
+    a.W = pk.warps;
+    a.HB = pk.hash_blocks;
+    a.kbp = (pk.kb_max + 3) & ~3;
+    a.groups = (N + R - 1) / R;
+    a.codes = codes;
+    a.proj = proj;
+    a.flags = d.flags;
+    const void* out = proj ? static_cast<const void*>(proj) : static_cast<const void*>(codes);
+    bool blocks_aligned = true;
+    for (int bl = 0; bl < pk.hash_blocks; ++bl)
+        if ((pk.block_h0[bl] % 4) || (pk.block_kb[bl] % 4)) blocks_aligned = false;
+    a.bulk = (p->k % 4 == 0) && blocks_aligned && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
+    if (std::getenv("FASTLSH_NO_BULK_STORE")) a.bulk = 0;  // experiment knob (and fallback test)
+    a.whole = (a.bulk && pk.hash_blocks == 1 && a.kbp == p->k) ? 1 : 0;
+
+    cudaError_t e =
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, smem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+    // persistent grid: as many row streams per hash block as fit resident at once
+    long long gpr = (long long)sms * per_sm / pk.hash_blocks;
+    if (gpr > a.groups) gpr = a.groups;
+    if (gpr < 1) gpr = 1;
+    const long long grid = gpr * pk.hash_blocks;
+    fn<<<(unsigned)grid, threads, smem, stream>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e);
+    return FASTLSH_OK;
+}
+
+}  // namespace fastlsh

@@ -41,6 +41,7 @@ struct Packing {
     std::vector<float> coef;     // [HB][W][MS][32]
     std::vector<uint16_t> unit_lane;  // [HB][kb_max][parts]: lane id (warp*32+lane) of each part
     double efficiency = 0;       // useful slots / (lanes * MS) over all warps
+    double cost = 1e300;         // modelled shared-memory wavefronts per row / pipe rate
     int64_t conflict_wavefronts = 0;  // extra wavefronts per stage (all blocks) beyond 4 per LDS
     // direct epilogue (parts == 1): warp w of a block holds hashes [32w, 32w+32) of the block, so
     // each lane quantises its own sums and the warp's code stores are contiguous runs (no
@@ -70,8 +71,42 @@ struct TPacking {
     double balance = 0;            // critical-path slots / mean slots per warp (>= 1)
 };
 
+// GPU packing for the row-major kernel K1r (gather_rows.cuh). Stages hold rows
+// row-major at a stride of S words (S = 32*ceil(n/32) + 32; the last 32 words of every staged row
+// are zero, one per bank, read by padding slots), so a coordinate's bank is idx mod 32 in every
+// row and TMA bulk copies fill the stages directly. Hash block hb serves hashes [h0, h0+kb); a
+// block's W warps hold hpw = 32/P hashes each, hash slot j of a warp in lanes j + hpw*q (q < P
+// parts, summed by an xor butterfly), and the hash in slot j is congruent to j mod hpw so that the
+// code stores of a warp hit distinct banks. At every slot position the 32 lanes of a warp read 32
+// distinct banks (König colouring of lanes x banks), so one LDS.32 per slot and row is one
+// wavefront. Slots are packed two per register (16-bit byte offsets within a row).
+constexpr int kRMaxSlots = 128;
+// Stage geometry per row-stride class (compile-time in the kernel, so the R rows of a stage are
+// immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages.
+struct RClass { int S, R, NS; };
+constexpr RClass kRClasses[] = {{160, 8, 8}, {288, 8, 8}, {544, 8, 6}, {1056, 8, 4}, {2080, 4, 4}, {4128, 4, 3}};
+constexpr int kNumRClasses = 6;
+struct RPacking {
+    bool ok = false;
+    int parts = 1, slots = 0, warps = 0, hash_blocks = 0, kb_max = 0, S = 0, cls = 0;
+    std::vector<int> block_h0, block_kb;
+    std::vector<uint32_t> offp;     // [HB][W][MS/2][32]: bits 0-15 slot 2t, bits 16-31 slot 2t+1
+    std::vector<float> coef;        // [HB][W][MS][32]
+    std::vector<int16_t> lane_hash; // [HB][W*32]: block-local hash of the lane's part, -1 = idle
+    double efficiency = 0;          // useful slots / (lanes * MS)
+    int64_t conflict_wavefronts = 0;  // extra wavefronts per row (all blocks) beyond 1 per LDS.32
+    double cost = 1e300;            // modelled shared-memory wavefronts per row / pipe rate
+};
+// true when K1r can hash rows of this params object (packing exists) — X alignment is per call
+void build_row_packing(const fastlsh_params& p, RPacking& out);
+
 struct DeviceCopy {
     bool ready = false;
+    uint32_t* r_offp = nullptr;           // K1r packing (RPacking), when applicable
+    float* r_coef = nullptr;
+    int16_t* r_lane_hash = nullptr;
+    int32_t* r_block_h0 = nullptr;
+    int32_t* r_block_kb = nullptr;
     uint32_t* offp = nullptr;
     float* coef = nullptr;
     uint16_t* unit_lane = nullptr;
@@ -110,8 +145,9 @@ struct fastlsh_params {
     std::vector<float> b;      // [k]
     fastlsh::Packing pack;
     fastlsh::TPacking tpack;
+    fastlsh::RPacking rpack;
     bool packed = false;
-    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 shared-memory K1, 2 TMEM K1t
+    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 K1, 2 TMEM K1t, 3 row-major K1r
     int32_t table_align = 1;   // hash blocks hold whole tables of this many hashes (fused keys)
     fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
     std::mutex mu;
@@ -128,6 +164,10 @@ namespace fastlsh {
 
 // packer.cpp
 void build_packing(const fastlsh_params& p, Packing& out);
+// König edge colouring of a bipartite multigraph with ncol >= max degree colours; edge e joins
+// left[e] and right[e]; returns each edge's colour (all -1 if ncol is too small)
+std::vector<int> color_bipartite(const std::vector<int>& left, const std::vector<int>& right, int nleft,
+                                 int nright, int ncol);
 
 // gather.cu
 struct FusedKeys {            // compound keys built in the hashing kernel's epilogue
@@ -144,6 +184,9 @@ bool keys_fusable(const fastlsh_params* p, const fastlsh_keys* keys);
 // gather_tmem.cu
 void build_tmem_packing(const fastlsh_params& p, TPacking& out);
 fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, const float* X,
+                                  int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+// gather_rows.cu
+fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                                   int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
 // the hashing dispatcher (api.cu): K1t when selected/applicable, else K1
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,

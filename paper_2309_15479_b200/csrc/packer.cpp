@@ -200,6 +200,8 @@ bool color_quarter(std::vector<Edge>& edges, int nlanes, int ncol) {
     return true;
 }
 
+}  // namespace
+
 // König edge colouring of a general bipartite multigraph (left x right nodes) with ncol >= max
 // degree colours. Edge e joins left[e] and right[e]; returns the colour of every edge (-1 = failed).
 std::vector<int> color_bipartite(const std::vector<int>& left, const std::vector<int>& right, int nleft,
@@ -239,6 +241,8 @@ std::vector<int> color_bipartite(const std::vector<int>& left, const std::vector
     }
     return col;
 }
+
+namespace {
 
 // Slot exchange between the parts of a hash (P >= 2): which of a hash's slots go to which part is
 // free (addition commutes), so single slots are swapped between partner units in different

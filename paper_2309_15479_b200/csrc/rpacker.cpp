@@ -1,0 +1,285 @@
+// rpacker.cpp — bank scheduling for the row-major kernel K1r (SURVEY.md §8(a3)
+// layout B "lane = hash, all lanes read the same row", bank-scheduled).
+//
+// Addition commutes, so the order of a hash's m products is free (Eq. 5 fixes the
+// value, not the order). K1r stages rows row-major at a stride of S = 32*ceil(n/32) + 32 words, so
+// coordinate c of any staged row sits in bank c mod 32, and a warp's LDS.32 at one slot position
+// is a single wavefront when its 32 lanes read 32 distinct banks (or the same word). The packer:
+//  1. splits k hashes into hash blocks (one CTA each) of <= 32/P * W hashes; block boundaries are
+//     multiples of 4 so every block's codes of a row are a 16-byte aligned run (TMA bulk stores);
+//  2. gives each warp hpw = 32/P hashes, hash slot j taking a hash congruent to j mod hpw (the
+//     warp's code stores then hit distinct banks); starting from consecutive hashes, it swaps
+//     same-slot hashes between warps to flatten every warp's per-bank load towards ceil(m/P)
+//     (local search on F = sum over (warp, bank) of max(0, load - T)^2, T relaxed when stuck);
+//  3. splits each hash's m slots into P parts (lanes j + hpw*q) and edge-colours the warp's
+//     lanes x banks multigraph with Delta colours (König): a colour is a slot position;
+//  4. fills free (lane, position) pairs with padding slots (coefficient 0, reading the zero word
+//     of an unused bank in the staged row's 32-word zero tail), or, in the capped variant, folds
+//     colours beyond the part size into existing positions (a few bank conflicts).
+// A cost model (wavefronts per row / measured pipe rate) picks P, warps per CTA and the variant.
+// Everything is deterministic, so every rank derives the identical packing and fp32 order.
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+
+#include "internal.h"
+
+namespace fastlsh {
+namespace {
+
+// slot counts the kernel is instantiated for: even up to 64, multiples of 8 up to 128
+int round_slots(int ms) {
+    if (ms <= 64) return std::max(2, (ms + 1) & ~1);
+    return (ms + 7) & ~7;
+}
+
+using Bank = std::array<int, 32>;
+
+// Step 2: warps of a block. slot[w*hpw + j] = block-local hash or -1. Returns per-warp loads.
+void balance_warps(const std::vector<Bank>& cnt, int kb, int hpw, int W, int T, std::vector<int>& slot,
+                   std::vector<Bank>& load) {
+    slot.assign((size_t)W * hpw, -1);
+    load.assign(W, Bank{});
+    for (int h = 0; h < kb; ++h) {
+        slot[(size_t)(h / hpw) * hpw + h % hpw] = h;
+        for (int b = 0; b < 32; ++b) load[h / hpw][b] += cnt[h][b];
+    }
+    if (W < 2) return;
+    auto ex = [](int v, int Tt) { return v > Tt ? (long)(v - Tt) * (v - Tt) : 0L; };
+    const Bank zero{};
+    for (int Tt = T, guard = 0; guard < 256; ++Tt, ++guard) {
+        bool any_excess = true;
+        for (int sweep = 0; sweep < 64; ++sweep) {
+            bool improved = false;
+            any_excess = false;
+            for (int w1 = 0; w1 < W; ++w1) {
+                long e1 = 0;
+                for (int b = 0; b < 32; ++b) e1 += ex(load[w1][b], Tt);
+                if (e1 == 0) continue;
+                any_excess = true;
+                long best = 0;
+                int bj = -1, bw = -1;
+                for (int j = 0; j < hpw; ++j) {
+                    const int h1 = slot[(size_t)w1 * hpw + j];
+                    const Bank& c1 = h1 >= 0 ? cnt[h1] : zero;
+                    for (int w2 = 0; w2 < W; ++w2) {
+                        if (w2 == w1) continue;
+                        const int h2 = slot[(size_t)w2 * hpw + j];
+                        if (h1 < 0 && h2 < 0) continue;
+                        const Bank& c2 = h2 >= 0 ? cnt[h2] : zero;
+                        long d = 0;
+                        for (int b = 0; b < 32; ++b) {
+                            const int dl = c2[b] - c1[b];
+                            if (dl == 0) continue;
+                            d += ex(load[w1][b] + dl, Tt) - ex(load[w1][b], Tt) + ex(load[w2][b] - dl, Tt) -
+                                 ex(load[w2][b], Tt);
+                        }
+                        if (d < best) { best = d; bj = j; bw = w2; }
+                    }
+                }
+                if (bj < 0) continue;
+                improved = true;
+                const int h1 = slot[(size_t)w1 * hpw + bj], h2 = slot[(size_t)bw * hpw + bj];
+                for (int b = 0; b < 32; ++b) {
+                    const int dl = (h2 >= 0 ? cnt[h2][b] : 0) - (h1 >= 0 ? cnt[h1][b] : 0);
+                    load[w1][b] += dl;
+                    load[bw][b] -= dl;
+                }
+                std::swap(slot[(size_t)w1 * hpw + bj], slot[(size_t)bw * hpw + bj]);
+            }
+            if (!any_excess || !improved) break;
+        }
+        if (!any_excess) break;
+    }
+}
+
+// One packing for P parts, at most Wmax warps per CTA, capped (fold beyond the part size) or not.
+void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& out) {
+    const int n = p.n, m = p.m, k = p.k;
+    RPacking pk;
+    pk.parts = P;
+    pk.cls = -1;
+    for (int c = kNumRClasses - 1; c >= 0; --c)
+        if (kRClasses[c].S >= 32 * ((n + 31) / 32) + 32) pk.cls = c;
+    if (pk.cls < 0) return;
+    pk.S = kRClasses[pk.cls].S;
+    const int hpw = 32 / P;
+    const int T = (m + P - 1) / P;
+    if (T > kRMaxSlots) return;
+    const int kb_cap = hpw * Wmax;
+    // blocks: multiples of 4 hashes (the last takes the rest), balanced
+    const int q4 = (k + 3) / 4;
+    int HB = std::max(1, (k + kb_cap - 1) / kb_cap);
+    while (4 * ((q4 + HB - 1) / HB) > kb_cap) ++HB;
+    pk.hash_blocks = HB;
+    pk.block_h0.resize(HB);
+    pk.block_kb.resize(HB);
+    for (int bl = 0, h0 = 0; bl < HB; ++bl) {
+        const int quads = q4 / HB + (bl < q4 % HB ? 1 : 0);
+        pk.block_h0[bl] = h0;
+        pk.block_kb[bl] = std::min(4 * quads, k - h0);
+        h0 += pk.block_kb[bl];
+    }
+    pk.kb_max = *std::max_element(pk.block_kb.begin(), pk.block_kb.end());
+    const int W = (pk.kb_max + hpw - 1) / hpw;
+    pk.warps = W;
+
+    // per block: warp assignment, part split, colouring
+    struct WarpPlan {
+        std::vector<int> lane, bank, word;  // one entry per sample edge
+        std::vector<float> coef;
+        std::vector<int> col;
+        int delta = 0;
+    };
+    std::vector<std::vector<WarpPlan>> plans(HB, std::vector<WarpPlan>(W));
+    std::vector<std::vector<int>> slots_of(HB);
+    int maxdelta = 0;
+    for (int bl = 0; bl < HB; ++bl) {
+        const int kb = pk.block_kb[bl], h0 = pk.block_h0[bl];
+        std::vector<Bank> cnt(kb, Bank{});
+        for (int h = 0; h < kb; ++h)
+            for (int j = 0; j < m; ++j) cnt[h][p.idx[(size_t)(h0 + h) * m + j] & 31]++;
+        std::vector<Bank> load;
+        balance_warps(cnt, kb, hpw, W, T, slots_of[bl], load);
+        for (int w = 0; w < W; ++w) {
+            WarpPlan& wp = plans[bl][w];
+            for (int j = 0; j < hpw; ++j) {
+                const int h = slots_of[bl][(size_t)w * hpw + j];
+                if (h < 0) continue;
+                // parts: samples sorted by bank, dealt round-robin (part degrees floor/ceil m/P)
+                std::vector<int> ord(m);
+                std::iota(ord.begin(), ord.end(), 0);
+                const int32_t* ix = &p.idx[(size_t)(h0 + h) * m];
+                std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return (ix[x] & 31) < (ix[y] & 31); });
+                for (int e = 0; e < m; ++e) {
+                    const int jj = ord[e];
+                    wp.lane.push_back(j + hpw * (e % P));
+                    wp.bank.push_back(ix[jj] & 31);
+                    wp.word.push_back(ix[jj]);
+                    wp.coef.push_back(p.a[(size_t)(h0 + h) * m + jj]);
+                }
+            }
+            int d = T;
+            for (int b = 0; b < 32; ++b) d = std::max(d, load[w][b]);
+            wp.delta = d;
+            wp.col = color_bipartite(wp.lane, wp.bank, 32, 32, std::max(1, d));
+            if (!wp.col.empty() && wp.col[0] < 0) return;  // cannot happen (König)
+            maxdelta = std::max(maxdelta, d);
+        }
+    }
+    int MS = round_slots(maxdelta);
+    if (capped) MS = std::min(MS, round_slots(T));
+    if (MS > kRMaxSlots) return;
+    if (Wmax == 16 && MS > 64) return;  // 16 warps x 32 lanes need <= 128 registers per lane
+    pk.slots = MS;
+
+    const size_t lanes_total = (size_t)HB * W * 32;
+    pk.offp.assign(lanes_total * (MS / 2), 0);
+    pk.coef.assign(lanes_total * MS, 0.0f);
+    pk.lane_hash.assign(lanes_total, (int16_t)-1);
+    int64_t useful = 0, conflicts = 0;
+    for (int bl = 0; bl < HB; ++bl) {
+        for (int w = 0; w < W; ++w) {
+            WarpPlan& wp = plans[bl][w];
+            std::vector<int> tword((size_t)MS * 32, -1);
+            std::vector<float> tcoef((size_t)MS * 32, 0.0f);
+            std::vector<int> used((size_t)MS * 32, 0);  // lanes per (t, bank) reading distinct words
+            std::vector<int> overflow;
+            for (size_t e = 0; e < wp.lane.size(); ++e) {
+                const int t = wp.col[e];
+                if (t < MS) {
+                    tword[(size_t)t * 32 + wp.lane[e]] = wp.word[e];
+                    tcoef[(size_t)t * 32 + wp.lane[e]] = wp.coef[e];
+                    used[(size_t)t * 32 + wp.bank[e]]++;
+                } else {
+                    overflow.push_back((int)e);
+                }
+            }
+            for (int e : overflow) {  // fold: the free position of this lane with the least-used bank
+                int bt = -1, bu = 1 << 30;
+                for (int t = 0; t < MS; ++t) {
+                    if (tword[(size_t)t * 32 + wp.lane[e]] >= 0) continue;
+                    const int u = used[(size_t)t * 32 + wp.bank[e]];
+                    if (u < bu) { bu = u; bt = t; }
+                }
+                if (bt < 0) return;  // lane degree > MS: cannot happen (MS >= T)
+                tword[(size_t)bt * 32 + wp.lane[e]] = wp.word[e];
+                tcoef[(size_t)bt * 32 + wp.lane[e]] = wp.coef[e];
+                used[(size_t)bt * 32 + wp.bank[e]]++;
+            }
+            useful += (int64_t)wp.lane.size();
+            for (int t = 0; t < MS; ++t) {
+                // padding lanes read the zero word of a bank unused at t (least used if none)
+                for (int l = 0; l < 32; ++l) {
+                    if (tword[(size_t)t * 32 + l] >= 0) continue;
+                    int bb = 0;
+                    for (int b = 1; b < 32; ++b)
+                        if (used[(size_t)t * 32 + b] < used[(size_t)t * 32 + bb]) bb = b;
+                    used[(size_t)t * 32 + bb]++;
+                    tword[(size_t)t * 32 + l] = pk.S - 32 + bb;
+                    tcoef[(size_t)t * 32 + l] = 0.0f;
+                }
+                // extra wavefronts: distinct words sharing a bank (equal words are a broadcast)
+                std::array<std::vector<int>, 32> words;
+                for (int l = 0; l < 32; ++l) {
+                    const int wd = tword[(size_t)t * 32 + l];
+                    auto& v = words[wd & 31];
+                    if (std::find(v.begin(), v.end(), wd) == v.end()) v.push_back(wd);
+                }
+                size_t mx = 1;
+                for (auto& v : words) mx = std::max(mx, v.size());
+                conflicts += (int64_t)mx - 1;
+            }
+            const size_t wl = (size_t)bl * W + w;
+            for (int l = 0; l < 32; ++l) {
+                for (int t = 0; t < MS; ++t) {
+                    const uint32_t off = 4u * (uint32_t)tword[(size_t)t * 32 + l];
+                    pk.offp[(wl * (MS / 2) + t / 2) * 32 + l] |= (t & 1) ? off << 16 : off;
+                    pk.coef[(wl * MS + t) * 32 + l] = tcoef[(size_t)t * 32 + l];
+                }
+                const int h = slots_of[bl][(size_t)w * hpw + (l % hpw)];
+                pk.lane_hash[wl * 32 + l] = (int16_t)h;
+            }
+        }
+    }
+    pk.conflict_wavefronts = conflicts;
+    pk.efficiency = (double)useful / ((double)lanes_total * MS);
+    // cost (shared-memory wavefronts per row): gathers (1 per warp, slot and row) + conflicts +
+    // staging (TMA writes n/32) + code stores (1 STS wavefront per warp and row, k/32 for the
+    // bulk store's reads). The LDS.32 loop runs at ~98% of the pipe with 8 or 16 warps per SM
+    // (tools/microbench_lds32.cu).
+    const double wf = (double)HB * W * MS + (double)conflicts + (double)HB * n / 32.0 + (double)HB * W + k / 32.0;
+    pk.cost = wf / 0.98;
+    pk.ok = true;
+    out = std::move(pk);
+}
+
+}  // namespace
+
+void build_row_packing(const fastlsh_params& p, RPacking& out) {
+    out = RPacking();
+    if (p.n <= 0 || p.m <= 0 || p.k <= 0) return;
+    if (32 * ((p.n + 31) / 32) + 32 > kRClasses[kNumRClasses - 1].S) return;  // largest stage class
+    if (std::getenv("FASTLSH_NO_ROWS")) return;       // experiment knob
+    int force_p = 0;
+    if (const char* e = std::getenv("FASTLSH_ROW_PARTS")) force_p = std::atoi(e);
+    for (int P = 1; P <= 32; P *= 2) {
+        if ((p.m + P - 1) / P > kRMaxSlots) continue;
+        if (force_p && P != force_p) continue;
+        for (int Wmax : {16, 8}) {
+            for (bool capped : {false, true}) {
+                RPacking t;
+                try_rows(p, P, Wmax, capped, t);
+                if (t.ok && t.cost < out.cost) out = std::move(t);
+            }
+        }
+    }
+    if (std::getenv("FASTLSH_PACK_DEBUG") && out.ok)
+        std::fprintf(stderr, "[rpack] P=%d MS=%d W=%d HB=%d eff=%.3f conflicts=%lld cost=%.1f\n", out.parts,
+                     out.slots, out.warps, out.hash_blocks, out.efficiency, (long long)out.conflict_wavefronts,
+                     out.cost);
+}
+
+}  // namespace fastlsh

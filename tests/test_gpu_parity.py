@@ -292,6 +292,83 @@ def test_tmem_kernel_determinism_and_flags():
     assert nf == c.k and sat == 0
 
 
+# ---- K1r (row-major stages, LDS.32; the auto choice where it applies): same rule, same inputs ---------
+
+ROWS_CASES = [("C0", None, None), ("C1", None, 2003), ("C2", 32, 517), ("C2", 128, 261), ("C2", 512, 131),
+              ("C3", None, 4099), ("C4", None, 1001), ("C1", None, 70_001)]
+
+
+@pytest.mark.parametrize("name,m,N", ROWS_CASES)
+def test_rows_kernel_parity(name, m, N):
+    c = configs.get(name)
+    m = m or c.m
+    N = N or c.N
+    P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
+    P.set_kernel("rows")
+    assert P.info()["kernel"] == 3
+    X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
+    rows = None if N <= 5000 else _sample_rows(N, 1500, seed=3, extra=[7, 8, 4095, 4096, N - 2])
+    rel, amb, codes = _run_and_check(P, idx, a, b, c.w, X, rows=rows)
+    assert amb < 1e-2
+    P.set_kernel("smem")
+    codes_smem = fl.fastlsh_hash(P, X)
+    # same Eq. 5 in fp32, different summation orders: codes differ only at fp32 bucket-boundary ties
+    assert (codes != codes_smem).float().mean().item() < 1e-3
+
+
+@pytest.mark.parametrize("N,n,m,k", [(1, 128, 16, 64), (5, 132, 7, 33), (77, 36, 50, 9), (64, 4, 5, 3),
+                                     (33, 8, 1, 1), (130, 256, 200, 20), (9, 96, 64, 257), (300, 4, 4, 100),
+                                     (17, 4096, 130, 6), (1000, 1000, 300, 70), (8, 2048, 64, 514)])
+def test_rows_kernel_edge_shapes(N, n, m, k):
+    """Ragged groups (N % 8), k % 4 != 0 (plain code stores), many parts (m > 64), every stride class."""
+    P, idx, a, b = _params(n, m, k, 1.5, seed=N + n)
+    P.set_kernel("rows")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(N * 31 + n)
+    X = torch.randn((N, n), generator=g, device="cuda")
+    _run_and_check(P, idx, a, b, 1.5, X)
+
+
+def test_rows_kernel_plain_store_path_and_offset_output():
+    """The code buffer leaves through plain stores when bulk stores cannot be used (forced here, and
+    for an output that is not 16-byte aligned); results are identical to the bulk path."""
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    P.set_kernel("rows")
+    X = data.generate(c.data, c.n, 0, 3001, seed=2, device="cuda")
+    ref = fl.fastlsh_hash(P, X)
+    os.environ["FASTLSH_NO_BULK_STORE"] = "1"
+    try:
+        plain = fl.fastlsh_hash(P, X)
+    finally:
+        del os.environ["FASTLSH_NO_BULK_STORE"]
+    assert torch.equal(ref, plain)
+    buf = torch.empty(X.shape[0] * c.k + 1, dtype=torch.int32, device="cuda")
+    out = buf[1:].view(X.shape[0], c.k)  # 4-byte aligned, not 16
+    fl.fastlsh_hash(P, X, out=out)
+    assert torch.equal(ref, out)
+
+
+def test_rows_kernel_determinism_and_flags():
+    c = configs.get("C1")
+    P, idx, a, b = _params(c.n, c.m, c.k, c.w)
+    P.set_kernel("rows")
+    X = data.generate(c.data, c.n, 0, 3000, seed=1, device="cuda")
+    c1 = fl.fastlsh_hash(P, X)
+    parts = torch.cat([fl.fastlsh_hash(P, X[i:j].contiguous()) for i, j in [(0, 999), (999, 3000)]])
+    assert torch.equal(c1, fl.fastlsh_hash(P, X)) and torch.equal(c1, parts)
+    X[5, :] = float("nan")
+    X[6, 3] = 1e30
+    fl.read_flags(P, reset=True)
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    assert (codes[5] == -(2 ** 31)).all()
+    nf, sat = fl.read_flags(P, reset=True)
+    assert nf == c.k
+    # row 6: hashes that sample coordinate 3 saturate (|p| ~ 1e30 |a| / w, finite, outside int32)
+    idx6 = (idx == 3).any(axis=1)
+    assert sat == int(idx6.sum()) and (codes[6][idx6] == -(2 ** 31)).all()
+
+
 def test_chunked_key_build_equals_whole():
     """Keys built chunk by chunk into columns [c0, c1) of one [L][N] table (the C3 bench path)."""
     c = configs.get("C3")

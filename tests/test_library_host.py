@@ -159,21 +159,111 @@ def test_bench_config_packing_quality(lib):
 
 
 def test_kernel_selection_rules(lib):
-    """fastlsh_params_set_kernel: 0/1/2 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128."""
+    """fastlsh_params_set_kernel: 0-3 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128;
+    auto mode reports K1r (3) for n % 4 == 0 shapes whose row packing exists, else K1."""
     import paper_2309_15479_b200 as fl
     from fastlsh_inputs import fastlsh_arrays
     idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
     P = fl.Params.from_arrays(128, 4.0, idx, a, b)
-    for k in ("auto", "smem", "tmem"):
+    assert P.info()["kernel"] == 3
+    for k in ("smem", "tmem", "rows", "auto"):
         P.set_kernel(k)
+    P.set_kernel("tmem")
     assert P.info()["kernel"] == 2 and P.info()["tmem_hash_blocks"] >= 1
+    P.set_kernel("smem")
+    assert P.info()["kernel"] == 1
     with pytest.raises(fl.FastLSHError):
-        P.set_kernel(3)
-    idx, a, b = fastlsh_arrays(130, 16, 64, 4.0, 1)   # n % 4 != 0: no TMA tensor map
+        P.set_kernel(4)
+    idx, a, b = fastlsh_arrays(130, 16, 64, 4.0, 1)   # n % 4 != 0: no TMA tensor map / bulk rows
     Q = fl.Params.from_arrays(130, 4.0, idx, a, b)
     with pytest.raises(fl.FastLSHError):
         Q.set_kernel("tmem")
     assert Q.info()["kernel"] == 1
+
+
+def _unpack_rows(p):
+    """Decode the K1r packing (rpacker.cpp) and check its invariants; returns (packing, conflicts)."""
+    pk = p.row_packing()
+    assert pk is not None
+    idx, a, b, _ = p.export()
+    n, k = p.n, p.k
+    P, MS, W, HB, S = pk["parts"], pk["slots"], pk["warps"], pk["hash_blocks"], pk["S"]
+    hpw = 32 // P
+    assert S % 32 == 0 and S >= 32 * ((n + 31) // 32) + 32 and MS % 2 == 0
+    op = pk["offp"].astype(np.int64)
+    offs = np.empty((HB, W, MS, 32), np.int64)
+    offs[:, :, 0::2, :] = op & 0xFFFF
+    offs[:, :, 1::2, :] = op >> 16
+    assert (offs % 4 == 0).all()
+    word = offs // 4
+    coef = pk["coef"]
+    pad = word >= n
+    assert (word[pad] >= S - 32).all() and (word < S).all()  # padding reads the zero tail
+    assert (coef[pad] == 0).all()
+    # bank conflicts: distinct words at one slot position must lie in distinct banks
+    conflicts = 0
+    for bl in range(HB):
+        for w in range(W):
+            for t in range(MS):
+                ws = set(int(x) for x in word[bl, w, t])
+                conflicts += max(Counter(x % 32 for x in ws).values()) - 1
+    # block boundaries: multiples of 4 (16-byte code runs), covering all k hashes in order
+    h0s, kbs = pk["block_h0"], pk["block_kb"]
+    assert int(h0s[0]) == 0 and int(kbs.sum()) == k
+    assert all(int(h0s[i + 1]) == int(h0s[i] + kbs[i]) for i in range(HB - 1))
+    assert all(int(x) % 4 == 0 for x in kbs[:-1])
+    lh = pk["lane_hash"]
+    for bl in range(HB):
+        h0, kb = int(h0s[bl]), int(kbs[bl])
+        seen = Counter()
+        for w in range(W):
+            for l in range(32):
+                h = int(lh[bl, w, l])
+                # parts of hash slot j = lanes j + hpw*q, and the hash is congruent to j mod hpw
+                assert h == int(lh[bl, w, l % hpw])
+                if h < 0:
+                    assert (coef[bl, w, :, l] == 0).all()
+                    continue
+                assert h % hpw == l % hpw and 0 <= h < kb
+                if l < hpw:
+                    seen[h] += 1
+        assert sorted(seen) == list(range(kb)) and set(seen.values()) == {1}
+        for hh in range(kb):
+            w = next(w for w in range(W) if hh in set(int(x) for x in lh[bl, w]))
+            lanes = [l for l in range(32) if int(lh[bl, w, l]) == hh]
+            assert len(lanes) == P
+            got = Counter()
+            for l in lanes:
+                for t in range(MS):
+                    if not pad[bl, w, t, l]:
+                        got[(int(word[bl, w, t, l]), float(coef[bl, w, t, l]))] += 1
+            want = Counter((int(c), float(x)) for c, x in zip(idx[h0 + hh], a[h0 + hh]))
+            assert got == want, f"hash {h0 + hh}"
+    return pk, conflicts
+
+
+@pytest.mark.parametrize("n,m,k", [(128, 16, 64), (960, 60, 500), (36, 50, 9), (128, 7, 33), (4, 5, 3),
+                                   (784, 64, 200), (256, 200, 20), (4096, 32, 130), (1000, 130, 6)])
+def test_row_packer_preserves_slots_and_banks(lib, n, m, k):
+    """K1r packing: every hash's (coordinate, coefficient) multiset is kept across its parts, padding
+    reads zeros, parts sit in lanes j + (32/P)q with hash = j mod 32/P, and the reported conflict
+    count matches the decoded slot table (0 for these shapes unless folding was chosen)."""
+    p = fl.Params.create(n, m, k, 1.0, seed=5)
+    pk, conflicts = _unpack_rows(p)
+    assert conflicts == pk["conflicts"]
+
+
+def test_row_packer_bench_configs(lib):
+    """The bench-relevant shapes pack with few padding slots and no bank conflicts."""
+    for name, kw in (("C1", {}), ("C3", {}), ("C4", {}), ("C2", {"m": 32})):
+        c = configs.get(name)
+        m = kw.get("m", c.m)
+        p = fl.Params.create(c.n, m, c.k, c.w, seed=1)
+        pk = p.row_packing()
+        assert pk is not None, name
+        useful = c.k * m
+        slots = pk["hash_blocks"] * pk["warps"] * 32 * pk["slots"]
+        assert useful / slots >= 0.85, (name, useful / slots, pk["slots"], pk["parts"])
 
 
 @pytest.mark.parametrize("n,m,k", [(960, 60, 500), (784, 64, 2000), (128, 16, 256), (4096, 32, 1000), (96, 40, 37)])

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--rows", type=int, default=262144)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--keys", action="store_true")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "smem", "tmem"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "smem", "tmem", "rows"])
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--dense", action="store_true", help="time the tcgen05 dense baseline too")
     ap.add_argument("--dense-e2lsh", action="store_true", help="dense baseline on E2LSH params (m = n)")
