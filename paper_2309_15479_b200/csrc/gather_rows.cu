@@ -21,11 +21,11 @@ RowKernelFn select_row_kernel(int MS, int cls) {
     return nullptr;
 }
 
-// stages + kCodeBufs code buffers + barriers + b
+// stages + NC code buffers + barriers + counters + b
 size_t row_smem_bytes(const RPacking& pk) {
     const RClass c = kRClasses[pk.cls];
     const int kbp = (pk.kb_max + 3) & ~3;
-    return (size_t)c.NS * c.R * c.S * 4 + (size_t)kCodeBufs * c.R * kbp * 4 + (size_t)(2 * c.NS + 2 * kCodeBufs) * 8 +
+    return (size_t)c.NS * c.R * c.S * 4 + (size_t)c.NC * c.R * kbp * 4 + (size_t)(c.NS + 2 * c.NC) * 8 + c.NS * 4 +
            (size_t)kbp * 4;
 }
 
@@ -71,9 +71,10 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     bool blocks_aligned = true;
     for (int bl = 0; bl < pk.hash_blocks; ++bl)
         if ((pk.block_h0[bl] % 4) || (pk.block_kb[bl] % 4)) blocks_aligned = false;
-    a.bulk = (p->k % 4 == 0) && blocks_aligned && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
-    if (std::getenv("FASTLSH_NO_BULK_STORE")) a.bulk = 0;  // experiment knob (and fallback test)
-    a.whole = (a.bulk && pk.hash_blocks == 1 && a.kbp == p->k) ? 1 : 0;
+    a.vec = (p->k % 4 == 0) && blocks_aligned && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
+    if (std::getenv("FASTLSH_NO_VEC_STORE")) a.vec = 0;  // experiment knob (and fallback test)
+    a.debug = 0;
+    if (const char* e = std::getenv("FASTLSH_K1R_DEBUG")) a.debug = std::atoi(e);  // experiment knob
 
     cudaError_t e =
         cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -3,10 +3,11 @@
 //
 // For every row v and hash i: h_i(v) = floor((a_i . S_i(v) + b_i) / w)   (Eq. 5),
 // SURVEY.md §8(a) steps a2-a5 in one persistent kernel:
-//  * a2 stage: thread 0 issues one TMA bulk copy (cp.async.bulk, complete_tx on the stage's full
-//    mbarrier) per row of a group of R rows straight into a ring of NS row-major stages (row stride
-//    S words, S % 32 == 0, 32-word zero tail per row). No transposition: a coordinate c lies in
-//    bank c mod 32 of every staged row.
+//  * a2 stage: one TMA bulk copy (cp.async.bulk, complete_tx on the stage's full mbarrier) per row
+//    of a group of R rows straight into a ring of NS row-major stages (row stride S words, S % 32
+//    == 0, 32-word zero tail per row; S, R, NS fixed per stride class, so rows are immediate
+//    offsets). No transposition: a coordinate c lies in bank c mod 32 of every staged row. The
+//    last warp to finish reading a stage (shared counter) issues its refill.
 //  * a3/a4 sample + project: each lane holds its hash part's MS slots in registers (16-bit byte
 //    offsets packed two per register, f32 coefficients). Per slot it issues R LDS.32 (one per row)
 //    and R FFMA. The packer (rpacker.cpp) guarantees that at every slot the warp's 32 lanes read 32
@@ -15,10 +16,11 @@
 //    lane obtains the bit-identical sum: fp addition is commutative).
 //  * a5 quantise: __fadd_rn(p, b), IEEE division by w (an exact multiply when w is a power of two),
 //    floor toward -inf, INT32_MIN + a device counter for non-finite or out-of-range quotients.
-//    Codes go to a shared-memory buffer (conflict-free: the hash in lane j is j mod 32/P) and
-//    leave as TMA bulk stores (one per row of the block, or one per group when the block covers
-//    all k hashes), issued by thread 0 once every warp has written its codes.
-//  * mbarriers only (no CTA barrier in the loop): stage full/empty, code-buffer full/empty.
+//    Codes go to a ring of NC shared-memory buffers (conflict-free: the hash in lane j is j mod
+//    32/P); D = NC-2 groups later every warp copies a share of the group's tile to global memory
+//    with coalesced 16-byte stores (no thread waits on a TMA store: a single flushing warp made the
+//    whole CTA run at its pace).
+//  * mbarriers only (no CTA barrier in the loop): stage full, code-buffer full/empty.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -47,11 +49,9 @@ struct RowArgs {
     int32_t* codes;
     float* proj;
     unsigned long long* flags;
-    int bulk;                  // 1: TMA bulk stores of the code buffer; 0: plain stores by all threads
-    int whole;                 // 1: one block covers all k hashes and kbp == k: a group is one run
+    int vec;                   // 1: the block's code runs are 16-byte aligned (16-byte copy-out)
+    int debug;                 // experiment knob (FASTLSH_K1R_DEBUG): 1 no code output, 2 no refills
 };
-
-constexpr int kCodeBufs = 3;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -98,7 +98,6 @@ __device__ __forceinline__ void mbar_wait_one(uint32_t bar, uint32_t parity) {
     while (!mbar_try(bar, parity)) {
     }
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile(
@@ -106,16 +105,6 @@ __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* src, uint
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void tma_store(void* dst, uint32_t src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void tma_store_wait_read1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 __device__ __forceinline__ int live_rows(long long N, long long row0, int cap) {
     const long long left = N - row0;
     return (int)(left < cap ? (left > 0 ? left : 0) : cap);
@@ -125,8 +114,8 @@ template <int MS, int CLS>
 __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const RowArgs a) {
     static_assert(MS % 2 == 0, "slots are packed two per register");
     constexpr int S = kRClasses[CLS].S, R = kRClasses[CLS].R, NS = kRClasses[CLS].NS;
-    constexpr int LAG = NS >= 4 ? 2 : 1;  // at iteration j thread 0 refills the stage of group j-LAG
-    constexpr int NC = kCodeBufs;
+    constexpr int NC = kRClasses[CLS].NC;
+    constexpr int D = NC - 2;  // a warp flushes its share of group j-D at iteration j
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t row_bytes = 4u * S;  // compile-time: row r of a stage is an immediate offset
     constexpr uint32_t stage_bytes = R * row_bytes;
@@ -134,10 +123,12 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     int32_t* cbuf = reinterpret_cast<int32_t*>(smem + (size_t)NS * stage_bytes);
     const int cwords = R * a.kbp;  // one code buffer
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(cbuf + NC * cwords);
-    float* s_b = reinterpret_cast<float*>(bars + 2 * NS + 2 * NC);
+    int* cnt = reinterpret_cast<int*>(bars + NS + 2 * NC);  // [NS] stage readers (monotone)
+    float* s_b = reinterpret_cast<float*>(cnt + NS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x;
+    const int W = a.W;
     const int hb = blockIdx.x % a.HB;
     const long long gpr = gridDim.x / a.HB;
     const long long rs = blockIdx.x / a.HB;
@@ -148,22 +139,19 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     const uint32_t stage0 = smem_u32(stages);
     const uint32_t cbuf0 = smem_u32(cbuf);
     const uint32_t bar0 = smem_u32(bars);
-    auto FULL = [&](int s) { return bar0 + 8u * s; };
-    auto EMPTY = [&](int s) { return bar0 + 8u * (NS + s); };
-    auto CFULL = [&](int c) { return bar0 + 8u * (2 * NS + c); };
-    auto CEMPTY = [&](int c) { return bar0 + 8u * (2 * NS + NC + c); };
+    auto FULL = [&](int s) { return bar0 + 8u * s; };              // stage s holds its next group (TMA)
+    auto CFULL = [&](int c) { return bar0 + 8u * (NS + c); };       // all warps wrote their codes
+    auto CEMPTY = [&](int c) { return bar0 + 8u * (NS + NC + c); }; // all warps flushed their share
 
     if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(FULL(s), 1);
-            mbar_init(EMPTY(s), a.W);
-        }
+        for (int s = 0; s < NS; ++s) mbar_init(FULL(s), 1);
         for (int c = 0; c < NC; ++c) {
-            mbar_init(CFULL(c), a.W);
-            mbar_init(CEMPTY(c), a.bulk ? 1 : nthreads);
+            mbar_init(CFULL(c), W);
+            mbar_init(CEMPTY(c), W);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (tid < NS) cnt[tid] = 0;
     // zero tails (targets of padding slots), never overwritten by the row copies
     for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + S - 32 + (i & 31)] = 0.f;
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
@@ -171,7 +159,7 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     uint32_t opk[MS / 2];
     float cf[MS];
     {
-        const size_t wl = (size_t)hb * a.W + warp;
+        const size_t wl = (size_t)hb * W + warp;
         const uint32_t* po = a.offp + wl * (MS / 2) * 32 + lane;
         const float* pc = a.coef + wl * MS * 32 + lane;
 #pragma unroll
@@ -179,7 +167,7 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
 #pragma unroll
         for (int t = 0; t < MS; ++t) cf[t] = __ldg(pc + t * 32);
     }
-    const int my_h = a.lane_hash[((size_t)hb * a.W + warp) * 32 + lane];
+    const int my_h = a.lane_hash[((size_t)hb * W + warp) * 32 + lane];
     const bool storing = lane < hpw && my_h >= 0;
     __syncthreads();
     const float my_b = storing ? s_b[my_h] : 0.f;
@@ -188,7 +176,7 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     auto group_of = [&](long long j) { return rs + j * gpr; };
     const uint32_t row_len = 4u * (uint32_t)a.n;
 
-    // thread 0: TMA copies of group j's live rows into stage j % NS
+    // one thread: TMA copies of group j's live rows into stage j % NS
     auto issue = [&](long long j) {
         const int s = (int)(j % NS);
         const long long row0 = group_of(j) * R;
@@ -199,37 +187,31 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
                          FULL(s));
     };
     void* out = a.proj ? static_cast<void*>(a.proj) : static_cast<void*>(a.codes);
-    // thread 0 (bulk mode): TMA stores of group g's code buffer, then release the buffer of g-1
-    auto store_codes = [&](long long g) {
-        const int c = (int)(g % NC);
-        mbar_wait_one(CFULL(c), (uint32_t)((g / NC) & 1));
+    // Every warp copies its share of group g's code buffer to global memory (coalesced 16-byte
+    // LDS/STG when the block's runs are 16-byte aligned, else 4-byte), D groups after writing its
+    // own codes of g, once all warps have (CFULL); then releases the buffer (CEMPTY).
+    auto flush_share = [&](long long g) {
+        const int cg = (int)(g % NC);
+        mbar_wait_warp(CFULL(cg), (uint32_t)((g / NC) & 1));
         const long long row0 = group_of(g) * R;
         const int rows = live_rows(a.N, row0, R);
-        const uint32_t src = cbuf0 + 4u * c * cwords;
-        int32_t* o = static_cast<int32_t*>(out);
-        if (a.whole) {
-            tma_store(o + row0 * a.k, src, 4u * rows * a.k);
+        const int32_t* src = cbuf + cg * cwords;
+        int32_t* o = static_cast<int32_t*>(out) + row0 * a.k + h0;
+        if (a.vec) {
+            const int q4 = kb >> 2;  // 16-byte chunks per row of the block
+            for (int u = tid; u < rows * q4; u += nthreads) {
+                const int r = u / q4, q = u - r * q4;
+                const int4 v = *reinterpret_cast<const int4*>(src + r * a.kbp + 4 * q);
+                *reinterpret_cast<int4*>(o + (long long)r * a.k + 4 * q) = v;
+            }
         } else {
-            for (int r = 0; r < rows; ++r)
-                tma_store(o + (row0 + r) * a.k + h0, src + 4u * r * a.kbp, 4u * kb);
+            for (int u = tid; u < rows * kb; u += nthreads) {
+                const int r = u / kb, h = u - r * kb;
+                o[(long long)r * a.k + h] = src[r * a.kbp + h];
+            }
         }
-        tma_store_commit();
-        tma_store_wait_read1();  // every group but this one has been read out of shared memory
-        if (g >= 1) mbar_arrive(CEMPTY((int)((g - 1) % NC)));
-    };
-    // all threads (fallback): plain stores of group g's code buffer
-    auto copy_codes = [&](long long g) {
-        const int c = (int)(g % NC);
-        mbar_wait_warp(CFULL(c), (uint32_t)((g / NC) & 1));
-        const long long row0 = group_of(g) * R;
-        const int rows = live_rows(a.N, row0, R);
-        int32_t* o = static_cast<int32_t*>(out);
-        const int32_t* src = cbuf + c * cwords;
-        for (int it = tid; it < rows * kb; it += nthreads) {
-            const int r = it / kb, h = it - r * kb;
-            o[(row0 + r) * a.k + h0 + h] = src[r * a.kbp + h];
-        }
-        mbar_arrive(CEMPTY(c));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(CEMPTY(cg));
     };
 
     if (tid == 0)
@@ -239,20 +221,14 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     const float inv_w = 1.0f / w;
     const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
 
+    // No producer thread: the last warp to finish reading a stage refills it (monotone shared
+    // counter), and every warp flushes a share of the code buffer of group j-D at iteration j.
     int s = 0;         // stage of group j
     uint32_t ph = 0;   // its full-barrier parity
+    int c = 0;         // code buffer of group j
     for (long long j = 0; j < iters; ++j) {
-        if (tid == 0) {
-            const long long jr = j - LAG;
-            if (jr >= 0 && jr + NS < iters) {
-                mbar_wait_one(EMPTY((int)(jr % NS)), (uint32_t)((jr / NS) & 1));
-                fence_proxy_async();
-                issue(jr + NS);
-            }
-            if (a.bulk && j >= 1) store_codes(j - 1);
-        }
         // gather-FMA: R rows per slot, one LDS.32 (one wavefront per warp) each
-        mbar_wait_warp(FULL(s), ph);
+        if (!(a.debug & 2) || j < NS) mbar_wait_warp(FULL(s), ph);
         const uint32_t sb = stage0 + s * stage_bytes;
         float acc[R];
 #pragma unroll
@@ -265,8 +241,9 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = fmaf(lds32(hi + r * row_bytes), cf[2 * t2 + 1], acc[r]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(EMPTY(s));
+        __syncwarp();  // every lane's loads of stage s have returned (their values were consumed)
+        // (no proxy fence: the reads are complete before the count, as in mbarrier-released TMA rings)
+        if (!(a.debug & 2) && lane == 0 && (atomicAdd(cnt + s, 1) + 1) % W == 0 && j + NS < iters) issue(j + NS);
         // parts of a hash: lanes j + hpw*q, xor butterfly
         for (int off = 16; off >= hpw; off >>= 1) {
 #pragma unroll
@@ -274,7 +251,14 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
         }
         const long long row0 = group_of(j) * R;
         const int nrows = live_rows(a.N, row0, R);
-        const int c = (int)(j % NC);
+        if (a.debug & 1) {
+            if (lane == 0 && acc[0] == 1234.5f) a.flags[0] = 0;  // keep the sums alive
+            if (++s == NS) {
+                s = 0;
+                ph ^= 1u;
+            }
+            continue;
+        }
         if (j >= NC) mbar_wait_warp(CEMPTY(c), (uint32_t)(((j - NC) / NC) & 1));
         if (storing) {
             int32_t* dst = cbuf + c * cwords + my_h;
@@ -308,23 +292,17 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
                 for (int r = 0; r < R; ++r) dst[r * a.kbp] = code[r];
             }
         }
-        if (a.bulk) fence_proxy_async();  // generic-proxy code writes -> visible to the TMA store
         __syncwarp();
-        if (lane == 0) mbar_arrive(CFULL(c));
-        if (!a.bulk && j >= 1) copy_codes(j - 1);
+        if (lane == 0) mbar_arrive(CFULL(c));  // release: this warp's codes of group j are in the buffer
+        if (j >= D) flush_share(j - D);
         if (++s == NS) {
             s = 0;
             ph ^= 1u;
         }
+        if (++c == NC) c = 0;
     }
-    if (a.bulk) {
-        if (tid == 0) {
-            if (iters >= 1) store_codes(iters - 1);
-            tma_store_wait_all();
-        }
-    } else if (iters >= 1) {
-        copy_codes(iters - 1);
-    }
+    if (!(a.debug & 1))
+        for (long long g = iters > D ? iters - D : 0; g < iters; ++g) flush_share(g);
 }
 
 typedef void (*RowKernelFn)(RowArgs);

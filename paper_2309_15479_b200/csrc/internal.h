@@ -82,9 +82,11 @@ struct TPacking {
 // wavefront. Slots are packed two per register (16-bit byte offsets within a row).
 constexpr int kRMaxSlots = 128;
 // Stage geometry per row-stride class (compile-time in the kernel, so the R rows of a stage are
-// immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages.
-struct RClass { int S, R, NS; };
-constexpr RClass kRClasses[] = {{160, 8, 8}, {288, 8, 8}, {544, 8, 6}, {1056, 8, 4}, {2080, 4, 4}, {4128, 4, 3}};
+// immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages, NC
+// code buffers (a deep code ring lets fast warps run ahead of the flush of a slow warp's group).
+struct RClass { int S, R, NS, NC; };
+constexpr RClass kRClasses[] = {{160, 8, 8, 4}, {288, 8, 8, 4}, {544, 8, 6, 4}, {1056, 8, 4, 4},
+                                {2080, 4, 4, 4}, {4128, 4, 3, 3}};
 constexpr int kNumRClasses = 6;
 struct RPacking {
     bool ok = false;

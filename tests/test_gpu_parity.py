@@ -330,18 +330,18 @@ def test_rows_kernel_edge_shapes(N, n, m, k):
 
 
 def test_rows_kernel_plain_store_path_and_offset_output():
-    """The code buffer leaves through plain stores when bulk stores cannot be used (forced here, and
-    for an output that is not 16-byte aligned); results are identical to the bulk path."""
+    """The code buffer leaves through 4-byte stores when 16-byte ones cannot be used (forced here, and
+    for an output that is not 16-byte aligned); results are identical to the vector path."""
     c = configs.get("C1")
     P, idx, a, b = _params(c.n, c.m, c.k, c.w)
     P.set_kernel("rows")
     X = data.generate(c.data, c.n, 0, 3001, seed=2, device="cuda")
     ref = fl.fastlsh_hash(P, X)
-    os.environ["FASTLSH_NO_BULK_STORE"] = "1"
+    os.environ["FASTLSH_NO_VEC_STORE"] = "1"
     try:
         plain = fl.fastlsh_hash(P, X)
     finally:
-        del os.environ["FASTLSH_NO_BULK_STORE"]
+        del os.environ["FASTLSH_NO_VEC_STORE"]
     assert torch.equal(ref, plain)
     buf = torch.empty(X.shape[0] * c.k + 1, dtype=torch.int32, device="cuda")
     out = buf[1:].view(X.shape[0], c.k)  # 4-byte aligned, not 16
