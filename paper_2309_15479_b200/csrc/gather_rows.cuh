@@ -111,7 +111,9 @@ __device__ __forceinline__ int live_rows(long long N, long long row0, int cap) {
 }
 
 template <int MS, int CLS>
-__global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const RowArgs a) {
+// register cap by slot count: small MS leaves room for more resident warps (C3: 3 CTAs of 8 warps)
+__global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 512 : 256), 1)
+    rows_kernel(const RowArgs a) {
     static_assert(MS % 2 == 0, "slots are packed two per register");
     constexpr int S = kRClasses[CLS].S, R = kRClasses[CLS].R, NS = kRClasses[CLS].NS;
     constexpr int NC = kRClasses[CLS].NC;
@@ -190,6 +192,9 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
     // Every warp copies its share of group g's code buffer to global memory (coalesced 16-byte
     // LDS/STG when the block's runs are 16-byte aligned, else 4-byte), D groups after writing its
     // own codes of g, once all warps have (CFULL); then releases the buffer (CEMPTY).
+    const int q4 = kb >> 2;  // 16-byte chunks per row of the block
+    const int r_first = q4 ? tid / q4 : R, q_first = q4 ? tid - r_first * q4 : 0;
+    const int r_step = q4 ? nthreads / q4 : 0, q_step = q4 ? nthreads - r_step * q4 : 0;
     auto flush_share = [&](long long g) {
         const int cg = (int)(g % NC);
         mbar_wait_warp(CFULL(cg), (uint32_t)((g / NC) & 1));
@@ -198,11 +203,16 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
         const int32_t* src = cbuf + cg * cwords;
         int32_t* o = static_cast<int32_t*>(out) + row0 * a.k + h0;
         if (a.vec) {
-            const int q4 = kb >> 2;  // 16-byte chunks per row of the block
-            for (int u = tid; u < rows * q4; u += nthreads) {
-                const int r = u / q4, q = u - r * q4;
+            // unit u = tid + i*nthreads = (row r, chunk q), stepped without divisions
+            for (int r = r_first, q = q_first; r < rows;) {
                 const int4 v = *reinterpret_cast<const int4*>(src + r * a.kbp + 4 * q);
                 *reinterpret_cast<int4*>(o + (long long)r * a.k + 4 * q) = v;
+                r += r_step;
+                q += q_step;
+                if (q >= q4) {
+                    q -= q4;
+                    ++r;
+                }
             }
         } else {
             for (int u = tid; u < rows * kb; u += nthreads) {
@@ -272,17 +282,15 @@ __global__ void __launch_bounds__((MS <= 64 ? 512 : 256), 1) rows_kernel(const R
                 for (int r = 0; r < R; ++r) {
                     const float num = __fadd_rn(acc[r], my_b);
                     const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
-                    const float f = floorf(qv);
-                    code[r] = (int)f;
-                    bad |= !(f > -2147483648.0f && f < 2147483648.0f);
+                    code[r] = __float2int_rd(qv);          // floor toward -inf (F2I.FLOOR)
+                    bad |= !(fabsf(qv) < 2147483648.0f);   // floor(qv) outside int32, or NaN
                 }
                 if (bad) {  // rare: sentinel + count (rows past N are not counted)
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const float num = __fadd_rn(acc[r], my_b);
                         const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
-                        const float f = floorf(qv);
-                        if (!(f > -2147483648.0f && f < 2147483648.0f)) {
+                        if (!(fabsf(qv) < 2147483648.0f)) {
                             code[r] = INT_MIN;
                             if (r < nrows) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
                         }

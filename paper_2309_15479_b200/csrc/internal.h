@@ -85,8 +85,8 @@ constexpr int kRMaxSlots = 128;
 // immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages, NC
 // code buffers (a deep code ring lets fast warps run ahead of the flush of a slow warp's group).
 struct RClass { int S, R, NS, NC; };
-constexpr RClass kRClasses[] = {{160, 8, 8, 4}, {288, 8, 8, 4}, {544, 8, 6, 4}, {1056, 8, 4, 4},
-                                {2080, 4, 4, 4}, {4128, 4, 3, 3}};
+constexpr RClass kRClasses[] = {{160, 8, 4, 6}, {288, 8, 8, 6}, {544, 8, 6, 6}, {1056, 8, 3, 6},
+                                {2080, 4, 4, 8}, {4128, 4, 3, 3}};
 constexpr int kNumRClasses = 6;
 struct RPacking {
     bool ok = false;
