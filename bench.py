@@ -160,6 +160,18 @@ def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1):
     return d
 
 
+def _packing_summary(P, info, fused_keys):
+    """The GPU layout of the kernel that ran (K1r's row packing, else K1's)."""
+    rp = P.row_packing() if info["kernel"] == 3 and not fused_keys else None
+    if rp is not None:
+        lanes = rp["hash_blocks"] * rp["warps"] * 32 * rp["slots"]
+        return {"kernel": "K1r", "parts": rp["parts"], "slots": rp["slots"], "warps_per_block": rp["warps"],
+                "hash_blocks": rp["hash_blocks"], "staged_row_words": rp["S"],
+                "bank_efficiency": P.k * P.m / lanes, "conflict_wavefronts": rp["conflicts"]}
+    return {"kernel": "K1", **{k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
+                                                    "bank_efficiency", "conflict_wavefronts")}}
+
+
 def _traffic_from_profiles(cfg, rows: int):
     """DRAM bytes per launch of the dominant kernel, from the committed `ncu --set full` capture
     (profiles/ncu_gather_full.json: dram__bytes_read + dram__bytes_write of one K1 launch on the
@@ -322,7 +334,9 @@ def main():
     roofline = {"bound": "smem", "achieved": gathers / t_hash / 1e9, "peak": g_peak / 1e9,
                 "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
                 "traffic": _traffic_from_profiles(cfg, N),
-                "kernel": "gather_kernel (K1 fastlsh_hash" + (", keys fused in its epilogue)" if fused_keys else ")"),
+                "kernel": ("gather_kernel (K1 fastlsh_hash, keys fused in its epilogue)" if fused_keys else
+                           {1: "gather_kernel (K1 fastlsh_hash)", 2: "tmem_gather_kernel (K1t fastlsh_hash)",
+                            3: "rows_kernel (K1r fastlsh_hash: row-major stages, LDS.32)"}[info["kernel"]]),
                 "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
                 "north_star_frac": t_roof / t_hash, "north_star_frac_nominal_8TBs": t_roof_nominal / t_hash,
                 "hbm_achieved_gbs": hbm_bytes / t_hash / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"],
@@ -468,8 +482,7 @@ def main():
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},
                 "dense_e2lsh": dense, "tables": tables, "queries": queries,
-                "packing": {k: info[k] for k in ("parts", "slots", "warps_per_block", "hash_blocks",
-                                                 "bank_efficiency", "conflict_wavefronts")}}
+                "packing": _packing_summary(P, info, fused_keys)}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

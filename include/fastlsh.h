@@ -103,8 +103,10 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* p, int32_t* sizes, u
                                       int32_t* block_kb);
 
 /* Diagnostic: copy the K1r packing out (rpacker.cpp).
- * sizes[0..7] = {ok, parts P, slots MS, warps W, hash_blocks HB, kb_max, staged row stride S
- * (words), conflict wavefronts per row}. When ok == 0 nothing else is written. Arrays (any may be
+ * sizes[0..9] = {ok, parts P, slots MS, warps W, hash_blocks HB, kb_max, staged row stride S
+ * (words), conflict wavefronts per row, S0, n1}: a staged row holds coordinates [0, n) at words
+ * [0, n), zeros at [S0-32, S0), and coordinates [0, n1) again at words S0+16+c. When ok == 0
+ * nothing else is written. Arrays (any may be
  * NULL): offp u32[HB*W*(MS/2)*32] (two 16-bit byte offsets into a staged row: bits 0-15 slot 2t,
  * bits 16-31 slot 2t+1), coef f32[HB*W*MS*32], lane_hash int16[HB*W*32] (block-local hash of the
  * lane's part, -1 idle; parts of hash slot j sit in lanes j + (32/P)q), block_h0/block_kb int32[HB]. */

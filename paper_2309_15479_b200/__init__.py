@@ -202,10 +202,10 @@ class Params:
 
     def row_packing(self) -> dict | None:
         """The K1r layout (diagnostic; see fastlsh_params_row_packing); None when K1r does not apply."""
-        sz = np.zeros(8, np.int32)
+        sz = np.zeros(10, np.int32)
         _check(self._lib.fastlsh_params_row_packing(self._h, _np_ptr(sz), None, None, None, None, None),
                "fastlsh_params_row_packing")
-        ok, P, MS, W, HB, kbm, S, conf = (int(x) for x in sz)
+        ok, P, MS, W, HB, kbm, S, conf, S0, n1 = (int(x) for x in sz)
         if not ok:
             return None
         offp = np.zeros(HB * W * (MS // 2) * 32, np.uint32)
@@ -215,7 +215,7 @@ class Params:
         kb = np.zeros(HB, np.int32)
         _check(self._lib.fastlsh_params_row_packing(self._h, _np_ptr(sz), _np_ptr(offp), _np_ptr(coef), _np_ptr(lh),
                                                     _np_ptr(h0), _np_ptr(kb)), "fastlsh_params_row_packing")
-        return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, S=S, conflicts=conf,
+        return dict(parts=P, slots=MS, warps=W, hash_blocks=HB, kb_max=kbm, S=S, conflicts=conf, S0=S0, n1=n1,
                     offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
                     lane_hash=lh.reshape(HB, W, 32), block_h0=h0, block_kb=kb)
 

@@ -304,6 +304,7 @@ fastlsh_status fastlsh_params_row_packing(const fastlsh_params* cp, int32_t* siz
         sizes[0] = pk.ok ? 1 : 0; sizes[1] = pk.parts; sizes[2] = pk.slots; sizes[3] = pk.warps;
         sizes[4] = pk.hash_blocks; sizes[5] = pk.kb_max; sizes[6] = pk.S;
         sizes[7] = (int32_t)pk.conflict_wavefronts;
+        sizes[8] = pk.S0; sizes[9] = pk.n1;
     }
     if (!pk.ok) return FASTLSH_OK;
     if (offp) std::memcpy(offp, pk.offp.data(), pk.offp.size() * sizeof(uint32_t));

@@ -51,6 +51,8 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     a.N = N;
     a.n = p->n;
     a.S = pk.S;
+    a.S0 = pk.S0;
+    a.n1 = pk.n1;
     a.offp = d.r_offp;
     a.coef = d.r_coef;
     a.lane_hash = d.r_lane_hash;

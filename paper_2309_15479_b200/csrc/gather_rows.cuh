@@ -37,6 +37,7 @@ struct RowArgs {
     const float* X;
     long long N;
     int n, S;                  // row length, staged row stride (words)
+    int S0, n1;                // copy 1 of coordinates [0, n1) at word S0 + 16 (zero tail at S0 - 32)
     const uint32_t* offp;      // [HB][W][MS/2][32]
     const float* coef;         // [HB][W][MS][32]
     const int16_t* lane_hash;  // [HB][W*32]
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     }
     if (tid < NS) cnt[tid] = 0;
     // zero tails (targets of padding slots), never overwritten by the row copies
-    for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + S - 32 + (i & 31)] = 0.f;
+    for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + a.S0 - 32 + (i & 31)] = 0.f;
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
 
     uint32_t opk[MS / 2];
@@ -183,10 +184,13 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
         const int s = (int)(j % NS);
         const long long row0 = group_of(j) * R;
         const int rows = live_rows(a.N, row0, R);
-        mbar_arrive_tx(FULL(s), row_len * rows);
-        for (int r = 0; r < rows; ++r)
-            tma_load_row(stage0 + s * stage_bytes + r * row_bytes, a.X + (row0 + r) * (long long)a.n, row_len,
-                         FULL(s));
+        mbar_arrive_tx(FULL(s), (row_len + 4u * a.n1) * rows);
+        for (int r = 0; r < rows; ++r) {
+            const uint32_t dst = stage0 + s * stage_bytes + r * row_bytes;
+            const float* src = a.X + (row0 + r) * (long long)a.n;
+            tma_load_row(dst, src, row_len, FULL(s));
+            if (a.n1) tma_load_row(dst + 4u * (a.S0 + 16), src, 4u * a.n1, FULL(s));
+        }
     };
     void* out = a.proj ? static_cast<void*>(a.proj) : static_cast<void*>(a.codes);
     // Every warp copies its share of group g's code buffer to global memory (coalesced 16-byte

@@ -72,9 +72,11 @@ struct TPacking {
 };
 
 // GPU packing for the row-major kernel K1r (gather_rows.cuh). Stages hold rows
-// row-major at a stride of S words (S = 32*ceil(n/32) + 32; the last 32 words of every staged row
-// are zero, one per bank, read by padding slots), so a coordinate's bank is idx mod 32 in every
-// row and TMA bulk copies fill the stages directly. Hash block hb serves hashes [h0, h0+kb); a
+// row-major at a stride of S words (a multiple of 32, fixed per class): copy 0 of the row at words
+// [0, n), a 32-word zero tail at [S0-32, S0) (S0 = 32*ceil(n/32) + 32) read by padding slots, and,
+// where the class leaves room, copy 1 of coordinates [0, n1) at word S0 + 16 + c (16 banks
+// rotated). A coordinate's bank is thus the same in every staged row, and TMA bulk copies fill the
+// stages directly. Hash block hb serves hashes [h0, h0+kb); a
 // block's W warps hold hpw = 32/P hashes each, hash slot j of a warp in lanes j + hpw*q (q < P
 // parts, summed by an xor butterfly), and the hash in slot j is congruent to j mod hpw so that the
 // code stores of a warp hit distinct banks. At every slot position the 32 lanes of a warp read 32
@@ -85,12 +87,16 @@ constexpr int kRMaxSlots = 128;
 // immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages, NC
 // code buffers (a deep code ring lets fast warps run ahead of the flush of a slow warp's group).
 struct RClass { int S, R, NS, NC; };
-constexpr RClass kRClasses[] = {{160, 8, 4, 6}, {288, 8, 8, 6}, {544, 8, 6, 6}, {1056, 8, 3, 6},
+// Classes 0-2 (n <= 128 / 256 / 512) stage a full second copy (n1 = n); classes 3-5 one copy.
+constexpr RClass kRClasses[] = {{320, 8, 3, 5}, {576, 8, 4, 6}, {1088, 8, 3, 5}, {1056, 8, 3, 6},
                                 {2080, 4, 4, 8}, {4128, 4, 3, 3}};
+constexpr int kRDualClasses = 3;
+constexpr int kRDualMaxN[kRDualClasses] = {128, 256, 512};
 constexpr int kNumRClasses = 6;
 struct RPacking {
     bool ok = false;
     int parts = 1, slots = 0, warps = 0, hash_blocks = 0, kb_max = 0, S = 0, cls = 0;
+    int S0 = 0, n1 = 0;  // copy 0 spans words [0, S0) (zero tail [S0-32, S0)); copy 1 = coords [0, n1) at S0+16
     std::vector<int> block_h0, block_kb;
     std::vector<uint32_t> offp;     // [HB][W][MS/2][32]: bits 0-15 slot 2t, bits 16-31 slot 2t+1
     std::vector<float> coef;        // [HB][W][MS][32]

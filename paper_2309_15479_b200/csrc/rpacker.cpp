@@ -13,7 +13,10 @@
 //     (local search on F = sum over (warp, bank) of max(0, load - T)^2, T relaxed when stuck);
 //  3. splits each hash's m slots into P parts (lanes j + hpw*q) and edge-colours the warp's
 //     lanes x banks multigraph with Delta colours (König): a colour is a slot position;
-//  4. fills free (lane, position) pairs with padding slots (coefficient 0, reading the zero word
+//  4. where the stage class leaves room, coordinates [0, n1) are staged twice, the second copy
+//     rotated by 16 banks; a warp's samples of those coordinates pick the copy that flattens its
+//     bank loads (with one copy, the per-bank totals alone bound C3 at 80% useful slots);
+//  5. fills free (lane, position) pairs with padding slots (coefficient 0, reading the zero word
 //     of an unused bank in the staged row's 32-word zero tail), or, in the capped variant, folds
 //     colours beyond the part size into existing positions (a few bank conflicts).
 // A cost model (wavefronts per row / measured pipe rate) picks P, warps per CTA and the variant.
@@ -101,10 +104,24 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     RPacking pk;
     pk.parts = P;
     pk.cls = -1;
-    for (int c = kNumRClasses - 1; c >= 0; --c)
-        if (kRClasses[c].S >= 32 * ((n + 31) / 32) + 32) pk.cls = c;
-    if (pk.cls < 0) return;
+    pk.S0 = 32 * ((n + 31) / 32) + 32;  // copy 0: the row + a 32-word zero tail
+    // short rows (n <= 512): a dual class, whose copy 1 holds all coordinates again at word
+    // S0 + 16 + c, i.e. in bank (c + 16) mod 32: a sample may read either copy, so only the 16 pair
+    // totals of a warp's bank loads matter (measured: a partial copy for longer rows cost more in
+    // TMA issues than it saved). Longer rows: the smallest single-copy class.
+    const bool no_copy1 = std::getenv("FASTLSH_NO_COPY1") != nullptr;  // experiment knob
+    for (int c = 0; c < kRDualClasses && pk.cls < 0 && !no_copy1; ++c)
+        if (n <= kRDualMaxN[c]) pk.cls = c;
+    if (pk.cls >= 0) {
+        pk.n1 = n;
+    } else {
+        for (int c = kNumRClasses - 1; c >= kRDualClasses; --c)
+            if (kRClasses[c].S >= pk.S0) pk.cls = c;
+        if (pk.cls < 0) return;
+        pk.n1 = 0;
+    }
     pk.S = kRClasses[pk.cls].S;
+    if (pk.n1 && pk.S0 + 16 + pk.n1 > pk.S) return;
     const int hpw = 32 / P;
     const int T = (m + P - 1) / P;
     if (T > kRMaxSlots) return;
@@ -138,11 +155,14 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     int maxdelta = 0;
     for (int bl = 0; bl < HB; ++bl) {
         const int kb = pk.block_kb[bl], h0 = pk.block_h0[bl];
+        // warp balance on bank loads; when every coordinate has two copies (n1 == n) a sample
+        // can sit in bank b or b+16, so only the 16 pair totals matter (target 2T)
+        const bool pairs = pk.n1 == n;
         std::vector<Bank> cnt(kb, Bank{});
         for (int h = 0; h < kb; ++h)
-            for (int j = 0; j < m; ++j) cnt[h][p.idx[(size_t)(h0 + h) * m + j] & 31]++;
+            for (int j = 0; j < m; ++j) cnt[h][p.idx[(size_t)(h0 + h) * m + j] & (pairs ? 15 : 31)]++;
         std::vector<Bank> load;
-        balance_warps(cnt, kb, hpw, W, T, slots_of[bl], load);
+        balance_warps(cnt, kb, hpw, W, pairs ? 2 * T : T, slots_of[bl], load);
         for (int w = 0; w < W; ++w) {
             WarpPlan& wp = plans[bl][w];
             for (int j = 0; j < hpw; ++j) {
@@ -161,8 +181,37 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
                     wp.coef.push_back(p.a[(size_t)(h0 + h) * m + jj]);
                 }
             }
+            // copies: samples of coordinates < n1 take the less loaded of banks c, c+16 (greedy in
+            // order, then flips out of the fullest banks while they lower the maximum)
+            Bank ld{};
+            std::vector<int> flex;
+            for (size_t e = 0; e < wp.word.size(); ++e) {
+                if (wp.word[e] < pk.n1) flex.push_back((int)e);
+                else ld[wp.bank[e]]++;
+            }
+            for (int e : flex) {
+                const int b0 = wp.bank[e], b1 = (b0 + 16) & 31;
+                if (ld[b1] < ld[b0]) {
+                    wp.bank[e] = b1;
+                    wp.word[e] += pk.S0 + 16;
+                }
+                ld[wp.bank[e]]++;
+            }
+            for (bool moved = !flex.empty(); moved;) {
+                moved = false;
+                for (int e : flex) {
+                    const int b = wp.bank[e], b2 = (b + 16) & 31;
+                    if (ld[b2] + 1 < ld[b]) {
+                        ld[b]--;
+                        ld[b2]++;
+                        wp.bank[e] = b2;
+                        wp.word[e] += wp.word[e] < pk.n1 ? pk.S0 + 16 : -(pk.S0 + 16);
+                        moved = true;
+                    }
+                }
+            }
             int d = T;
-            for (int b = 0; b < 32; ++b) d = std::max(d, load[w][b]);
+            for (int b = 0; b < 32; ++b) d = std::max(d, ld[b]);
             wp.delta = d;
             wp.col = color_bipartite(wp.lane, wp.bank, 32, 32, std::max(1, d));
             if (!wp.col.empty() && wp.col[0] < 0) return;  // cannot happen (König)
@@ -218,7 +267,7 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
                     for (int b = 1; b < 32; ++b)
                         if (used[(size_t)t * 32 + b] < used[(size_t)t * 32 + bb]) bb = b;
                     used[(size_t)t * 32 + bb]++;
-                    tword[(size_t)t * 32 + l] = pk.S - 32 + bb;
+                    tword[(size_t)t * 32 + l] = pk.S0 - 32 + bb;
                     tcoef[(size_t)t * 32 + l] = 0.0f;
                 }
                 // extra wavefronts: distinct words sharing a bank (equal words are a broadcast)
@@ -250,7 +299,8 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     // staging (TMA writes n/32) + code stores (1 STS wavefront per warp and row, k/32 for the
     // bulk store's reads). The LDS.32 loop runs at ~98% of the pipe with 8 or 16 warps per SM
     // (tools/microbench_lds32.cu).
-    const double wf = (double)HB * W * MS + (double)conflicts + (double)HB * n / 32.0 + (double)HB * W + k / 32.0;
+    const double wf = (double)HB * W * MS + (double)conflicts + (double)HB * (n + pk.n1) / 32.0 + (double)HB * W +
+                      k / 32.0;
     pk.cost = wf / 0.98;
     pk.ok = true;
     out = std::move(pk);

@@ -194,7 +194,7 @@ def test_fused_keys_equal_separate_kernels(name, L, K, N, extra_k):
     k = L * K + extra_k if name == "C0" else c.k
     idx, a, b = fastlsh_arrays(c.n, c.m, k, c.w, 3)
     P_fused = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(K)
-    P_plain = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    P_plain = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_kernel("smem")  # the fused path is K1's
     Kobj = fl.Keys.from_arrays(philox.key_multipliers(L, K, seed=4))
     X = data.generate(c.data, c.n, 0, N, seed=5, device="cuda")
     codes_f, keys_f = fl.hash_keys(P_fused, Kobj, X)
