@@ -118,7 +118,11 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     static_assert(MS % 2 == 0, "slots are packed two per register");
     constexpr int S = kRClasses[CLS].S, R = kRClasses[CLS].R, NS = kRClasses[CLS].NS;
     constexpr int NC = kRClasses[CLS].NC;
-    constexpr int D = NC - 2;  // a warp flushes its share of group j-D at iteration j
+    // A warp flushes its share of group j-D at iteration j: it waits for every warp to have written
+    // group j-D (slack D), and buffer reuse waits for every warp's flush of group j-NC, done at its
+    // iteration j-NC+D (slack NC-D). D = NC/2 balances the two (measured: D = NC-2 left 1-2 groups of
+    // slack whatever NC, and C3's warps waited there 18% of the time).
+    constexpr int D = NC - 1;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t row_bytes = 4u * S;  // compile-time: row r of a stage is an immediate offset
     constexpr uint32_t stage_bytes = R * row_bytes;
