@@ -301,7 +301,19 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     // (tools/microbench_lds32.cu).
     const double wf = (double)HB * W * MS + (double)conflicts + (double)HB * (n + pk.n1) / 32.0 + (double)HB * W +
                       k / 32.0;
-    pk.cost = wf / 0.98;
+    // resident warps per SM (register cap by MS as in the kernel's launch bounds, shared memory of
+    // the class): the LDS.32 loop alone runs at ~98% with 8 or 16 warps/SM, but the whole kernel
+    // needs more warps to cover its epilogue: measured slot wavefronts (+ staging) per cycle per SM,
+    // 16-warp packings 0.78-0.90 (C1, C4 P=2, C2 m=128 P=4), 8-warp ones 0.69-0.74 (C4 P=1, C2
+    // m=128 P=1) -> 8 warps/SM cost a factor 0.8
+    const int regs = MS <= 24 ? 85 : MS <= 40 ? 102 : MS <= 64 ? 128 : 255;
+    const RClass cl = kRClasses[pk.cls];
+    const int kbp = (pk.kb_max + 3) & ~3;
+    const double smem = (double)cl.NS * cl.R * cl.S * 4 + (double)cl.NC * cl.R * kbp * 4 + 1024;
+    const int by_regs = 65536 / (W * 32 * regs), by_smem = (int)(227.0 * 1024 / smem);
+    const int warps_sm = W * std::max(1, std::min(by_regs, by_smem));
+    const double rate = warps_sm >= 16 ? 0.98 : 0.98 * (0.6 + 0.4 * warps_sm / 16.0);
+    pk.cost = wf / rate;
     pk.ok = true;
     out = std::move(pk);
 }
@@ -322,6 +334,10 @@ void build_row_packing(const fastlsh_params& p, RPacking& out) {
             for (bool capped : {false, true}) {
                 RPacking t;
                 try_rows(p, P, Wmax, capped, t);
+                if (t.ok && std::getenv("FASTLSH_PACK_DEBUG"))
+                    std::fprintf(stderr, "[rpack-try] P=%d Wmax=%d capped=%d MS=%d W=%d HB=%d conflicts=%lld cost=%.1f\n",
+                                 P, Wmax, (int)capped, t.slots, t.warps, t.hash_blocks,
+                                 (long long)t.conflict_wavefronts, t.cost);
                 if (t.ok && t.cost < out.cost) out = std::move(t);
             }
         }
