@@ -259,15 +259,17 @@ def test_row_packer_preserves_slots_and_banks(lib, n, m, k):
 def test_row_packer_bench_configs(lib):
     """The bench-relevant shapes pack with few padding slots (two-copy staging flattens the bank
     loads that limit a single copy) and no bank conflicts."""
-    for name, kw in (("C1", {}), ("C3", {}), ("C4", {}), ("C2", {"m": 32})):
+    # floors: C1 sits at its bound (max bank total 1001 / 16 warps -> 63 -> MS 64), C3 at its
+    # bank-pair bound (MS 18), C4 takes P = 2 (16-warp CTAs beat 8-warp MS = 72 on the GPU)
+    for name, m, floor in (("C1", None, 0.91), ("C3", None, 0.88), ("C4", None, 0.8), ("C2", 32, 0.85)):
         c = configs.get(name)
-        m = kw.get("m", c.m)
+        m = m or c.m
         p = fl.Params.create(c.n, m, c.k, c.w, seed=1)
         pk = p.row_packing()
         assert pk is not None, name
         useful = c.k * m
         slots = pk["hash_blocks"] * pk["warps"] * 32 * pk["slots"]
-        assert useful / slots >= 0.86, (name, useful / slots, pk["slots"], pk["parts"])
+        assert useful / slots >= floor, (name, useful / slots, pk["slots"], pk["parts"])
         assert pk["conflicts"] == 0
 
 
