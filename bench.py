@@ -198,7 +198,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
     ap.add_argument("--fused-keys", action="store_true",
-                    help="build keys in K1's epilogue (measured slower on C1: 6.80 vs 6.42 ms/step)")
+                    help="K1 with keys built in its epilogue (set_table_size; measured slower than K1r)")
+    ap.add_argument("--separate-keys", action="store_true",
+                    help="codes, then the standalone key kernel (default: keys built from K1r's code tile)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
     ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build and query measurements")
@@ -251,7 +253,11 @@ def main():
     stream = torch.cuda.current_stream()
 
     fused_keys = bool(Kobj) and args.fused_keys
-    launches_per_step = len(bounds) * (1 + (1 if (Kobj and not fused_keys) else 0))
+    # default: K1r builds the keys from its shared-memory code tile (one launch per chunk) when one
+    # CTA hash block covers all k hashes (C1, C3)
+    rp = P.row_packing() if info["kernel"] == 3 else None
+    rows_fused = bool(Kobj) and not fused_keys and not args.separate_keys and rp is not None and rp["hash_blocks"] == 1
+    launches_per_step = len(bounds) * (1 + (1 if (Kobj and not fused_keys and not rows_fused) else 0))
     ev = []
 
     def step(record: bool):
@@ -261,7 +267,11 @@ def main():
             if record:
                 e[0].record(stream)
             cb = codes[:c1 - c0]
-            if Kobj and args.fused_keys:
+            if rows_fused:
+                fl.hash_keys(P, Kobj, X[c0:c1], codes=cb, keys_out=keys, col0=c0)  # one launch: codes + keys
+                if record:
+                    e[1].record(stream)
+            elif Kobj and args.fused_keys:
                 if strong:  # keys only: the codes of the 2e8 rows never reach HBM
                     fl.hash_keys(P, Kobj, X[c0:c1], keys_out=keys, with_codes=False, col0=c0)
                 else:
@@ -335,6 +345,8 @@ def main():
                 "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
                 "traffic": _traffic_from_profiles(cfg, N),
                 "kernel": ("gather_kernel (K1 fastlsh_hash, keys fused in its epilogue)" if fused_keys else
+                           "rows_kernel (K1r fastlsh_hash_keys: row-major stages, LDS.32; keys built from its "
+                           "shared-memory code tile)" if rows_fused else
                            {1: "gather_kernel (K1 fastlsh_hash)", 2: "tmem_gather_kernel (K1t fastlsh_hash)",
                             3: "rows_kernel (K1r fastlsh_hash: row-major stages, LDS.32)"}[info["kernel"]]),
                 "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
@@ -477,7 +489,7 @@ def main():
                 "config": _config_dict(cfg, world, N, N_total, len(bounds)), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks,
-                "keys_fused": fused_keys,
+                "keys_fused": "K1 epilogue" if fused_keys else "K1r code tile" if rows_fused else False,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
                                  "hash_max_over_ranks": hash_ms_max},

@@ -627,6 +627,16 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
     if (st != FASTLSH_OK) return st;
+    // K1r (one hash block): keys built from the code tile in shared memory; codes not written
+    // when codes == NULL. Falls through when K1r cannot serve the call.
+    if (rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1) {
+        const uint64_t* dr = nullptr;
+        st = keys_device(ks, dev, &dr);
+        if (st != FASTLSH_OK) return st;
+        FusedKeys fk{dr, ks->L, ks->K, keys_out, ldk};
+        st = launch_gather_rows(p, p->dev[dev], X, N, codes, nullptr, reinterpret_cast<cudaStream_t>(stream), &fk);
+        if (st != FASTLSH_EUNSUPPORTED) return st;
+    }
     const bool fusable = keys_fusable(p, ks) && !tmem_selected(p);
     if (!codes && !fusable) return FASTLSH_EINVAL;  // keys only needs the fused kernel
     if (fusable) {  // keys built in K1's epilogue (codes not written when codes == NULL)
@@ -704,9 +714,18 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         const int64_t rows = (N - r0 < chunk_rows) ? N - r0 : chunk_rows;
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
-        if (fuse) {
+        bool fused_here = false;
+        if (want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1) {
+            FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
+            st = launch_gather_rows(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
+            fused_here = st == FASTLSH_OK;
+            if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
+        }
+        if (fused_here) {
+        } else if (fuse) {
             FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
             st = launch_gather(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
+            fused_here = true;
         } else {
             st = launch_hash(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
         }
@@ -714,7 +733,7 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
         if (want_keys) {
-            if (!fuse) st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
+            if (!fused_here) st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
             if (st != FASTLSH_OK) return st;
             // keys of this chunk: [L][rows] on device -> columns r0.. of the [L][N] host matrix
             FL_CUDA(cudaMemcpy2DAsync(keys_host + r0, (size_t)N * sizeof(uint64_t), d.ws_keys[b],

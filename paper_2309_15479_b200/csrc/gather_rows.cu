@@ -21,12 +21,12 @@ RowKernelFn select_row_kernel(int MS, int cls) {
     return nullptr;
 }
 
-// stages + NC code buffers + barriers + counters + b
-size_t row_smem_bytes(const RPacking& pk) {
+// stages + NC code buffers + barriers + key multipliers + counters + b
+size_t row_smem_bytes(const RPacking& pk, int key_words = 0) {
     const RClass c = kRClasses[pk.cls];
     const int kbp = (pk.kb_max + 3) & ~3;
-    return (size_t)c.NS * c.R * c.S * 4 + (size_t)c.NC * c.R * kbp * 4 + (size_t)(c.NS + 2 * c.NC) * 8 + c.NS * 4 +
-           (size_t)kbp * 4;
+    return (size_t)c.NS * c.R * c.S * 4 + (size_t)c.NC * c.R * kbp * 4 + (size_t)(c.NS + 2 * c.NC) * 8 +
+           (size_t)key_words * 8 + c.NS * 4 + (size_t)kbp * 4;
 }
 
 }  // namespace k1r
@@ -34,14 +34,17 @@ size_t row_smem_bytes(const RPacking& pk) {
 using namespace k1r;
 
 fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
-                                  int32_t* codes, float* proj, cudaStream_t stream) {
+                                  int32_t* codes, float* proj, cudaStream_t stream, const FusedKeys* fk) {
     const RPacking& pk = p->rpack;
     if (!pk.ok || !d.r_offp) return FASTLSH_EUNSUPPORTED;
+    // keys from the code tile need every table's codes in the one block
+    if (fk && (pk.hash_blocks != 1 || (int64_t)fk->L * fk->K > p->k)) return FASTLSH_EUNSUPPORTED;
+    const int key_words = fk ? fk->L * (fk->K + 1) : 0;
     // TMA bulk row copies need 16-byte aligned rows
     if ((p->n % 4) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
     constexpr size_t kSmemMax = 227 * 1024;
     const int threads = pk.warps * 32;
-    const size_t smem = row_smem_bytes(pk);
+    const size_t smem = row_smem_bytes(pk, key_words);
     if (smem > kSmemMax) return FASTLSH_EUNSUPPORTED;
     const int R = kRClasses[pk.cls].R;
     RowKernelFn fn = select_row_kernel(pk.slots, pk.cls);
@@ -75,6 +78,11 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
         if ((pk.block_h0[bl] % 4) || (pk.block_kb[bl] % 4)) blocks_aligned = false;
     a.vec = (p->k % 4 == 0) && blocks_aligned && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
     if (std::getenv("FASTLSH_NO_VEC_STORE")) a.vec = 0;  // experiment knob (and fallback test)
+    a.kr = fk ? fk->r : nullptr;
+    a.L = fk ? fk->L : 0;
+    a.K = fk ? fk->K : 1;
+    a.keys = fk ? fk->keys : nullptr;
+    a.ldk = fk ? fk->ldk : 0;
     a.debug = 0;
     if (const char* e = std::getenv("FASTLSH_K1R_DEBUG")) a.debug = std::atoi(e);  // experiment knob
 

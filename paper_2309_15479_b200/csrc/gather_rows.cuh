@@ -52,6 +52,12 @@ struct RowArgs {
     unsigned long long* flags;
     int vec;                   // 1: the block's code runs are 16-byte aligned (16-byte copy-out)
     int debug;                 // experiment knob (FASTLSH_K1R_DEBUG): 1 no code output, 2 no refills
+    // compound keys built from the code tile in the flush (R9), when one
+    // block covers all hashes: key_l(v) = (r0 + sum_j r_{j+1} u32(c_{lK+j})) mod 2^61-1
+    const uint64_t* kr;        // multipliers [L][K+1] (nullptr: no keys)
+    int L, K;
+    uint64_t* keys;            // [L][ldk], column = row index
+    long long ldk;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,7 +136,8 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     int32_t* cbuf = reinterpret_cast<int32_t*>(smem + (size_t)NS * stage_bytes);
     const int cwords = R * a.kbp;  // one code buffer
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(cbuf + NC * cwords);
-    int* cnt = reinterpret_cast<int*>(bars + NS + 2 * NC);  // [NS] stage readers (monotone)
+    uint64_t* s_kr = reinterpret_cast<uint64_t*>(bars + NS + 2 * NC);  // [L][K+1] key multipliers (a.kr)
+    int* cnt = reinterpret_cast<int*>(s_kr + (a.kr ? a.L * (a.K + 1) : 0));  // [NS] stage readers (monotone)
     float* s_b = reinterpret_cast<float*>(cnt + NS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -162,6 +169,8 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     // zero tails (targets of padding slots), never overwritten by the row copies
     for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + a.S0 - 32 + (i & 31)] = 0.f;
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
+    if (a.kr)
+        for (int i = tid; i < a.L * (a.K + 1); i += nthreads) s_kr[i] = a.kr[i];
 
     uint32_t opk[MS / 2];
     float cf[MS];
@@ -210,7 +219,9 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
         const int rows = live_rows(a.N, row0, R);
         const int32_t* src = cbuf + cg * cwords;
         int32_t* o = static_cast<int32_t*>(out) + row0 * a.k + h0;
-        if (a.vec) {
+        if (!out) {
+            // keys only: the codes never leave shared memory
+        } else if (a.vec) {
             // unit u = tid + i*nthreads = (row r, chunk q), stepped without divisions
             for (int r = r_first, q = q_first; r < rows;) {
                 const int4 v = *reinterpret_cast<const int4*>(src + r * a.kbp + 4 * q);
@@ -226,6 +237,29 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
             for (int u = tid; u < rows * kb; u += nthreads) {
                 const int r = u / kb, h = u - r * kb;
                 o[(long long)r * a.k + h] = src[r * a.kbp + h];
+            }
+        }
+        if (a.kr) {
+            // items (table t, row r), rows fastest: 8 lanes write one 64-byte run of a table.
+            // Exact 128-bit accumulation of the K products (each < 2^93), one Mersenne reduction.
+            const int K = a.K;
+            for (int u = tid; u < a.L * R; u += nthreads) {
+                const int r = u % R, t = u / R;
+                if (r >= rows) continue;
+                const uint64_t* rl = s_kr + t * (K + 1);
+                const int32_t* cc = src + r * a.kbp + t * K;
+                uint64_t lo = rl[0], hi = 0;
+                for (int jj = 0; jj < K; ++jj) {
+                    const uint64_t rv = rl[jj + 1];
+                    const uint64_t u32c = (uint32_t)cc[jj];
+                    const uint64_t plo = rv * u32c;
+                    lo += plo;
+                    hi += __umul64hi(rv, u32c) + (lo < plo ? 1 : 0);
+                }
+                constexpr uint64_t P61 = (1ull << 61) - 1;
+                uint64_t x = (lo & P61) + (lo >> 61) + (hi << 3);  // 2^64 = 8 (mod 2^61 - 1)
+                x = (x & P61) + (x >> 61);
+                a.keys[(long long)t * a.ldk + row0 + r] = x >= P61 ? x - P61 : x;
             }
         }
         __syncwarp();

@@ -193,9 +193,11 @@ bool keys_fusable(const fastlsh_params* p, const fastlsh_keys* keys);
 void build_tmem_packing(const fastlsh_params& p, TPacking& out);
 fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                                   int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
-// gather_rows.cu
+// gather_rows.cu (fk: compound keys built in the flush of the code tile; needs one hash block)
+struct FusedKeys;
 fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X,
-                                  int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
+                                  int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
+                                  const FusedKeys* fk = nullptr);
 // the hashing dispatcher (api.cu): K1t when selected/applicable, else K1
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream);

@@ -369,6 +369,29 @@ def test_rows_kernel_determinism_and_flags():
     assert sat == int(idx6.sum()) and (codes[6][idx6] == -(2 ** 31)).all()
 
 
+@pytest.mark.parametrize("name,L,K,N", [("C1", 50, 10, 3001), ("C3", 16, 16, 4099), ("C0", 5, 12, 999),
+                                         ("C4", 200, 10, 1203)])
+def test_rows_kernel_keys_from_code_tile(name, L, K, N):
+    """K1r builds the compound keys from its shared-memory code tile when one CTA block covers all
+    hashes (C0/C1/C3); bit-exact vs codes + the standalone key kernel, also keys-only and into
+    columns [col0, col0 + N) of a wider table. C4 (8 blocks) takes the separate kernel, same result."""
+    c = configs.get(name)
+    idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 3)
+    P = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    assert P.info()["kernel"] == 3
+    Kobj = fl.Keys.from_arrays(philox.key_multipliers(L, K, seed=4))
+    X = data.generate(c.data, c.n, 0, N, seed=5, device="cuda")
+    codes_f, keys_f = fl.hash_keys(P, Kobj, X)
+    codes_p = fl.fastlsh_hash(P, X)
+    keys_p = fl.build_keys(Kobj, codes_p)
+    assert torch.equal(codes_f, codes_p)
+    assert torch.equal(keys_f, keys_p)
+    if P.row_packing()["hash_blocks"] == 1:
+        wide = torch.zeros((L, N + 77), dtype=torch.int64, device="cuda")
+        _, w2 = fl.hash_keys(P, Kobj, X, keys_out=wide, with_codes=False, col0=77)
+        assert torch.equal(w2[:, 77:], keys_p) and (w2[:, :77] == 0).all()
+
+
 def test_chunked_key_build_equals_whole():
     """Keys built chunk by chunk into columns [c0, c1) of one [L][N] table (the C3 bench path)."""
     c = configs.get("C3")
