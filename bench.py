@@ -256,7 +256,9 @@ def main():
     # default: K1r builds the keys from its shared-memory code tile (one launch per chunk) when one
     # CTA hash block covers all k hashes (C1, C3)
     rp = P.row_packing() if info["kernel"] == 3 else None
-    rows_fused = bool(Kobj) and not fused_keys and not args.separate_keys and rp is not None and rp["hash_blocks"] == 1
+    rows_fused = (bool(Kobj) and not fused_keys and not args.separate_keys and rp is not None and rp["hash_blocks"] == 1
+                  # the library's rule (api.cu rows_keys_pay): key work small next to the gathers
+                  and cfg.L * cfg.K <= 0.75 * rp["hash_blocks"] * rp["warps"] * rp["slots"])
     launches_per_step = len(bounds) * (1 + (1 if (Kobj and not fused_keys and not rows_fused) else 0))
     ev = []
 

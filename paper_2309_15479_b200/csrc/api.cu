@@ -132,6 +132,13 @@ bool rows_selected(const fastlsh_params* p) {
     if (p->n % 4) return false;  // rows are not 16-byte multiples: no bulk row copies
     return p->kernel == 0 && p->rpack.cost <= p->pack.cost * kK1Derate;
 }
+// Keys from K1r's code tile pay off when the key work (L*K products per row, spread over the CTA)
+// is small next to the gather work (HB*W*MS LDS.32 wavefronts per row): measured C1 (500 vs 1024)
+// 4.49 vs 4.59 ms for hash + keys, C3 (256 vs 144) 10.9 vs 9.8 ms per 8M rows.
+bool rows_keys_pay(const fastlsh_params* p, const fastlsh_keys* ks) {
+    const RPacking& r = p->rpack;
+    return (double)ks->L * ks->K <= 0.75 * (double)r.hash_blocks * r.warps * r.slots;
+}
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
     if (tmem_selected(p)) {
@@ -629,7 +636,8 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     if (st != FASTLSH_OK) return st;
     // K1r (one hash block): keys built from the code tile in shared memory; codes not written
     // when codes == NULL. Falls through when K1r cannot serve the call.
-    if (rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1) {
+    if (rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
+        (!codes || rows_keys_pay(p, ks))) {
         const uint64_t* dr = nullptr;
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;
@@ -715,7 +723,8 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
         bool fused_here = false;
-        if (want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1) {
+        if (want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
+            rows_keys_pay(p, ks)) {
             FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
             st = launch_gather_rows(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
             fused_here = st == FASTLSH_OK;
