@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--rows", type=int, default=262144)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--keys", action="store_true")
+    ap.add_argument("--fused-keys", action="store_true", help="hash_keys (K1r builds keys from its code tile)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "smem", "tmem", "rows"])
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--dense", action="store_true", help="time the tcgen05 dense baseline too")
@@ -30,11 +31,14 @@ def main():
     m = args.m or c.m
     P = fl.Params.create(c.n, m, c.k, c.w, seed=c.seed)
     P.set_kernel(args.kernel)
-    K = fl.Keys.create(c.L, c.K, seed=c.seed) if (args.keys and c.L) else None
+    K = fl.Keys.create(c.L, c.K, seed=c.seed) if ((args.keys or args.fused_keys) and c.L) else None
     X = data.generate(c.data, c.n, 0, args.rows, seed=c.seed, device="cuda")
     codes = torch.empty((args.rows, c.k), dtype=torch.int32, device="cuda")
     keys = torch.empty((c.L, args.rows), dtype=torch.int64, device="cuda") if K else None
     for _ in range(args.iters):
+        if K and args.fused_keys:
+            fl.hash_keys(P, K, X, codes=codes, keys_out=keys)
+            continue
         fl.fastlsh_hash(P, X, out=codes)
         if K:
             fl.build_keys(K, codes, out=keys)
