@@ -212,10 +212,10 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     const int q4 = kb >> 2;  // 16-byte chunks per row of the block
     const int r_first = q4 ? tid / q4 : R, q_first = q4 ? tid - r_first * q4 : 0;
     const int r_step = q4 ? nthreads / q4 : 0, q_step = q4 ? nthreads - r_step * q4 : 0;
-    auto flush_share = [&](long long g) {
-        const int cg = (int)(g % NC);
-        mbar_wait_warp(CFULL(cg), (uint32_t)((g / NC) & 1));
-        const long long row0 = group_of(g) * R;
+    // (buffer cg, its CFULL parity and the group's first row are tracked by the caller: no 64-bit
+    // divisions per group)
+    auto flush_share = [&](int cg, uint32_t pg, long long row0) {
+        mbar_wait_warp(CFULL(cg), pg);
         const int rows = live_rows(a.N, row0, R);
         const int32_t* src = cbuf + cg * cwords;
         int32_t* o = static_cast<int32_t*>(out) + row0 * a.k + h0;
@@ -278,7 +278,12 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     int s = 0;         // stage of group j
     uint32_t ph = 0;   // its full-barrier parity
     int c = 0;         // code buffer of group j
-    for (long long j = 0; j < iters; ++j) {
+    uint32_t cph = 0;  // (j / NC) & 1: the CEMPTY parity of buffer reuse is cph ^ 1
+    int fc = 0;        // flush: buffer of group j - D, its CFULL parity, its first row
+    uint32_t fph = 0;
+    const long long row_step = gpr * R;
+    long long row0 = rs * R, frow0 = rs * R;
+    for (long long j = 0; j < iters; ++j, row0 += row_step) {
         // gather-FMA: R rows per slot, one LDS.32 (one wavefront per warp) each
         if (!(a.debug & 2) || j < NS) mbar_wait_warp(FULL(s), ph);
         const uint32_t sb = stage0 + s * stage_bytes;
@@ -301,7 +306,6 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
         }
-        const long long row0 = group_of(j) * R;
         const int nrows = live_rows(a.N, row0, R);
         if (a.debug & 1) {
             if (lane == 0 && acc[0] == 1234.5f) a.flags[0] = 0;  // keep the sums alive
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
             }
             continue;
         }
-        if (j >= NC) mbar_wait_warp(CEMPTY(c), (uint32_t)(((j - NC) / NC) & 1));
+        if (j >= NC) mbar_wait_warp(CEMPTY(c), cph ^ 1u);
         if (storing) {
             int32_t* dst = cbuf + c * cwords + my_h;
             if (a.proj) {
@@ -344,15 +348,32 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(CFULL(c));  // release: this warp's codes of group j are in the buffer
-        if (j >= D) flush_share(j - D);
+        if (j >= D) {
+            flush_share(fc, fph, frow0);
+            frow0 += row_step;
+            if (++fc == NC) {
+                fc = 0;
+                fph ^= 1u;
+            }
+        }
         if (++s == NS) {
             s = 0;
             ph ^= 1u;
         }
-        if (++c == NC) c = 0;
+        if (++c == NC) {
+            c = 0;
+            cph ^= 1u;
+        }
     }
     if (!(a.debug & 1))
-        for (long long g = iters > D ? iters - D : 0; g < iters; ++g) flush_share(g);
+        for (long long g = iters > D ? iters - D : 0; g < iters; ++g) {
+            flush_share(fc, fph, frow0);
+            frow0 += row_step;
+            if (++fc == NC) {
+                fc = 0;
+                fph ^= 1u;
+            }
+        }
 }
 
 typedef void (*RowKernelFn)(RowArgs);
