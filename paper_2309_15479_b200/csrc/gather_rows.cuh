@@ -128,7 +128,7 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     // group j-D (slack D), and buffer reuse waits for every warp's flush of group j-NC, done at its
     // iteration j-NC+D (slack NC-D). D = NC/2 balances the two (measured: D = NC-2 left 1-2 groups of
     // slack whatever NC, and C3's warps waited there 18% of the time).
-    constexpr int D = NC - 1;
+    constexpr int D = kRClasses[CLS].D;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t row_bytes = 4u * S;  // compile-time: row r of a stage is an immediate offset
     constexpr uint32_t stage_bytes = R * row_bytes;

@@ -86,10 +86,10 @@ constexpr int kRMaxSlots = 128;
 // Stage geometry per row-stride class (compile-time in the kernel, so the R rows of a stage are
 // immediate offsets of one LDS address): S words per staged row, R rows per stage, NS stages, NC
 // code buffers (a deep code ring lets fast warps run ahead of the flush of a slow warp's group).
-struct RClass { int S, R, NS, NC; };
+struct RClass { int S, R, NS, NC, D; };  // D: code-ring flush lag (gather_rows.cuh)
 // Classes 0-2 (n <= 128 / 256 / 512) stage a full second copy (n1 = n); classes 3-5 one copy.
-constexpr RClass kRClasses[] = {{320, 8, 3, 5}, {576, 8, 4, 6}, {1088, 8, 3, 5}, {1056, 8, 3, 6},
-                                {2080, 4, 4, 8}, {4128, 4, 3, 3}};
+constexpr RClass kRClasses[] = {{320, 8, 3, 5, 3}, {576, 8, 4, 6, 5}, {1088, 8, 3, 5, 4}, {1056, 8, 3, 6, 5},
+                                {2080, 4, 4, 8, 7}, {4128, 4, 3, 3, 2}};
 constexpr int kRDualClasses = 3;
 constexpr int kRDualMaxN[kRDualClasses] = {128, 256, 512};
 constexpr int kNumRClasses = 6;
