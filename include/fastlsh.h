@@ -137,7 +137,8 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
 
 /* codes[r*k + i] = floor((a_i . S_i(X[r]) + b_i) / w) as int32, for r < N, i < k — Eq. 5.
- * fp32 accumulation (K1: bank-conflict-free slot order in chunks of <= 64 products; K1t: slots
+ * fp32 accumulation (K1r: each lane sums <= 128 products in its bank-scheduled slot order, the
+ * P <= 32 parts of a hash then by an xor butterfly; K1: chunks of <= 64 products; K1t: slots
  * grouped by 128-coordinate block, one accumulator over <= 128 products), then
  * __fadd_rn(p, b), __fdiv_rn(., w), floor toward -inf. Non-finite or out-of-int32 quotients
  * write INT32_MIN and count in the params' flags. Requires fastlsh_params_upload. */
