@@ -332,3 +332,17 @@ def test_table_query_transform_argument_checks(lib):
     assert lib.fastlsh_mips_transform(V, 5, 4, None, 0, V, None) == fl.EINVAL  # data transform needs kappa
     rc = lib.fastlsh_normalize_rows(V, 5, 4, V, None)
     assert rc in (fl.ECUDA, fl.EUNSUPPORTED)
+
+
+@pytest.mark.parametrize("n,dual", [(4, True), (128, True), (256, True), (512, True), (516, False), (960, False),
+                                    (4096, False)])
+def test_row_packing_stage_classes(lib, n, dual):
+    """Rows of n <= 512 are staged twice (second copy rotated 16 banks, n1 = n); longer rows once.
+    The staged stride is a multiple of 32 words and holds copy 0, its zero tail and copy 1."""
+    p = fl.Params.create(n, 16, 64, 1.0, seed=2)
+    pk = p.row_packing()
+    assert pk is not None
+    S, S0, n1 = pk["S"], pk["S0"], pk["n1"]
+    assert S % 32 == 0 and S0 == 32 * ((n + 31) // 32) + 32
+    assert n1 == (n if dual else 0)
+    assert (S0 + 16 + n1 <= S) if dual else (S0 <= S)
