@@ -112,6 +112,8 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     const bool no_copy1 = std::getenv("FASTLSH_NO_COPY1") != nullptr;  // experiment knob
     for (int c = 0; c < kRDualClasses && pk.cls < 0 && !no_copy1; ++c)
         if (n <= kRDualMaxN[c]) pk.cls = c;
+    // experiment knob: a dual copy in the 2080-word class (4 rows per stage) for n <= 1024
+    if (pk.cls < 0 && std::getenv("FASTLSH_ROW_DUAL") && 2 * pk.S0 - 16 <= kRClasses[4].S) pk.cls = 4;
     if (pk.cls >= 0) {
         pk.n1 = n;
     } else {
