@@ -99,7 +99,7 @@ void balance_warps(const std::vector<Bank>& cnt, int kb, int hpw, int W, int T, 
 }
 
 // One packing for P parts, at most Wmax warps per CTA, capped (fold beyond the part size) or not.
-void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& out) {
+void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& out, bool dual4 = false) {
     const int n = p.n, m = p.m, k = p.k;
     RPacking pk;
     pk.parts = P;
@@ -112,8 +112,12 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     const bool no_copy1 = std::getenv("FASTLSH_NO_COPY1") != nullptr;  // experiment knob
     for (int c = 0; c < kRDualClasses && pk.cls < 0 && !no_copy1; ++c)
         if (n <= kRDualMaxN[c]) pk.cls = c;
-    // experiment knob: a dual copy in the 2080-word class (4 rows per stage) for n <= 1024
-    if (pk.cls < 0 && std::getenv("FASTLSH_ROW_DUAL") && 2 * pk.S0 - 16 <= kRClasses[4].S) pk.cls = 4;
+    // dual4: a dual copy in the 2080-word class (4 rows per stage) for rows up to ~1000 words, tried
+    // beside the single-copy class by the cost model (C4: 2.15 -> 1.90 ms; C1 loses, 3.92 -> 4.42)
+    if (pk.cls < 0 && dual4) {
+        if (2 * pk.S0 - 16 > kRClasses[4].S) return;
+        pk.cls = 4;
+    }
     if (pk.cls >= 0) {
         pk.n1 = n;
     } else {
@@ -315,7 +319,10 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     const int by_regs = 65536 / (W * 32 * regs), by_smem = (int)(227.0 * 1024 / smem);
     const int warps_sm = W * std::max(1, std::min(by_regs, by_smem));
     const double rate = warps_sm >= 16 ? 0.98 : 0.98 * (0.6 + 0.4 * warps_sm / 16.0);
-    pk.cost = wf / rate;
+    // per-group costs (waits, epilogue, flush) ~ 97 wavefront-equivalents per warp and group,
+    // fitted to C1 single (R = 8) vs dual (R = 4) copies and checked on C4 (model 0.877, measured
+    // 0.884 for the dual/single time ratio)
+    pk.cost = (wf + (double)HB * W * 97.0 / cl.R) / rate;
     pk.ok = true;
     out = std::move(pk);
 }
@@ -333,14 +340,18 @@ void build_row_packing(const fastlsh_params& p, RPacking& out) {
         if ((p.m + P - 1) / P > kRMaxSlots) continue;
         if (force_p && P != force_p) continue;
         for (int Wmax : {16, 8}) {
-            for (bool capped : {false, true}) {
+            for (int variant = 0; variant < 2; ++variant) {
+                const bool capped = variant & 1;
+                for (bool dual4 : {false, true}) {
+                if (dual4 && (p.n <= kRDualMaxN[kRDualClasses - 1] || std::getenv("FASTLSH_NO_COPY1"))) continue;
                 RPacking t;
-                try_rows(p, P, Wmax, capped, t);
+                try_rows(p, P, Wmax, capped, t, dual4);
                 if (t.ok && std::getenv("FASTLSH_PACK_DEBUG"))
-                    std::fprintf(stderr, "[rpack-try] P=%d Wmax=%d capped=%d MS=%d W=%d HB=%d conflicts=%lld cost=%.1f\n",
-                                 P, Wmax, (int)capped, t.slots, t.warps, t.hash_blocks,
+                    std::fprintf(stderr, "[rpack-try] P=%d Wmax=%d capped=%d dual4=%d MS=%d W=%d HB=%d conflicts=%lld cost=%.1f\n",
+                                 P, Wmax, (int)capped, (int)dual4, t.slots, t.warps, t.hash_blocks,
                                  (long long)t.conflict_wavefronts, t.cost);
                 if (t.ok && t.cost < out.cost) out = std::move(t);
+                }
             }
         }
     }
