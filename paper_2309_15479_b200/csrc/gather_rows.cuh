@@ -386,7 +386,8 @@ RowKernelFn row_kernel_for(int cls) {
         case 2: return rows_kernel<MS, 2>;
         case 3: return rows_kernel<MS, 3>;
         case 4: return rows_kernel<MS, 4>;
-        default: return rows_kernel<MS, 5>;
+        case 5: return rows_kernel<MS, 5>;
+        default: return rows_kernel<MS, 6>;
     }
 }
 

@@ -99,7 +99,7 @@ void balance_warps(const std::vector<Bank>& cnt, int kb, int hpw, int W, int T, 
 }
 
 // One packing for P parts, at most Wmax warps per CTA, capped (fold beyond the part size) or not.
-void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& out, bool dual4 = false) {
+void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& out, int dual_cls = -1) {
     const int n = p.n, m = p.m, k = p.k;
     RPacking pk;
     pk.parts = P;
@@ -112,16 +112,17 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     const bool no_copy1 = std::getenv("FASTLSH_NO_COPY1") != nullptr;  // experiment knob
     for (int c = 0; c < kRDualClasses && pk.cls < 0 && !no_copy1; ++c)
         if (n <= kRDualMaxN[c]) pk.cls = c;
-    // dual4: a dual copy in the 2080-word class (4 rows per stage) for rows up to ~1000 words, tried
-    // beside the single-copy class by the cost model (C4: 2.15 -> 1.90 ms; C1 loses, 3.92 -> 4.42)
-    if (pk.cls < 0 && dual4) {
-        if (2 * pk.S0 - 16 > kRClasses[4].S) return;
-        pk.cls = 4;
+    // dual_cls (4 or 6): a dual copy in a 2080-word class (4- or 8-row stages) for rows up to ~1000
+    // words, tried beside the single-copy class by the cost model (C4: 2.15 -> 1.90 ms with 4-row
+    // stages; C1 loses with them, 3.92 -> 4.42)
+    if (pk.cls < 0 && dual_cls >= 0) {
+        if (2 * pk.S0 - 16 > kRClasses[dual_cls].S) return;
+        pk.cls = dual_cls;
     }
     if (pk.cls >= 0) {
         pk.n1 = n;
     } else {
-        for (int c = kNumRClasses - 1; c >= kRDualClasses; --c)
+        for (int c = 5; c >= kRDualClasses; --c)  // single-copy classes 3-5
             if (kRClasses[c].S >= pk.S0) pk.cls = c;
         if (pk.cls < 0) return;
         pk.n1 = 0;
@@ -305,7 +306,9 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     // staging (TMA writes n/32) + code stores (1 STS wavefront per warp and row, k/32 for the
     // bulk store's reads). The LDS.32 loop runs at ~98% of the pipe with 8 or 16 warps per SM
     // (tools/microbench_lds32.cu).
-    const double wf = (double)HB * W * MS + (double)conflicts + (double)HB * (n + pk.n1) / 32.0 + (double)HB * W +
+    // staged words count twice: TMA writes into shared memory measured ~2x their 128-byte
+    // wavefronts (C1 with a second copy: 3% fewer slots, 2.6% slower)
+    const double wf = (double)HB * W * MS + (double)conflicts + 2.0 * HB * (n + pk.n1) / 32.0 + (double)HB * W +
                       k / 32.0;
     // resident warps per SM (register cap by MS as in the kernel's launch bounds, shared memory of
     // the class): the LDS.32 loop alone runs at ~98% with 8 or 16 warps/SM, but the whole kernel
@@ -332,7 +335,7 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
 void build_row_packing(const fastlsh_params& p, RPacking& out) {
     out = RPacking();
     if (p.n <= 0 || p.m <= 0 || p.k <= 0) return;
-    if (32 * ((p.n + 31) / 32) + 32 > kRClasses[kNumRClasses - 1].S) return;  // largest stage class
+    if (32 * ((p.n + 31) / 32) + 32 > kRClasses[5].S) return;  // largest stage class
     if (std::getenv("FASTLSH_NO_ROWS")) return;       // experiment knob
     int force_p = 0;
     if (const char* e = std::getenv("FASTLSH_ROW_PARTS")) force_p = std::atoi(e);
@@ -342,13 +345,15 @@ void build_row_packing(const fastlsh_params& p, RPacking& out) {
         for (int Wmax : {16, 8}) {
             for (int variant = 0; variant < 2; ++variant) {
                 const bool capped = variant & 1;
-                for (bool dual4 : {false, true}) {
-                if (dual4 && (p.n <= kRDualMaxN[kRDualClasses - 1] || std::getenv("FASTLSH_NO_COPY1"))) continue;
+                for (int dual_cls : {-1, 4, 6}) {
+                if (dual_cls >= 0 && (p.n <= kRDualMaxN[kRDualClasses - 1] || std::getenv("FASTLSH_NO_COPY1"))) continue;
+                if (const char* e = std::getenv("FASTLSH_DUAL_CLS"))  // experiment knob: pin the option
+                    if (std::atoi(e) != dual_cls) continue;
                 RPacking t;
-                try_rows(p, P, Wmax, capped, t, dual4);
+                try_rows(p, P, Wmax, capped, t, dual_cls);
                 if (t.ok && std::getenv("FASTLSH_PACK_DEBUG"))
-                    std::fprintf(stderr, "[rpack-try] P=%d Wmax=%d capped=%d dual4=%d MS=%d W=%d HB=%d conflicts=%lld cost=%.1f\n",
-                                 P, Wmax, (int)capped, (int)dual4, t.slots, t.warps, t.hash_blocks,
+                    std::fprintf(stderr, "[rpack-try] P=%d Wmax=%d capped=%d dual_cls=%d MS=%d W=%d HB=%d conflicts=%lld cost=%.1f\n",
+                                 P, Wmax, (int)capped, dual_cls, t.slots, t.warps, t.hash_blocks,
                                  (long long)t.conflict_wavefronts, t.cost);
                 if (t.ok && t.cost < out.cost) out = std::move(t);
                 }
