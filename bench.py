@@ -203,6 +203,8 @@ def main():
                     help="time the step with K1r building the keys from its code tile (one launch) instead of "
                          "codes + the key kernel; the default reports it as a side measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N > 1: wait for each step's key all-gather before the next step hashes")
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
     ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build and query measurements")
     ap.add_argument("--queries", type=int, default=10_000, help="queries answered in the query measurement")
@@ -251,6 +253,12 @@ def main():
     codes = torch.empty((chunk, cfg.k), dtype=torch.int32, device=dev)
     keys = torch.empty((cfg.L, N), dtype=torch.int64, device=dev) if Kobj else None
     gathered = torch.empty((cfg.L, world * N), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
+    # N > 1: the key all-gather of step j runs on NCCL's stream while step j+1 hashes into the other
+    # keys buffer (double-buffered); step j+1 waits for it before launching its own all-gather
+    overlap = gathered is not None and not args.no_overlap
+    keys_bufs = [keys, torch.empty_like(keys)] if overlap else [keys]
+    pending = []  # NCCL works of the previous step's all-gather
+    step_no = [0]
     stream = torch.cuda.current_stream()
 
     fused_keys = bool(Kobj) and args.fused_keys
@@ -268,6 +276,8 @@ def main():
 
     def step(record: bool):
         marks = []  # per chunk: (before hash, after hash, after keys)
+        keys = keys_bufs[step_no[0] % len(keys_bufs)]
+        step_no[0] += 1
         for c0, c1 in bounds:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
             if record:
@@ -297,10 +307,20 @@ def main():
         if record:
             ea[0].record(stream)
         if gathered is not None:
-            allgather_keys(keys, out=gathered)
+            if overlap:
+                for w in pending:  # the previous step's all-gather (overlapped with this step's hashing)
+                    w.wait()
+                pending[:] = allgather_keys(keys, out=gathered, wait=False)
+            else:
+                allgather_keys(keys, out=gathered)
         if record:
             ea[1].record(stream)
             ev.append((marks, ea))
+
+    def drain():
+        for w in pending:
+            w.wait()
+        pending.clear()
 
     smi_index = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -313,6 +333,7 @@ def main():
     sampler.start()
     for _ in range(args.warmup):
         step(False)
+    drain()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -322,6 +343,7 @@ def main():
     t0.record(stream)
     for _ in range(args.steps):
         step(True)
+    drain()  # the last step's all-gather is inside the timed region
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:

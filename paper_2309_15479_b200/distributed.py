@@ -21,11 +21,13 @@ def shard_rows(N: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def allgather_keys(keys_local, out=None, group=None):
+def allgather_keys(keys_local, out=None, group=None, wait=True):
     """All-gather table-major keys [L][N_local] (int64 view of u64) into [L][world * N_local].
 
     Equal shard sizes are required (all_gather_into_tensor semantics); the per-table calls are
-    issued asynchronously back to back and waited on together, so NCCL pipelines them. Returns `out`.
+    issued asynchronously back to back and waited on together, so NCCL pipelines them. Returns `out`,
+    or (wait=False) the list of pending works: the caller waits on them later (on NCCL that makes
+    its current stream wait), e.g. after overlapping the next step's hashing.
     """
     import torch
     import torch.distributed as dist
@@ -38,6 +40,8 @@ def allgather_keys(keys_local, out=None, group=None):
         raise ValueError("output must be [L, world * N_local]")
     works = [dist.all_gather_into_tensor(out[l], keys_local[l].contiguous(), group=group, async_op=True)
              for l in range(L)]
+    if not wait:
+        return works
     for w in works:
         w.wait()
     return out

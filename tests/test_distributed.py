@@ -49,6 +49,12 @@ def _worker(rank, world, port, q):
         out = allgather_keys(torch.from_numpy(local.copy()))
         full = okeys.build_keys(codes, r, L, K).view(np.int64)
         ok_layout = np.array_equal(out.numpy(), full)
+        # the bench's overlapped form: works returned unwaited, waited before the buffer is reused
+        out2 = torch.zeros_like(out)
+        works = allgather_keys(torch.from_numpy(local.copy()), out=out2, wait=False)
+        for w in works:
+            w.wait()
+        ok_layout = ok_layout and len(works) == L and np.array_equal(out2.numpy(), full)
         m = max_over_ranks(1.0 + rank)
         q.put((rank, ok_layout, m))
     finally:
