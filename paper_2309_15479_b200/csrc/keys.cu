@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -232,6 +233,108 @@ FastKeysFn fast_keys_for(int K, int V) {
     }
 }
 
+// TMA-staged path (K <= 16, k % 4 == 0, codes 16-byte aligned): a persistent CTA of 512 threads
+// streams blocks of RB consecutive code rows — one bulk copy of RB*k*4 contiguous bytes per block
+// into a 3-stage shared-memory ring (complete_tx on an mbarrier) — so tens of KB per SM are in
+// flight without costing registers (the register-batched kernel above reached ~4 TB/s on C1).
+// Thread (t, j) owns table t (its K multipliers held in registers as 21-bit limbs, loaded once) and
+// rows j, j + TPT, ... of every block (TPT = threads per table): per term one shared-memory code
+// load and three IMAD.WIDE.U32, the exact limb combination of keys_kernel_fast.
+constexpr int kTKThreads = 512;
+constexpr int kTKStages = 3;
+
+template <int K>
+__global__ void __launch_bounds__(kTKThreads, 1) keys_kernel_tma(const uint64_t* __restrict__ rmul,
+                                                             const int32_t* __restrict__ codes, long long N,
+                                                             int k, int L, uint64_t* __restrict__ out,
+                                                             long long ldk, int RB) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int stage_words = RB * k;
+    int32_t* stage = reinterpret_cast<int32_t*>(sm);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(stage + kTKStages * stage_words);
+    const int tid = threadIdx.x;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+    if (tid == 0) {
+        for (int s = 0; s < kTKStages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int TPT = blockDim.x / L;             // threads per table (>= 1: L <= blockDim)
+    const int t = tid / TPT, j = tid - t * TPT;
+    const bool live = t < L;
+    uint32_t r0[K], r1[K], r2[K];
+    uint64_t rc = 0;
+    if (live) {
+        rc = rmul[(size_t)t * (K + 1)];
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj) {
+            const uint64_t r = rmul[(size_t)t * (K + 1) + jj + 1];
+            r0[jj] = (uint32_t)(r & 0x1fffff);
+            r1[jj] = (uint32_t)((r >> 21) & 0x1fffff);
+            r2[jj] = (uint32_t)(r >> 42);
+        }
+    }
+    const long long nblocks = (N + RB - 1) / RB;
+    const long long my = blockIdx.x < nblocks ? (nblocks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto issue = [&](long long i) {  // thread 0: block blockIdx.x + i*gridDim.x into stage i % kTKStages
+        const long long b = blockIdx.x + i * gridDim.x;
+        const long long rows = min((long long)RB, N - b * RB);
+        const uint32_t bytes = (uint32_t)(rows * k * 4);
+        const uint32_t bar = bar0 + 8u * (uint32_t)(i % kTKStages);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + (i % kTKStages) * stage_words);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(codes + b * RB * (long long)k), "r"(bytes), "r"(bar)
+                     : "memory");
+    };
+    if (tid == 0)
+        for (long long i = 0; i < kTKStages && i < my; ++i) issue(i);
+    for (long long i = 0; i < my; ++i) {
+        const long long b = blockIdx.x + i * gridDim.x;
+        const int rows = (int)min((long long)RB, N - b * RB);
+        const uint32_t bar = bar0 + 8u * (uint32_t)(i % kTKStages), parity = (uint32_t)((i / kTKStages) & 1);
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "TK_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra TK_WAIT_%=;\n}" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+        const int32_t* st = stage + (i % kTKStages) * stage_words;
+        if (live) {
+            for (int r = j; r < rows; r += TPT) {
+                const int32_t* cc = st + r * k + t * K;
+                uint64_t s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+                for (int jj = 0; jj < K; ++jj) {
+                    const uint32_t c = (uint32_t)cc[jj];
+                    s0 += (uint64_t)r0[jj] * c;
+                    s1 += (uint64_t)r1[jj] * c;
+                    s2 += (uint64_t)r2[jj] * c;
+                }
+                out[(long long)t * ldk + b * RB + r] =
+                    mod61(rc + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
+            }
+        }
+        __syncthreads();  // every thread is done with this stage
+        if (tid == 0 && i + kTKStages < my) issue(i + kTKStages);
+    }
+}
+
+typedef void (*TmaKeysFn)(const uint64_t*, const int32_t*, long long, int, int, uint64_t*, long long, int);
+TmaKeysFn tma_keys_for(int K) {
+    switch (K) {
+#define FASTLSH_TKCASE(X) \
+    case X: return keys_kernel_tma<X>;
+        FASTLSH_TKCASE(1) FASTLSH_TKCASE(2) FASTLSH_TKCASE(3) FASTLSH_TKCASE(4) FASTLSH_TKCASE(5) FASTLSH_TKCASE(6)
+        FASTLSH_TKCASE(7) FASTLSH_TKCASE(8) FASTLSH_TKCASE(9) FASTLSH_TKCASE(10) FASTLSH_TKCASE(11) FASTLSH_TKCASE(12)
+        FASTLSH_TKCASE(13) FASTLSH_TKCASE(14) FASTLSH_TKCASE(15) FASTLSH_TKCASE(16)
+#undef FASTLSH_TKCASE
+        default: return nullptr;
+    }
+}
+
 }  // namespace
 
 fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r,
@@ -240,6 +343,30 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
     const int L = keys->L, K = keys->K;
     const uintptr_t base = reinterpret_cast<uintptr_t>(codes);
     const int vec = (k % 4 == 0 && K % 4 == 0 && base % 16 == 0) ? 4 : (k % 2 == 0 && K % 2 == 0 && base % 8 == 0) ? 2 : 1;
+    // TMA-staged path: rows 16-byte multiples, codes 16-byte aligned, every table owns >= 1 thread
+    // (k % 32 == 0 puts every staged row on the same banks, so the lanes of one table read one bank:
+    // C3, k = 256, measured 7.7 vs 2.3 ms — those shapes keep the register-batched kernel)
+    TmaKeysFn tk = (k % 4 == 0 && k % 32 != 0 && base % 16 == 0 && L <= kTKThreads &&
+                    !std::getenv("FASTLSH_KEYS_NO_TMA"))
+                       ? tma_keys_for(K) : nullptr;
+    if (tk) {
+        int RB = (int)((56 * 1024) / ((long long)k * 4)) & ~7;  // ~56 KB per stage, multiple of 8 rows
+        if (RB > 64) RB = 64;
+        const size_t smem = (size_t)kTKStages * RB * k * 4 + kTKStages * 8;
+        if (RB >= 8 && smem <= 227 * 1024) {
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(tk),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return set_cuda_error(e);
+            long long blocks = (N + RB - 1) / RB;
+            if (blocks > sms) blocks = sms;
+            tk<<<(unsigned)blocks, kTKThreads, smem, stream>>>(dev_r, codes, N, k, L, out, ldk, RB);
+            e = cudaGetLastError();
+            return e == cudaSuccess ? FASTLSH_OK : set_cuda_error(e);
+        }
+    }
     if (FastKeysFn fk = fast_keys_for(K, vec)) {  // K <= 16: register-resident limbs (above)
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);

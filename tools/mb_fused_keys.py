@@ -17,7 +17,7 @@ def timed(fn, iters=5):
     return e0.elapsed_time(e1) / iters
 
 
-for name, rows in (("C1", 1_000_000), ("C3", 8_388_608)):
+for name, rows in (("C1", 1_000_000), ("C3", 8_388_608), ("C4", 100_000)):
     c = configs.get(name)
     P = fl.Params.create(c.n, c.m, c.k, c.w, seed=c.seed)
     K = fl.Keys.create(c.L, c.K, seed=c.seed)
@@ -25,7 +25,10 @@ for name, rows in (("C1", 1_000_000), ("C3", 8_388_608)):
     codes = torch.empty((rows, c.k), dtype=torch.int32, device="cuda")
     keys = torch.empty((c.L, rows), dtype=torch.int64, device="cuda")
     t_f = timed(lambda: fl.hash_keys(P, K, X, codes=codes, keys_out=keys))
-    t_fk = timed(lambda: fl.hash_keys(P, K, X, keys_out=keys, with_codes=False))
+    try:
+        t_fk = timed(lambda: fl.hash_keys(P, K, X, keys_out=keys, with_codes=False))
+    except fl.FastLSHError:
+        t_fk = float("nan")  # keys-only needs a fused path (one CTA block, or K1 with table size)
     t_h = timed(lambda: fl.fastlsh_hash(P, X, out=codes))
     t_k = timed(lambda: fl.build_keys(K, codes, out=keys))
     print(f"{name} rows={rows}: fused {t_f:.3f} ms, fused keys-only {t_fk:.3f}, hash {t_h:.3f} + keys {t_k:.3f} = {t_h + t_k:.3f} ms")
