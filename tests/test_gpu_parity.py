@@ -221,11 +221,15 @@ def test_host_entry_point_matches_device_path(fused):
 
 # ---- compound keys: bit-exact vs Python big integers, on seeded code matrices ------------------------
 
-@pytest.mark.parametrize("L,K,N,ldk_pad", [(50, 10, 1000, 0), (16, 16, 333, 5), (200, 10, 257, 0), (1, 1, 7, 0)])
-def test_keys_bit_exact(L, K, N, ldk_pad):
+@pytest.mark.parametrize("L,K,N,ldk_pad,extra", [(50, 10, 1000, 0, 3), (16, 16, 333, 5, 3), (200, 10, 257, 0, 3),
+                                                  (1, 1, 7, 0, 3), (50, 10, 1001, 0, 0), (12, 16, 777, 2, 4),
+                                                  (600, 2, 1001, 0, 0)])
+def test_keys_bit_exact(L, K, N, ldk_pad, extra):
+    """k = L*K + extra code columns: k % 4 == 0 and rows not bank-aligned take the TMA-staged K3t
+    (50x10 at k = 500, 12x16 at k = 196), others the register-batched K3 (L > 512, k % 4 != 0)."""
     r = philox.key_multipliers(L, K, seed=3)
     Kobj = fl.Keys.from_arrays(r)
-    codes = data.random_codes(N, L * K + 3, seed=L + K, lo=-(2 ** 31), hi=2 ** 31 - 1)
+    codes = data.random_codes(N, L * K + extra, seed=L + K, lo=-(2 ** 31), hi=2 ** 31 - 1)
     keys_gpu = fl.build_keys(Kobj, codes.cuda(), ldk=N + ldk_pad)[:, :N].cpu().numpy().view(np.uint64)
     ref = okeys.build_keys(codes.numpy(), r, L, K)
     assert np.array_equal(keys_gpu, ref)
