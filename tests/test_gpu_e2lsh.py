@@ -60,3 +60,23 @@ def test_plain_tf32_is_less_accurate_than_3xtf32():
     e1 = np.abs(fl.e2lsh_project(P, X, precision=1).cpu().numpy() - p) / s
     assert e3.max() < 1e-5
     assert e1.max() > 10 * e3.max()
+
+
+def test_plain_tf32_violation_rate_c1_shape():
+    """the ungated 1xTF32 comparator is reported with its violation rate — the
+    fraction of projections outside the north-star band 1e-5 * |a| |S(v)| and of codes that differ
+    from the oracle outside the ambiguity band. 3xTF32 has none; 1xTF32 has many."""
+    c = configs.get("C1")
+    idx, A, b = e2lsh_arrays(c.n, c.k, c.w, seed=c.seed)
+    P = fl.Params.from_arrays(c.n, c.w, idx, A, b)
+    X = data.generate(c.data, c.n, 0, 2000, seed=1, device="cuda")
+    p, s, code = oracle.e2lsh(X.cpu().numpy(), A, b, c.w, threads=THREADS)
+    rates = {}
+    for prec in (3, 1):
+        pr = fl.e2lsh_project(P, X, precision=prec).cpu().numpy()
+        cg = fl.e2lsh_hash(P, X, precision=prec).cpu().numpy()
+        rates[prec] = (float((np.abs(pr - p) > 1e-5 * s).mean()), float((cg != code).mean()))
+    print(f"\n1xTF32 violation rate (C1 shape, 2000 rows x {c.k}): projections {rates[1][0]:.3e}, "
+          f"codes {rates[1][1]:.3e}; 3xTF32: {rates[3][0]:.1e}, {rates[3][1]:.1e}")
+    assert rates[3][0] == 0.0
+    assert rates[1][0] > 0.01
