@@ -86,17 +86,29 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     a.debug = 0;
     if (const char* e = std::getenv("FASTLSH_K1R_DEBUG")) a.debug = std::atoi(e);  // experiment knob
 
-    cudaError_t e =
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
-    if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+    // resident CTAs per device: queried once per (params, device, shared-memory size) — at C0's
+    // 10^4 rows the attribute + occupancy queries per call cost as much as the kernel
+    const int slot = fk ? 1 : 0;
+    int resident = d.r_resident[slot];
+    cudaError_t e;
+    if (resident <= 0 || d.r_resident_smem[slot] != smem) {
+        // the device maximum, never lowered: another params object sharing this kernel may launch
+        // it with more shared memory than this one
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemMax);
+        if (e != cudaSuccess) return set_cuda_error(e);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, smem);
+        if (e != cudaSuccess) return set_cuda_error(e);
+        if (per_sm < 1) return FASTLSH_EUNSUPPORTED;
+        resident = sms * per_sm;
+        d.r_resident[slot] = resident;
+        d.r_resident_smem[slot] = smem;
+    }
     // persistent grid: as many row streams per hash block as fit resident at once
-    long long gpr = (long long)sms * per_sm / pk.hash_blocks;
+    long long gpr = (long long)resident / pk.hash_blocks;
     if (gpr > a.groups) gpr = a.groups;
     if (gpr < 1) gpr = 1;
     const long long grid = gpr * pk.hash_blocks;

@@ -114,6 +114,8 @@ struct DeviceCopy {
     uint32_t* r_offp = nullptr;           // K1r packing (RPacking), when applicable
     float* r_coef = nullptr;
     int16_t* r_lane_hash = nullptr;
+    mutable int r_resident[2] = {0, 0};          // K1r resident CTAs per device [plain, keys], cached
+    mutable size_t r_resident_smem[2] = {0, 0};  // ... for this dynamic shared-memory size
     int32_t* r_block_h0 = nullptr;
     int32_t* r_block_kb = nullptr;
     uint32_t* offp = nullptr;
