@@ -58,7 +58,8 @@ typedef struct {
     int64_t conflict_wavefronts; /* extra smem wavefronts per row left by the scheduler          */
     int32_t kernel;            /* hashing kernel for 16-B aligned X: 1 = shared-memory gather K1,
                                   2 = tensor-memory gather K1t,
-                                  3 = row-major gather K1r                     */
+                                  3 = row-major gather K1r,
+                                  4 = params-specialised lane = row kernel K1j */
     int32_t tmem_hash_blocks;  /* K1t: CTAs hash blocks (0 when K1t does not apply)              */
     int32_t tmem_hashes_per_warp; /* K1t: hashes (register accumulator pairs) per warp           */
 } fastlsh_params_info_t;
@@ -132,14 +133,34 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
  *       beats K1's, for calls with n % 4 == 0 and X 16-byte aligned; else the shared-memory K1;
  *   1 = always the shared-memory gather K1 (column-interleaved stages, LDS.128);
  *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED);
- *   3 = always K1r (row-major stages, LDS.32; likewise EUNSUPPORTED when it cannot serve).
- * EINVAL for other values; EUNSUPPORTED for 2 or 3 when that kernel cannot serve the params. */
+ *   3 = always K1r (row-major stages, LDS.32; likewise EUNSUPPORTED when it cannot serve);
+ *   4 = always K1j, the params-specialised kernel: the library generates
+ *       CUDA source in which S_i are register operands of a row held in registers (lane = row)
+ *       and a_i, b_i, 1/w instruction immediates, compiles it with NVRTC for sm_100a on first
+ *       use and caches the module (per process, keyed by the generated source). Applies when
+ *       n <= 128, n % 4 == 0, k % 4 == 0, k*m <= 16384 and libnvrtc can be loaded; calls need X
+ *       and codes/proj 16-byte aligned. In automatic mode K1j is preferred wherever it applies
+ *       (set FASTLSH_NO_JIT=1 to disable it).
+ * EINVAL for other values; EUNSUPPORTED for 2, 3 or 4 when that kernel cannot serve the params. */
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
+
+/* K1j only: compile ahead of time the variants a later call will use, so that the first
+ * fastlsh_hash / fastlsh_project / fastlsh_hash_keys call does not pay the NVRTC compile
+ * (seconds). what: bit 0 codes, bit 1 projections, bit 2 codes + keys of `keys` (its L and K;
+ * the multipliers are kernel arguments, not compiled in). FASTLSH_OK and nothing done when the
+ * params do not use K1j. EUNSUPPORTED when NVRTC fails (see fastlsh_params_jit_status). */
+fastlsh_status fastlsh_params_prepare(const fastlsh_params* p, const fastlsh_keys* keys, int32_t what);
+
+/* K1j diagnostics: total NVRTC compile time spent for these params and the last compile / load
+ * error (empty when none); msg receives at most msg_len-1 bytes plus a NUL. */
+fastlsh_status fastlsh_params_jit_status(const fastlsh_params* p, double* compile_seconds, char* msg,
+                                         int64_t msg_len);
 
 /* codes[r*k + i] = floor((a_i . S_i(X[r]) + b_i) / w) as int32, for r < N, i < k — Eq. 5.
  * fp32 accumulation (K1r: each lane sums <= 128 products in its bank-scheduled slot order, the
  * P <= 32 parts of a hash then by an xor butterfly; K1: chunks of <= 64 products; K1t: slots
- * grouped by 128-coordinate block, one accumulator over <= 128 products), then
+ * grouped by 128-coordinate block, one accumulator over <= 128 products; K1j: the m products in the
+ * paper's slot order, one accumulator), then
  * __fadd_rn(p, b), __fdiv_rn(., w), floor toward -inf. Non-finite or out-of-int32 quotients
  * write INT32_MIN and count in the params' flags. Requires fastlsh_params_upload. */
 fastlsh_status fastlsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,

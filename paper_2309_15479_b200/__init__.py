@@ -21,6 +21,7 @@ EXPORTED = [
     "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
     "fastlsh_params_row_packing",
     "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
+    "fastlsh_params_prepare", "fastlsh_params_jit_status",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables",
@@ -72,6 +73,8 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_params_upload": [P, i32, P],
         "fastlsh_params_set_kernel": [P, i32],
         "fastlsh_params_set_table_size": [P, i32],
+        "fastlsh_params_prepare": [P, P, i32],
+        "fastlsh_params_jit_status": [P, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, i64],
         "fastlsh_params_packing": [P, P, P, P, P, P, P],
         "fastlsh_params_row_packing": [P, P, P, P, P, P, P],
         "fastlsh_hash": [P, P, i64, P, P],
@@ -125,6 +128,16 @@ def _dev_ptr(t, dtype, what: str):
     if t.dtype != dtype or not t.is_contiguous():
         raise TypeError(f"{what} must be a contiguous {dtype} tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _check_X(params, X, what: str = "X"):
+    if X.ndim != 2 or X.shape[1] != params.n:
+        raise ValueError(f"{what} must be [N, n={params.n}], got {tuple(X.shape)}")
+
+
+def _check_out(out, rows: int, cols: int, what: str):
+    if out.ndim != 2 or tuple(out.shape) != (rows, cols):
+        raise ValueError(f"{what} must be [{rows}, {cols}], got {tuple(out.shape)}")
 
 
 def _stream_ptr(stream):
@@ -219,12 +232,30 @@ class Params:
                     offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
                     lane_hash=lh.reshape(HB, W, 32), block_h0=h0, block_kb=kb)
 
+    KERNELS = {1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}
+
     def set_kernel(self, kernel):
-        """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t) or "rows" (3, K1r);
-        see fastlsh_params_set_kernel. Returns self."""
-        code = {"auto": 0, "smem": 1, "tmem": 2, "rows": 3}.get(kernel, kernel)
+        """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t), "rows" (3, K1r) or
+        "jit" (4, K1j); see fastlsh_params_set_kernel. Returns self."""
+        code = {"auto": 0, "smem": 1, "tmem": 2, "rows": 3, "jit": 4}.get(kernel, kernel)
         _check(self._lib.fastlsh_params_set_kernel(self._h, int(code)), "fastlsh_params_set_kernel")
         return self
+
+    def prepare(self, keys=None, codes: bool = True, proj: bool = False):
+        """K1j: compile the kernel variants later calls will use (fastlsh_params_prepare), so the
+        first hash call does not pay the NVRTC compile. No-op for params served by K1r / K1."""
+        what = (1 if codes else 0) | (2 if proj else 0) | (4 if keys is not None else 0)
+        _check(self._lib.fastlsh_params_prepare(self._h, keys._h if keys is not None else None, what),
+               "fastlsh_params_prepare")
+        return self
+
+    def jit_status(self) -> dict:
+        """K1j diagnostics: NVRTC seconds spent so far and the last compile/load error."""
+        sec = ctypes.c_double()
+        buf = ctypes.create_string_buffer(4096)
+        _check(self._lib.fastlsh_params_jit_status(self._h, ctypes.byref(sec), buf, len(buf)),
+               "fastlsh_params_jit_status")
+        return {"compile_seconds": sec.value, "error": buf.value.decode(errors="replace")}
 
     def set_table_size(self, K: int):
         """Pack hash blocks as whole tables of K hashes so keys are built inside the hashing kernel
@@ -305,9 +336,11 @@ def fastlsh_hash(params: Params, X, out=None, stream=None):
     """codes[N,k] int32 = floor((a_i . S_i(x) + b_i) / w) (Eq. 5) for X f32 [N,n] on the GPU."""
     import torch
     params._ready()
+    _check_X(params, X)
     N = X.shape[0]
     if out is None:
         out = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    _check_out(out, N, params.k, "codes")
     _check(params._lib.fastlsh_hash(params._h, _dev_ptr(X, torch.float32, "X"), N,
                                     _dev_ptr(out, torch.int32, "codes"), _stream_ptr(stream)), "fastlsh_hash")
     return out
@@ -317,9 +350,11 @@ def fastlsh_project(params: Params, X, out=None, stream=None):
     """proj[N,k] f32 = a_i . S_i(x) — the projection before +b, /w, floor."""
     import torch
     params._ready()
+    _check_X(params, X)
     N = X.shape[0]
     if out is None:
         out = torch.empty((N, params.k), dtype=torch.float32, device=X.device)
+    _check_out(out, N, params.k, "proj")
     _check(params._lib.fastlsh_project(params._h, _dev_ptr(X, torch.float32, "X"), N,
                                        _dev_ptr(out, torch.float32, "proj"), _stream_ptr(stream)), "fastlsh_project")
     return out
@@ -329,9 +364,11 @@ def e2lsh_hash(params: Params, X, out=None, precision: int = 3, stream=None):
     """Dense baseline codes on tcgen05 (3xTF32 by default)."""
     import torch
     params._ready()
+    _check_X(params, X)
     N = X.shape[0]
     if out is None:
         out = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    _check_out(out, N, params.k, "codes")
     _check(params._lib.e2lsh_hash(params._h, _dev_ptr(X, torch.float32, "X"), N,
                                   _dev_ptr(out, torch.int32, "codes"), precision, _stream_ptr(stream)), "e2lsh_hash")
     return out
@@ -340,9 +377,11 @@ def e2lsh_hash(params: Params, X, out=None, precision: int = 3, stream=None):
 def e2lsh_project(params: Params, X, out=None, precision: int = 3, stream=None):
     import torch
     params._ready()
+    _check_X(params, X)
     N = X.shape[0]
     if out is None:
         out = torch.empty((N, params.k), dtype=torch.float32, device=X.device)
+    _check_out(out, N, params.k, "proj")
     _check(params._lib.e2lsh_project(params._h, _dev_ptr(X, torch.float32, "X"), N,
                                      _dev_ptr(out, torch.float32, "proj"), precision, _stream_ptr(stream)),
            "e2lsh_project")
@@ -355,7 +394,11 @@ def build_keys(keys: Keys, codes, out=None, ldk=None, stream=None, col0: int = 0
     With `out` an [L, ldk] tensor and `col0` > 0, the N keys of each table go to columns
     [col0, col0 + N) (chunked table builds)."""
     import torch
+    if codes.ndim != 2:
+        raise ValueError(f"codes must be [N, k], got {tuple(codes.shape)}")
     N, k = codes.shape
+    if keys.L * keys.K > k:
+        raise ValueError(f"codes has k={k} < L*K={keys.L * keys.K}")
     if out is None:
         ldk = (N + col0) if ldk is None else ldk
         out = torch.empty((keys.L, ldk), dtype=torch.int64, device=codes.device)
@@ -405,6 +448,12 @@ def query(X, tables, Q, qkeys, topk: int = 10, workspace=None, stream=None):
     N, n = X.shape
     nq = Q.shape[0]
     L, ldq = qkeys.shape
+    if Q.ndim != 2 or Q.shape[1] != n:
+        raise ValueError(f"Q must be [nq, n={n}], got {tuple(Q.shape)}")
+    if sk.shape[0] != L or ids.shape[0] != L or sk.shape[1] != N or ids.shape[1] != N:
+        raise ValueError(f"tables must be [L={L}, N={N}] (the L of qkeys and the rows of X)")
+    if ldq < nq:
+        raise ValueError(f"qkeys must have >= nq={nq} columns")
     dev = Q.device
     out_i = torch.empty((nq, topk), dtype=torch.int32, device=dev)
     out_d = torch.empty((nq, topk), dtype=torch.float32, device=dev)
@@ -467,9 +516,14 @@ def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, s
     N keys of each table written to columns [col0, col0 + N)."""
     import torch
     params._ready()
+    _check_X(params, X)
     N = X.shape[0]
     if with_codes and codes is None:
         codes = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    if codes is not None:
+        _check_out(codes, N, params.k, "codes")
+    if keys is not None and keys.L * keys.K > params.k:
+        raise ValueError(f"keys need L*K={keys.L * keys.K} <= k={params.k} codes")
     kp = ctypes.c_void_p(0)
     ldk = N
     if keys is not None:
@@ -493,13 +547,24 @@ def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_h
     params._ready()
     if isinstance(X_host, np.ndarray):
         X_host = torch.from_numpy(np.ascontiguousarray(X_host, dtype=np.float32))
+    if X_host.is_cuda or X_host.dtype != torch.float32 or not X_host.is_contiguous():
+        raise TypeError("X_host must be a contiguous float32 host tensor")
+    _check_X(params, X_host, "X_host")
     N = X_host.shape[0]
     if codes_host is None:
         codes_host = torch.empty((N, params.k), dtype=torch.int32, pin_memory=X_host.is_pinned())
+    if codes_host.is_cuda or codes_host.dtype != torch.int32 or not codes_host.is_contiguous():
+        raise TypeError("codes_host must be a contiguous int32 host tensor")
+    _check_out(codes_host, N, params.k, "codes_host")
     kp = ctypes.c_void_p(0)
     if keys is not None:
+        if keys.L * keys.K > params.k:
+            raise ValueError(f"keys need L*K={keys.L * keys.K} <= k={params.k} codes")
         if keys_host is None:
             keys_host = torch.empty((keys.L, N), dtype=torch.int64, pin_memory=X_host.is_pinned())
+        if keys_host.is_cuda or keys_host.dtype != torch.int64 or not keys_host.is_contiguous():
+            raise TypeError("keys_host must be a contiguous int64 host tensor")
+        _check_out(keys_host, keys.L, N, "keys_host")
         kp = ctypes.c_void_p(keys_host.data_ptr())
     _check(params._lib.fastlsh_hash_host(params._h, keys._h if keys is not None else None,
                                          ctypes.c_void_p(X_host.data_ptr()), N,

@@ -106,6 +106,7 @@ void free_device_copy(DeviceCopy& d) {
     cudaFree(d.dense_hi); cudaFree(d.dense_lo);
     cudaFree(d.t_recs); cudaFree(d.t_counts); cudaFree(d.t_offs); cudaFree(d.t_hinfo); cudaFree(d.t_groups);
     cudaFree(d.r_offp); cudaFree(d.r_coef); cudaFree(d.r_lane_hash); cudaFree(d.r_block_h0); cudaFree(d.r_block_kb);
+    cudaFree(d.j_idx); cudaFree(d.j_a);
     for (int i = 0; i < 2; ++i) {
         cudaFree(d.ws_x[i]); cudaFree(d.ws_codes[i]); cudaFree(d.ws_keys[i]);
         if (d.ws_stream[i]) cudaStreamDestroy(d.ws_stream[i]);
@@ -139,8 +140,18 @@ bool rows_keys_pay(const fastlsh_params* p, const fastlsh_keys* ks) {
     const RPacking& r = p->rpack;
     return (double)ks->L * ks->K <= 0.75 * (double)r.hash_blocks * r.warps * r.slots;
 }
+// K1j (params-specialised lane = row kernel, jit.cpp) serves the call when pinned (kernel 4) or, in
+// auto mode, whenever it applies (n <= 128: the gathers become register operands, no shared-memory
+// bound). Calls it cannot serve (alignment, compile failure) fall through unless pinned.
+bool jit_selected(const fastlsh_params* p) {
+    return p->kernel == 4 || (p->kernel == 0 && jit::applicable(*p));
+}
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
+    if (jit_selected(p)) {
+        fastlsh_status st = jit::launch(p, d, X, N, codes, proj, nullptr, nullptr, nullptr, 0, stream);
+        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 4) return st;
+    }
     if (tmem_selected(p)) {
         fastlsh_status st = launch_gather_tmem(p, d, X, N, codes, proj, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 2) return st;
@@ -267,7 +278,7 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
-    info->kernel = tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
+    info->kernel = jit_selected(p) ? 4 : tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
     info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
     info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
@@ -371,6 +382,11 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
         free_device_copy(d);
         return st;
     }
+    if (jit::applicable(*p) && ((st = upload_vec(&d.j_idx, p->idx, s)) != FASTLSH_OK ||
+                                (st = upload_vec(&d.j_a, p->a, s)) != FASTLSH_OK)) {
+        free_device_copy(d);
+        return st;
+    }
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d.flags), 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(d.flags, 0, 2 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors may be reused right away
@@ -384,12 +400,13 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
-    if (!p || kernel < 0 || kernel > 3) return FASTLSH_EINVAL;
+    if (!p || kernel < 0 || kernel > 4) return FASTLSH_EINVAL;
     std::lock_guard<std::mutex> g(p->mu);
     fastlsh_status st = ensure_packed(p);
     if (st != FASTLSH_OK) return st;
     if (kernel == 2 && !p->tpack.ok) return FASTLSH_EUNSUPPORTED;
     if (kernel == 3 && !p->rpack.ok) return FASTLSH_EUNSUPPORTED;
+    if (kernel == 4 && !jit::applicable(*p)) return FASTLSH_EUNSUPPORTED;
     p->kernel = kernel;
     return FASTLSH_OK;
 }
@@ -634,6 +651,14 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
     if (st != FASTLSH_OK) return st;
+    // K1j: codes and keys in one launch, keys accumulated in registers; codes optional
+    if (jit_selected(p)) {
+        const uint64_t* dr = nullptr;
+        st = keys_device(ks, dev, &dr);
+        if (st != FASTLSH_OK) return st;
+        st = jit::launch(p, p->dev[dev], X, N, codes, nullptr, ks, dr, keys_out, ldk, reinterpret_cast<cudaStream_t>(stream));
+        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 4) return st;
+    }
     // K1r (one hash block): keys built from the code tile in shared memory; codes not written
     // when codes == NULL. Falls through when K1r cannot serve the call.
     if (rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
@@ -657,6 +682,28 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     st = fastlsh_hash(p, X, N, codes, stream);
     if (st != FASTLSH_OK) return st;
     return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
+}
+
+fastlsh_status fastlsh_params_prepare(const fastlsh_params* p, const fastlsh_keys* ks, int32_t what) {
+    if (!p || what < 0 || what > 7) return FASTLSH_EINVAL;
+    if (!jit_selected(p)) return FASTLSH_OK;  // nothing to compile: K1r / K1 are built in
+    fastlsh_status st = FASTLSH_OK;
+    if ((what & 1) && (st = jit::prepare(p, 0, nullptr)) != FASTLSH_OK) return st;
+    if ((what & 2) && (st = jit::prepare(p, 1, nullptr)) != FASTLSH_OK) return st;
+    if ((what & 4) && ks && (st = jit::prepare(p, 0, ks)) != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
+    return FASTLSH_OK;
+}
+
+fastlsh_status fastlsh_params_jit_status(const fastlsh_params* p, double* compile_seconds, char* msg, int64_t msg_len) {
+    if (!p) return FASTLSH_EINVAL;
+    std::lock_guard<std::mutex> g(p->jit.mu);
+    if (compile_seconds) *compile_seconds = p->jit.compile_seconds;
+    if (msg && msg_len > 0) {
+        const size_t n = p->jit.last_error.size() < (size_t)msg_len - 1 ? p->jit.last_error.size() : (size_t)msg_len - 1;
+        std::memcpy(msg, p->jit.last_error.data(), n);
+        msg[n] = 0;
+    }
+    return FASTLSH_OK;
 }
 
 fastlsh_status fastlsh_read_flags(const fastlsh_params* p, uint64_t* nonfinite,
@@ -723,7 +770,12 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
         bool fused_here = false;
-        if (want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
+        if (want_keys && jit_selected(p)) {
+            st = jit::launch(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, ks, dr, d.ws_keys[b], rows, s);
+            fused_here = st == FASTLSH_OK;
+            if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
+        }
+        if (!fused_here && want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
             rows_keys_pay(p, ks)) {
             FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
             st = launch_gather_rows(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);

@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -109,8 +111,22 @@ struct RPacking {
 // true when K1r can hash rows of this params object (packing exists) — X alignment is per call
 void build_row_packing(const fastlsh_params& p, RPacking& out);
 
+namespace jit {
+struct Module;  // a compiled K1j variant (jit.cpp)
+// K1j variants of one params object: (mode, L, K) -> module; compiled on first use
+struct State {
+    std::mutex mu;
+    int applicable = -1;  // -1 not decided yet
+    std::vector<std::pair<std::array<int, 3>, std::shared_ptr<Module>>> variants;
+    std::string last_error;
+    double compile_seconds = 0;  // total NVRTC time spent for this params object
+};
+}  // namespace jit
+
 struct DeviceCopy {
     bool ready = false;
+    int32_t* j_idx = nullptr;             // K1j slow path: canonical idx / a on the device
+    float* j_a = nullptr;
     uint32_t* r_offp = nullptr;           // K1r packing (RPacking), when applicable
     float* r_coef = nullptr;
     int16_t* r_lane_hash = nullptr;
@@ -158,10 +174,11 @@ struct fastlsh_params {
     fastlsh::TPacking tpack;
     fastlsh::RPacking rpack;
     bool packed = false;
-    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 K1, 2 TMEM K1t, 3 row-major K1r
+    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 K1, 2 TMEM K1t, 3 row-major K1r, 4 K1j
     int32_t table_align = 1;   // hash blocks hold whole tables of this many hashes (fused keys)
     fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
     std::mutex mu;
+    mutable fastlsh::jit::State jit;
 };
 
 struct fastlsh_keys {
@@ -229,5 +246,32 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);
 
 fastlsh_status set_cuda_error(cudaError_t e);
+
+// jit.cpp — K1j, the params-specialised lane = row kernel
+namespace jit {
+struct Spec {
+    int n, m, k;
+    float w;
+    const int32_t* idx;  // canonical [k][m]
+    const float* a;      // [k][m]
+    const float* b;      // [k]
+    int L, K;            // fused compound keys (L = 0: none)
+    int warps, ncb;      // warps per CTA, code boxes per warp
+    int mode;            // 0: codes (+ keys when L > 0), 1: projections
+};
+std::string k1j_source(const Spec& s);
+bool nvrtc_available();
+bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, double* seconds);
+// K1j can serve this params object (shape limits, NVRTC present, not disabled by FASTLSH_NO_JIT)
+bool applicable(const fastlsh_params& p);
+// Hash (codes, or proj when proj != NULL) and optionally build compound keys in one launch.
+// Returns FASTLSH_EUNSUPPORTED when K1j cannot serve this call (alignment, sizes, compile
+// failure): the caller then uses K1r / K1.
+fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
+                      float* proj, const fastlsh_keys* ks, const uint64_t* dev_r, uint64_t* keys, int64_t ldk,
+                      cudaStream_t stream);
+// compile (if needed) the variant a call with these arguments would use
+fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks);
+}  // namespace jit
 
 }  // namespace fastlsh

@@ -1,0 +1,733 @@
+// jit.cpp — K1j: the params-specialised, lane = row hashing kernel, generated at params upload
+// and compiled with NVRTC.
+//
+// For every row v and hash i: h_i(v) = floor((a_i . S_i(v) + b_i) / w)   (Eq. 5).
+//
+// Why: K1r/K1 read every sampled coordinate from shared memory (one 128-B wavefront per 32
+// gathers), which bounds them at G_s = 9.3e12 gathers/s. For short rows (n <= 128: C0, C3) a whole
+// row fits in a thread's registers, and once the params are fixed the sampled index set S_i is a
+// compile-time constant: x[idx[i][j]] becomes a register operand and a[i][j], b[i] become
+// instruction immediates. The gather then costs no shared-memory wavefront at all — one FFMA per
+// sampled coordinate (O(m) per hash) — and the kernel is bound by instruction issue
+// or by HBM (reading X, writing codes and keys), not by the shared-memory pipe.
+//
+// Kernel (one generated module per params object; one warp = 32 rows, lane = row):
+//  * stage: TMA 2D tensor loads of the warp's 32-row tile of X as boxes of 32 rows x 32 floats
+//    with the 128-byte swizzle (one box per 32 coordinates), complete_tx on a per-warp mbarrier;
+//    lane t reads its row with LDS.128 at chunk (c ^ (t & 7)) — conflict-free quarter-warps. The
+//    next tile's copy is issued as soon as the row is in registers (one stage per warp suffices:
+//    a tile's compute is thousands of cycles).
+//  * sample + project: per hash, p = x[i0]*a0 then fma(x[ij], aj, p) in the paper's slot order,
+//    all straight-line code with immediate coefficients (fp32; parity bound as K1r's, m <= 128
+//    terms: m * 2^-24 * ||a|| ||S(v)||).
+//  * quantise: __fadd_rn(p, b), then * (1/w) (w a power of two: exact) or IEEE / w, F2I.FLOOR.
+//    Out-of-range / non-finite quotients are detected by a per-lane flag; a warp with a flagged
+//    row re-runs those rows in a generic slow path (canonical params from global memory, the same
+//    operation sequence, so bit-identical values) which writes INT32_MIN and counts the flags.
+//  * codes: every 32 hashes, a lane writes its 32 codes into a swizzled shared-memory box and one
+//    lane issues a TMA tensor store (bulk_group, ring of NCB boxes); rows past N and hashes past k
+//    are clipped by the tensor map.
+//  * compound keys (R9), when a keys object is fused: the codes of table l
+//    (hashes [lK, lK+K)) are accumulated as they are produced — three IMAD.WIDE.U32 with 21-bit
+//    limbs of r[l][j+1] (kernel-parameter operands) — and key_l(v) = (r_{l,0} + S0 + S1*2^21 +
+//    S2*2^42) mod 2^61-1 is stored as one coalesced 256-byte run per warp and table. Codes may
+//    then stay on chip (keys only: X in, keys out).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace fastlsh {
+namespace jit {
+
+// ------------------------------------------------------------------------------------------
+// source generation
+// ------------------------------------------------------------------------------------------
+
+namespace {
+
+void add_float(std::string& s, float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "__uint_as_float(0x%08xu)", u);
+    s += buf;
+}
+
+void add_int(std::string& s, long long v) { s += std::to_string(v); }
+
+bool pow2_w(float w) {
+    uint32_t u;
+    std::memcpy(&u, &w, 4);
+    const float inv = 1.0f / w;
+    return (u & 0x007fffffu) == 0 && std::isfinite(inv) && inv != 0.0f;
+}
+
+const char* kPrelude = R"FL(
+typedef unsigned long long u64;
+typedef unsigned int u32;
+struct __align__(64) TMap { u64 v[16]; };
+struct JArgs {
+    long long N, tiles;
+    int write_out;          // 0: keys only, the codes never leave the SM
+    int* out;               // codes / projections [N][k] (slow path only; the fast path uses omap)
+    u64* keys;              // [L][ldk]
+    long long ldk, col0;
+    u64* flags;             // [0] non-finite, [1] saturated
+    const int* idx;         // canonical params [k][m], [k][m], [k] (slow path)
+    const float* a;
+    const float* b;
+    const u64* kr;          // key multipliers [L][K+1] (slow path)
+};
+#define P61 ((1ull << 61) - 1ull)
+__device__ __forceinline__ u64 mod61(u64 x) { x = (x & P61) + (x >> 61); return x >= P61 ? x - P61 : x; }
+__device__ __forceinline__ u64 rotl61(u64 x, int j) { return ((x << j) & P61) | (x >> (61 - j)); }
+__device__ __forceinline__ u32 su32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u32 bar, u32 c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u32 bar, u32 ph) {
+    asm volatile("{\n\t.reg .pred p;\nFLW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra FLW_%=;\n}"
+                 ::"r"(bar), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma_load(u32 dst, const TMap* m, int x, int y, u32 bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"((u64)m), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_store(const TMap* m, u32 src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"((u64)m), "r"(src), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_ring() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(FL_NCB - 1) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one group of 32 outputs of the warp's tile -> swizzled box -> TMA tensor store
+__device__ __forceinline__ void store_group(const int (&cv)[32], unsigned char* cring, u32 cring_s, int& cbi, int lane,
+                                            u32 sw, const TMap* om, int g, long long t) {
+    if (lane == 0) bulk_wait_read_ring();  // the store that last read box cbi has read it
+    __syncwarp();
+    unsigned char* dst = cring + cbi * 4096 + lane * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<int4*>(dst + (((u32)q << 4) ^ sw)) = make_int4(cv[4 * q], cv[4 * q + 1], cv[4 * q + 2], cv[4 * q + 3]);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store(om, cring_s + cbi * 4096, 32 * g, (int)(32 * t));
+        bulk_commit();
+    }
+    cbi = cbi + 1 == FL_NCB ? 0 : cbi + 1;
+}
+
+// Generic path for a row with a flagged hash (non-finite or out-of-int32 quotient): the same
+// operation sequence as the generated code (so bit-identical values), INT32_MIN + flag counts,
+// codes rewritten in global memory, keys recomputed from the corrected codes.
+__device__ __noinline__ void fix_row(const JArgs& a, float* scr, long long row, int lane) {
+    int* sc = reinterpret_cast<int*>(scr + FL_N);
+    for (int i = lane; i < FL_K; i += 32) {
+        const int* id = a.idx + (long long)i * FL_M;
+        const float* co = a.a + (long long)i * FL_M;
+        float p = __fmul_rn(scr[id[0]], co[0]);
+        for (int j = 1; j < FL_M; ++j) p = __fmaf_rn(scr[id[j]], co[j], p);
+        const float q = FL_QUANT(__fadd_rn(p, a.b[i]));
+        int c = __float2int_rd(q);
+        if (!(fabsf(q) < 2147483648.0f)) {
+            c = (int)0x80000000;
+            if (row < a.N) atomicAdd(a.flags + (isfinite(q) ? 1 : 0), 1ull);
+        }
+        sc[i] = c;
+        if (a.write_out && row < a.N) a.out[row * FL_K + i] = c;
+    }
+    __syncwarp();
+#if FL_L > 0
+    for (int l = lane; l < FL_L; l += 32) {
+        // the limb form of the generated code (exact for K <= 1024): S_q = sum limb_q(r) * u32(c)
+        const u64* rl = a.kr + l * (FL_KT + 1);
+        u64 s0 = 0, s1 = 0, s2 = 0;
+        for (int j = 0; j < FL_KT; ++j) {
+            const u64 rv = rl[j + 1];
+            const u64 u = (u32)sc[l * FL_KT + j];
+            s0 += (rv & 0x1fffffull) * u;
+            s1 += ((rv >> 21) & 0x1fffffull) * u;
+            s2 += (rv >> 42) * u;
+        }
+        const u64 key = mod61(rl[0] + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
+        if (row < a.N && !(FL_DEBUG & 1)) a.keys[l * a.ldk + a.col0 + row] = key;
+    }
+#endif
+}
+)FL";
+
+// the per-tile prologue shared by both kernels: wait for the tile, load the lane's row into x[]
+const char* kTileHead = R"FL(
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const u32 raw_s = su32(sm_raw);
+    unsigned char* sm = sm_raw + (((raw_s + 1023u) & ~1023u) - raw_s);
+    unsigned char* wb = sm + warp * FL_WB;
+    unsigned char* cring = wb + FL_NBX * 4096;
+    const u32 xs = su32(wb), cring_s = xs + FL_NBX * 4096;
+    const u32 bar = su32(sm + FL_NW * FL_WB) + 8u * warp;
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    long long t = (long long)blockIdx.x * FL_NW + warp;
+    const long long tstride = (long long)gridDim.x * FL_NW;
+    if (lane == 0 && t < a.tiles) {
+        mbar_expect(bar, FL_NBX * 4096);
+#pragma unroll
+        for (int bx = 0; bx < FL_NBX; ++bx) tma_load(xs + bx * 4096, &xmap, 32 * bx, (int)(32 * t), bar);
+    }
+    u32 ph = 0;
+    int cbi = 0;
+    const u32 sw = (u32)(lane & 7) << 4;
+    for (; t < a.tiles; t += tstride) {
+        mbar_wait(bar, ph);
+        ph ^= 1u;
+        float x[FL_NX];
+#pragma unroll
+        for (int c = 0; c < FL_NX / 4; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(wb + (c >> 3) * 4096 + lane * 128 + ((((u32)c & 7u) << 4) ^ sw));
+            x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        }
+        __syncwarp();  // every lane's row is in registers: the stage may be refilled
+        if (lane == 0 && t + tstride < a.tiles) {
+            mbar_expect(bar, FL_NBX * 4096);
+#pragma unroll
+            for (int bx = 0; bx < FL_NBX; ++bx) tma_load(xs + bx * 4096, &xmap, 32 * bx, (int)(32 * (t + tstride)), bar);
+        }
+        const long long row = t * 32 + lane;
+        (void)row;
+)FL";
+
+}  // namespace
+
+std::string k1j_source(const Spec& s) {
+    const int nbx = (s.n + 31) / 32;
+    const int nx = (s.n + 3) / 4 * 4;
+    const int wb = (nbx + s.ncb) * 4096;
+    const int groups = (s.k + 31) / 32;
+    const bool p2 = pow2_w(s.w);
+    std::string src;
+    src.reserve((size_t)s.k * s.m * 48 + 65536);
+    auto def = [&](const char* name, long long v) {
+        src += "#define ";
+        src += name;
+        src += " ";
+        add_int(src, v);
+        src += "\n";
+    };
+    src += "// K1j generated for n=" + std::to_string(s.n) + " m=" + std::to_string(s.m) + " k=" + std::to_string(s.k) +
+           " (libfastlsh jit.cpp; DESIGN.md \"K1j\")\n";
+    def("FL_N", s.n);
+    def("FL_M", s.m);
+    def("FL_K", s.k);
+    def("FL_NX", nx);
+    def("FL_NBX", nbx);
+    def("FL_NW", s.warps);
+    def("FL_NCB", s.ncb);
+    def("FL_WB", wb);
+    def("FL_L", s.L);
+    def("FL_KT", s.K > 0 ? s.K : 1);
+    {
+        const char* dbg = std::getenv("FASTLSH_JIT_DEBUG");  // experiment knob (tools/dbg_keys*.py)
+        def("FL_DEBUG", dbg ? std::atoi(dbg) : 0);
+    }
+    if (p2) {
+        src += "#define FL_QUANT(v) __fmul_rn((v), ";
+        add_float(src, 1.0f / s.w);
+        src += ")\n";
+    } else {
+        src += "#define FL_QUANT(v) __fdiv_rn((v), ";
+        add_float(src, s.w);
+        src += ")\n";
+    }
+    src += kPrelude;
+    if (s.L > 0) {
+        src += "struct KArgs { u32 limb[" + std::to_string(s.L * s.K * 3) + "]; u64 r0[" + std::to_string(s.L) + "]; };\n";
+    } else {
+        src += "struct KArgs { u32 unused; };\n";
+    }
+
+    // One hash as one inline-PTX block: p in the paper's slot order with immediate coefficients,
+    // then (codes) p + b, * 1/w or / w, floor. NVVM does not re-optimise asm: with plain C++
+    // expressions the front end took ~14 s for the C3 shape, as asm ~2 s.
+    auto hash_asm = [&](int i, int j) {
+        const int32_t* id = s.idx + (size_t)i * s.m;
+        const float* co = s.a + (size_t)i * s.m;
+        const int base = s.mode == 0 ? 2 : 1;  // outputs: code, q (codes) or p (projections)
+        std::vector<int> ops;                  // distinct coordinates -> asm operand numbers
+        std::vector<int> opnum(s.n, -1);
+        for (int t = 0; t < s.m; ++t)
+            if (opnum[id[t]] < 0) {
+                opnum[id[t]] = (int)ops.size() + base;
+                ops.push_back(id[t]);
+            }
+        const char* P = s.mode == 0 ? "%1" : "%0";  // register holding p (q is reused for p)
+        char buf[96];
+        std::string h = s.mode == 0 ? "            { float q; asm(\"" : "            { float p; asm(\"";
+        for (int t = 0; t < s.m; ++t) {
+            uint32_t u;
+            std::memcpy(&u, &co[t], 4);
+            if (t == 0)
+                std::snprintf(buf, sizeof buf, "mul.rn.f32 %s, %%%d, 0f%08X;", P, opnum[id[t]], u);
+            else
+                std::snprintf(buf, sizeof buf, " fma.rn.f32 %s, %%%d, 0f%08X, %s;", P, opnum[id[t]], u, P);
+            h += buf;
+        }
+        if (s.mode == 0) {
+            uint32_t ub, uw;
+            std::memcpy(&ub, &s.b[i], 4);
+            const float wq = p2 ? 1.0f / s.w : s.w;
+            std::memcpy(&uw, &wq, 4);
+            std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; %s.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;",
+                          ub, p2 ? "mul" : "div", uw);
+            h += buf;
+            h += "\" : \"=r\"(cv[" + std::to_string(j) + "]), \"=f\"(q) :";
+        } else {
+            h += "\" : \"=f\"(p) :";
+        }
+        for (size_t o = 0; o < ops.size(); ++o) {
+            h += o ? ", " : " ";
+            h += "\"f\"(x[" + std::to_string(ops[o]) + "])";
+        }
+        h += ");";
+        if (s.mode == 0)
+            h += " bad |= !(fabsf(q) < 2147483648.0f);";
+        else
+            h += " cv[" + std::to_string(j) + "] = __float_as_int(p);";
+        return h;
+    };
+
+    const bool keys = s.mode == 0 && s.L > 0;
+    src += s.mode == 0 ? "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
+                         "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, "
+                         "const __grid_constant__ JArgs a, const __grid_constant__ KArgs ka) {\n"
+                       : "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
+                         "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, "
+                         "const __grid_constant__ JArgs a) {\n";
+    src += kTileHead;
+    if (s.mode == 0) src += "        bool bad = false;\n";
+    if (keys) src += "        u64 s0 = 0, s1 = 0, s2 = 0;\n        const bool live = row < a.N;\n        u64* kp = a.keys + a.col0 + row;\n";
+    for (int g = 0; g < groups; ++g) {
+        src += "        {\n            int cv[32];\n";
+        for (int j = 0; j < 32; ++j) {
+            const int i = 32 * g + j;
+            if (i >= s.k) {
+                src += "            cv[" + std::to_string(j) + "] = 0;\n";
+                continue;
+            }
+            src += hash_asm(i, j);
+            if (keys && i < s.L * s.K) {
+                // key term: three 21-bit limbs of r[l][jj+1] times u32(code), exact 64-bit sums
+                const int l = i / s.K, jj = i % s.K;
+                const int li = (l * s.K + jj) * 3;
+                src += " { const u32 u = (u32)cv[" + std::to_string(j) + "]; s0 += (u64)ka.limb[" + std::to_string(li) +
+                       "] * u; s1 += (u64)ka.limb[" + std::to_string(li + 1) + "] * u; s2 += (u64)ka.limb[" +
+                       std::to_string(li + 2) + "] * u; }";
+                // key = (r0 + S0 + S1*2^21 + S2*2^42) mod 2^61-1; for K < 256 every S_q < K*2^53 < 2^61-1
+                // is already reduced, so only the final sum (< 2^63) needs a reduction
+                if (jj == s.K - 1)
+                    src += "\n            { const u64 key = mod61(ka.r0[" + std::to_string(l) + "] + " +
+                           (s.K < 256 ? "s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
+                                      : "mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42)); ") +
+                           "if (live && !(FL_DEBUG & 2)) kp[" + std::to_string(l) + "ll * a.ldk] = key; s0 = 0; s1 = 0; s2 = 0; }";
+            }
+            src += " }\n";
+        }
+        src += "            if (a.write_out) store_group(cv, cring, cring_s, cbi, lane, sw, &omap, " + std::to_string(g) +
+               ", t);\n        }\n";
+    }
+    if (s.mode == 0) {
+        src += R"FL(
+        if (__any_sync(0xffffffffu, bad)) {
+            unsigned bm = __ballot_sync(0xffffffffu, bad);
+            if (lane == 0) {
+                bulk_wait_all();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            __syncwarp();
+            float* scr = reinterpret_cast<float*>(cring);
+            while (bm) {
+                const int r = __ffs(bm) - 1;
+                bm &= bm - 1;
+#pragma unroll
+                for (int c = 0; c < FL_N; ++c) {
+                    const float v = __shfl_sync(0xffffffffu, x[c], r);
+                    if (lane == 0) scr[c] = v;
+                }
+                __syncwarp();
+                fix_row(a, scr, t * 32 + r, lane);
+                __syncwarp();
+            }
+        }
+)FL";
+    }
+    src += "    }\n    if (lane == 0) bulk_wait_all();\n}\n";
+    return src;
+}
+
+// ------------------------------------------------------------------------------------------
+// NVRTC (loaded at run time: without it K1j is simply unavailable and K1r serves the call)
+// ------------------------------------------------------------------------------------------
+
+namespace {
+
+typedef int (*nvrtcCreateProgram_t)(void**, const char*, const char*, int, const char* const*, const char* const*);
+typedef int (*nvrtcCompileProgram_t)(void*, int, const char* const*);
+typedef int (*nvrtcGetSize_t)(void*, size_t*);
+typedef int (*nvrtcGetBuf_t)(void*, char*);
+typedef int (*nvrtcDestroyProgram_t)(void**);
+
+struct Nvrtc {
+    bool ok = false;
+    nvrtcCreateProgram_t create = nullptr;
+    nvrtcCompileProgram_t compile = nullptr;
+    nvrtcGetSize_t log_size = nullptr, cubin_size = nullptr;
+    nvrtcGetBuf_t log = nullptr, cubin = nullptr;
+    nvrtcDestroyProgram_t destroy = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+    static Nvrtc lib = [] {
+        Nvrtc r;
+        const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                               "/usr/local/cuda/lib64/libnvrtc.so"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
+        if (!h) return r;
+        r.create = (nvrtcCreateProgram_t)dlsym(h, "nvrtcCreateProgram");
+        r.compile = (nvrtcCompileProgram_t)dlsym(h, "nvrtcCompileProgram");
+        r.log_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetProgramLogSize");
+        r.log = (nvrtcGetBuf_t)dlsym(h, "nvrtcGetProgramLog");
+        r.cubin_size = (nvrtcGetSize_t)dlsym(h, "nvrtcGetCUBINSize");
+        r.cubin = (nvrtcGetBuf_t)dlsym(h, "nvrtcGetCUBIN");
+        r.destroy = (nvrtcDestroyProgram_t)dlsym(h, "nvrtcDestroyProgram");
+        r.ok = r.create && r.compile && r.log_size && r.log && r.cubin_size && r.cubin && r.destroy;
+        return r;
+    }();
+    return lib;
+}
+
+}  // namespace
+
+bool nvrtc_available() { return nvrtc().ok; }
+
+bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, double* seconds) {
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) {
+        log = "libnvrtc not found";
+        return false;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    void* prog = nullptr;
+    if (nv.create(&prog, src.c_str(), "k1j.cu", 0, nullptr, nullptr) != 0) {
+        log = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const char* opts[] = {"-arch=sm_100a", "--std=c++17", "-lineinfo", "--device-as-default-execution-space"};
+    const int rc = nv.compile(prog, 4, opts);
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    log.assign(ls, '\0');
+    if (ls) nv.log(prog, &log[0]);
+    bool ok = rc == 0;
+    if (ok) {
+        size_t cs = 0;
+        nv.cubin_size(prog, &cs);
+        cubin.resize(cs);
+        ok = cs > 0 && nv.cubin(prog, cubin.data()) == 0;
+    }
+    nv.destroy(&prog);
+    if (seconds)
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return ok;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// runtime: variants, module cache, tensor maps, launch
+// ------------------------------------------------------------------------------------------
+
+struct Module {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    int warps = 0;
+    size_t smem = 0;
+    bool attr_set[kMaxDevices] = {};
+    std::mutex mu;
+};
+
+namespace {
+
+constexpr int kMaxN = 128;          // a row lives in registers: x[n] plus ~100 working registers
+constexpr int kMaxCode = 16384;     // k*m straight-line FFMAs (16 B each: 256 KB of code)
+constexpr int kNcb = 2;             // code boxes per warp (TMA store ring)
+constexpr size_t kSmemBudget = 220 * 1024;
+
+int warps_for(int n) {
+    const int wb = ((n + 31) / 32 + kNcb) * 4096;
+    int w = (int)(kSmemBudget / (size_t)(wb + 8));
+    return w > 8 ? 8 : w;
+}
+
+size_t smem_bytes(int n, int warps) {
+    return (size_t)warps * ((n + 31) / 32 + kNcb) * 4096 + 8 * (size_t)warps + 1024;
+}
+
+// process-wide cache: identical sources (same params arrays and variant) share one module
+std::mutex g_cache_mu;
+std::vector<std::pair<std::string, std::shared_ptr<Module>>>& cache() {
+    static std::vector<std::pair<std::string, std::shared_ptr<Module>>> c;
+    return c;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) != cudaSuccess ||
+            r != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return reinterpret_cast<EncodeTiledFn>(q);
+    }();
+    return fn;
+}
+
+// [rows][cols] 4-byte elements, boxes of 32 rows x 32 elements (128 B), 128-byte swizzle
+bool make_map(CUtensorMap* m, const void* base, long long rows, int cols, bool f32) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims,
+               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count(int dev) {
+    static int cnt[kMaxDevices] = {};
+    if (!cnt[dev]) {
+        int c = 0;
+        if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0) c = 148;
+        cnt[dev] = c;
+    }
+    return cnt[dev];
+}
+
+// key multipliers as kernel-parameter operands: 21-bit limbs of r[l][j+1], then r[l][0]
+std::vector<unsigned char> key_args(const fastlsh_keys* ks) {
+    const int L = ks->L, K = ks->K;
+    const size_t limb_bytes = (size_t)L * K * 3 * 4;
+    const size_t r0_off = (limb_bytes + 7) / 8 * 8;
+    std::vector<unsigned char> buf(r0_off + (size_t)L * 8, 0);
+    uint32_t* limb = reinterpret_cast<uint32_t*>(buf.data());
+    for (int l = 0; l < L; ++l) {
+        for (int j = 0; j < K; ++j) {
+            const uint64_t r = ks->r[(size_t)l * (K + 1) + j + 1];
+            limb[(l * K + j) * 3 + 0] = (uint32_t)(r & 0x1fffff);
+            limb[(l * K + j) * 3 + 1] = (uint32_t)((r >> 21) & 0x1fffff);
+            limb[(l * K + j) * 3 + 2] = (uint32_t)(r >> 42);
+        }
+        const uint64_t r0 = ks->r[(size_t)l * (K + 1)];
+        std::memcpy(buf.data() + r0_off + 8 * l, &r0, 8);
+    }
+    return buf;
+}
+
+bool keys_fit(const fastlsh_params& p, const fastlsh_keys* ks) {
+    // kernel parameters <= 32 KB: two tensor maps, JArgs and the limbs
+    return (int64_t)ks->L * ks->K <= p.k && (size_t)ks->L * ks->K * 12 + (size_t)ks->L * 8 + 512 <= 31 * 1024;
+}
+
+std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, int L, int K, fastlsh_status* st) {
+    State& js = p->jit;
+    std::lock_guard<std::mutex> g(js.mu);
+    for (auto& v : js.variants)
+        if (v.first[0] == mode && v.first[1] == L && v.first[2] == K) return v.second;
+    const int warps = warps_for(p->n);
+    Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), L, K, warps, kNcb, mode};
+    std::string src = k1j_source(s);
+    std::shared_ptr<Module> mod;
+    {
+        std::lock_guard<std::mutex> gc(g_cache_mu);
+        for (auto& c : cache())
+            if (c.first == src) mod = c.second;
+    }
+    if (!mod) {
+        std::vector<char> cubin;
+        std::string log;
+        double sec = 0;
+        if (!compile_cubin(src, cubin, log, &sec)) {
+            js.last_error = "K1j compile failed: " + log.substr(0, 2000);
+            *st = FASTLSH_EUNSUPPORTED;
+            return nullptr;
+        }
+        js.compile_seconds += sec;
+        mod = std::make_shared<Module>();
+        cudaError_t e = cudaLibraryLoadData(&mod->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        if (e == cudaSuccess) e = cudaLibraryGetKernel(&mod->kern, mod->lib, "k1j");
+        if (e != cudaSuccess) {
+            js.last_error = std::string("K1j module load failed: ") + cudaGetErrorString(e);
+            *st = set_cuda_error(e);
+            return nullptr;
+        }
+        mod->warps = warps;
+        mod->smem = smem_bytes(p->n, warps);
+        std::lock_guard<std::mutex> gc(g_cache_mu);
+        cache().emplace_back(std::move(src), mod);
+    }
+    js.variants.push_back({{mode, L, K}, mod});
+    return mod;
+}
+
+}  // namespace
+
+bool applicable(const fastlsh_params& p) {
+    State& js = p.jit;
+    std::lock_guard<std::mutex> g(js.mu);
+    if (js.applicable < 0) {
+        const char* off = std::getenv("FASTLSH_NO_JIT");
+        const bool disabled = off && *off && std::strcmp(off, "0") != 0;
+        js.applicable = !disabled && p.n <= kMaxN && p.n % 4 == 0 && p.k % 4 == 0 &&
+                        (int64_t)p.k * p.m <= kMaxCode && (size_t)4 * (p.n + p.k) <= (size_t)kNcb * 4096 &&
+                        warps_for(p.n) >= 1 && nvrtc_available();
+    }
+    return js.applicable == 1;
+}
+
+fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks) {
+    if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
+    if (ks && (mode != 0 || !keys_fit(*p, ks))) return FASTLSH_EUNSUPPORTED;
+    fastlsh_status st = FASTLSH_OK;
+    return get_variant(p, mode, ks ? ks->L : 0, ks ? ks->K : 0, &st) ? FASTLSH_OK : st;
+}
+
+fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
+                      float* proj, const fastlsh_keys* ks, const uint64_t* dev_r, uint64_t* keys, int64_t ldk,
+                      cudaStream_t stream) {
+    if (!applicable(*p) || !d.j_idx) return FASTLSH_EUNSUPPORTED;
+    void* out = proj ? static_cast<void*>(proj) : static_cast<void*>(codes);
+    const int mode = proj ? 1 : 0;
+    if (proj && ks) return FASTLSH_EUNSUPPORTED;
+    if (!out && !ks) return FASTLSH_EINVAL;
+    if (ks && (!keys_fit(*p, ks) || !keys || !dev_r)) return FASTLSH_EUNSUPPORTED;
+    if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+        N > (int64_t)0x7fffffff - 64)
+        return FASTLSH_EUNSUPPORTED;
+    fastlsh_status st = FASTLSH_OK;
+    std::shared_ptr<Module> mod = get_variant(p, mode, ks ? ks->L : 0, ks ? ks->K : 0, &st);
+    if (!mod) return st;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    {
+        std::lock_guard<std::mutex> g(mod->mu);
+        if (!mod->attr_set[dev]) {
+            e = cudaKernelSetAttributeForDevice(mod->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mod->smem, dev);
+            if (e != cudaSuccess) return set_cuda_error(e);
+            mod->attr_set[dev] = true;
+        }
+    }
+    CUtensorMap xmap, omap;
+    if (!make_map(&xmap, X, N, p->n, true)) return FASTLSH_EUNSUPPORTED;
+    if (out) {
+        if (!make_map(&omap, out, N, p->k, proj != nullptr)) return FASTLSH_EUNSUPPORTED;
+    } else {
+        omap = xmap;  // keys only: never used
+    }
+    struct JArgs {
+        long long N, tiles;
+        int write_out;
+        int* out;
+        uint64_t* keys;
+        long long ldk, col0;
+        unsigned long long* flags;
+        const int* idx;
+        const float* a;
+        const float* b;
+        const uint64_t* kr;
+    } a;
+    a.N = N;
+    a.tiles = (N + 31) / 32;
+    a.write_out = out ? 1 : 0;
+    a.out = static_cast<int*>(out);
+    a.keys = keys;
+    a.ldk = ldk;
+    a.col0 = 0;
+    a.flags = d.flags;
+    a.idx = d.j_idx;
+    a.a = d.j_a;
+    a.b = d.b;
+    a.kr = dev_r;
+    std::vector<unsigned char> kargs = ks ? key_args(ks) : std::vector<unsigned char>(4, 0);
+    const long long ctas_needed = (a.tiles + mod->warps - 1) / mod->warps;
+    const int grid = (int)(ctas_needed < sm_count(dev) ? ctas_needed : sm_count(dev));
+    void* args[4] = {&xmap, &omap, &a, kargs.data()};
+    e = cudaLaunchKernel(reinterpret_cast<const void*>(mod->kern), dim3(grid), dim3(mod->warps * 32), args, mod->smem,
+                         stream);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    return FASTLSH_OK;
+}
+
+}  // namespace jit
+}  // namespace fastlsh
+
+#ifdef FASTLSH_JIT_MAIN
+// Standalone check of the generator + NVRTC (no GPU needed): prints the compile time and writes
+// the source and cubin for inspection with cuobjdump.
+#include "philox.h"
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? atoi(argv[1]) : 128, m = argc > 2 ? atoi(argv[2]) : 16, k = argc > 3 ? atoi(argv[3]) : 256;
+    const int L = argc > 4 ? atoi(argv[4]) : 16, K = argc > 5 ? atoi(argv[5]) : 16;
+    const float w = 4.0f;
+    std::vector<int32_t> idx((size_t)k * m);
+    std::vector<float> a((size_t)k * m), b(k);
+    for (int i = 0; i < k; ++i) {
+        for (int j = 0; j < m; ++j) {
+            idx[(size_t)i * m + j] = fastlsh::draw_index(1, i, j, n);
+            a[(size_t)i * m + j] = fastlsh::draw_gaussian(1, i, j);
+        }
+        b[i] = fastlsh::draw_offset(1, i, w);
+    }
+    fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, 8, 2, argc > 6 ? atoi(argv[6]) : 0};
+    const std::string src = fastlsh::jit::k1j_source(s);
+    FILE* f = fopen("/tmp/k1j.cu", "w");
+    fwrite(src.data(), 1, src.size(), f);
+    fclose(f);
+    std::vector<char> cubin;
+    std::string log;
+    double sec = 0;
+    const bool ok = fastlsh::jit::compile_cubin(src, cubin, log, &sec);
+    printf("source %zu bytes, compile %s in %.2f s, cubin %zu bytes\n%s\n", src.size(), ok ? "ok" : "FAILED", sec,
+           cubin.size(), log.c_str());
+    if (ok) {
+        f = fopen("/tmp/k1j.cubin", "wb");
+        fwrite(cubin.data(), 1, cubin.size(), f);
+        fclose(f);
+    }
+    return ok ? 0 : 1;
+}
+#endif

@@ -193,7 +193,7 @@ def test_fused_keys_equal_separate_kernels(name, L, K, N, extra_k):
     c = configs.get(name)
     k = L * K + extra_k if name == "C0" else c.k
     idx, a, b = fastlsh_arrays(c.n, c.m, k, c.w, 3)
-    P_fused = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(K)
+    P_fused = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(K).set_kernel("smem")
     P_plain = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_kernel("smem")  # the fused path is K1's
     Kobj = fl.Keys.from_arrays(philox.key_multipliers(L, K, seed=4))
     X = data.generate(c.data, c.n, 0, N, seed=5, device="cuda")
@@ -381,7 +381,7 @@ def test_rows_kernel_keys_from_code_tile(name, L, K, N):
     columns [col0, col0 + N) of a wider table. C4 (8 blocks) takes the separate kernel, same result."""
     c = configs.get(name)
     idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 3)
-    P = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    P = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_kernel("rows")  # (C0/C3 default to K1j)
     assert P.info()["kernel"] == 3
     Kobj = fl.Keys.from_arrays(philox.key_multipliers(L, K, seed=4))
     X = data.generate(c.data, c.n, 0, N, seed=5, device="cuda")
@@ -570,8 +570,8 @@ def test_fused_keys_only_chunked_equals_separate():
     equals codes + the key kernel (C3 shape: 16 tables of 16 codes)."""
     c = configs.get("C3")
     idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 2)
-    Pf = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(c.K)
-    Pp = fl.Params.from_arrays(c.n, c.w, idx, a, b)
+    Pf = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_table_size(c.K).set_kernel("smem")
+    Pp = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_kernel("smem")
     Kobj = fl.Keys.create(c.L, c.K, seed=7)
     N = 20_011
     X = data.generate(c.data, c.n, 0, N, seed=3, device="cuda")

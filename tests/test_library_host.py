@@ -158,27 +158,52 @@ def test_bench_config_packing_quality(lib):
     assert info["bank_efficiency"] >= 0.9
 
 
-def test_kernel_selection_rules(lib):
-    """fastlsh_params_set_kernel: 0-3 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128;
-    auto mode reports K1r (3) for n % 4 == 0 shapes whose row packing exists, else K1."""
+def test_kernel_selection_rules(lib, monkeypatch):
+    """fastlsh_params_set_kernel: 0-4 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128;
+    auto mode reports K1j (4) for n <= 128 shapes (NVRTC present), K1r (3) for other n % 4 == 0
+    shapes whose row packing exists, else K1; FASTLSH_NO_JIT=1 turns K1j off."""
     import paper_2309_15479_b200 as fl
     from fastlsh_inputs import fastlsh_arrays
     idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
     P = fl.Params.from_arrays(128, 4.0, idx, a, b)
-    assert P.info()["kernel"] == 3
-    for k in ("smem", "tmem", "rows", "auto"):
+    assert P.info()["kernel"] == 4
+    for k in ("smem", "tmem", "rows", "jit", "auto"):
         P.set_kernel(k)
     P.set_kernel("tmem")
     assert P.info()["kernel"] == 2 and P.info()["tmem_hash_blocks"] >= 1
     P.set_kernel("smem")
     assert P.info()["kernel"] == 1
+    P.set_kernel("rows")
+    assert P.info()["kernel"] == 3
     with pytest.raises(fl.FastLSHError):
-        P.set_kernel(4)
+        P.set_kernel(5)
     idx, a, b = fastlsh_arrays(130, 16, 64, 4.0, 1)   # n % 4 != 0: no TMA tensor map / bulk rows
     Q = fl.Params.from_arrays(130, 4.0, idx, a, b)
-    with pytest.raises(fl.FastLSHError):
-        Q.set_kernel("tmem")
+    for kern in ("tmem", "jit"):
+        with pytest.raises(fl.FastLSHError):
+            Q.set_kernel(kern)
     assert Q.info()["kernel"] == 1
+    idx, a, b = fastlsh_arrays(960, 60, 500, 1.0, 1)  # n > 128: K1j does not apply
+    assert fl.Params.from_arrays(960, 1.0, idx, a, b).info()["kernel"] == 3
+    monkeypatch.setenv("FASTLSH_NO_JIT", "1")
+    idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
+    assert fl.Params.from_arrays(128, 4.0, idx, a, b).info()["kernel"] == 3
+
+
+def test_jit_source_compiles_for_sm100a(lib):
+    """K1j's generated source (C0 shape: 64 hashes x 16 samples) compiles with NVRTC for sm_100a on
+    this CPU-only host; loading the module then needs a driver (ECUDA here, OK on a B200)."""
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import fastlsh_arrays
+    idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
+    P = fl.Params.from_arrays(128, 4.0, idx, a, b)
+    try:
+        P.prepare()
+    except fl.FastLSHError as e:
+        assert e.status == fl.ECUDA
+    st = P.jit_status()
+    assert st["compile_seconds"] > 0, st
+    assert "compile failed" not in st["error"], st
 
 
 def _unpack_rows(p):
