@@ -1,13 +1,20 @@
 #!/usr/bin/env python
 """Benchmark of the FastLSH hot path on B200 (BASELINE.json metric: hashes/s and roofline fraction).
 
-One step = one pass of the whole hot path over the workload resident in HBM:
-  K1 fastlsh_hash (stage X, gather S_i(v), project, +b, /w, floor, int32 codes)
-  K3 fastlsh_build_keys (L tables of K codes -> 64-bit keys)
-  (N>1 GPUs) NCCL all-gather of the keys, one all_gather_into_tensor per table.
-Default workload: BASELINE.json configs[1] (C1: N=1e6, n=960, k=500, m=60, w=1, L=50 x K=10).
+One step = one pass of the whole hot path over the workload resident in HBM (SURVEY.md §8(a)):
+  a2-a5 hash (stage X, gather S_i(v), project, +b, /w, floor, int32 codes stored to HBM) and
+  a6 compound keys (L tables of K codes -> 64-bit keys, table-major [L][N]);
+  a8 (N > 1 GPUs) the NCCL all-gather of the keys, one all_gather_into_tensor per table.
+Where the params-specialised kernel K1j applies (n <= 128: C0, C3) a2-a6 are ONE launch per chunk
+(fastlsh_hash_keys: codes and keys); elsewhere K1r + the key kernel.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl reference]
+Default workload: BASELINE.json configs[3] (C3), the configuration the metric "at 1/2/4/8 B200"
+is quoted on: a fixed 2e8-row dataset (n=128, k=256, m=16, w=4, keys 16 x 16) row-sharded across
+the ranks (strong scaling), hashed in chunks (its 204.8 GB of codes do not fit one GPU; each
+chunk's codes are written to HBM and overwritten by the next chunk, keys of all rows kept).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C1|C2|C4] [--impl reference]
+  python bench.py --config C4 --stream      (streaming rebuild: 1000 batches through host rings)
 
 Rank 0 prints ONE JSON line. See DESIGN.md "Measurement" for every field.
 """
@@ -16,6 +23,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -29,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FastLSH hashes/sec (N*k) and % of HBM/smem roofline"
 SMEM_GATHERS_PER_CLK_PER_SM = 32  # one 128-B wavefront of 4-B words per SM per clock
+NUM_SMS = 148
 
 
 def _peaks():
@@ -36,7 +45,7 @@ def _peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
         return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
-                "source": "measured (MEASURED_PEAKS.json)"}
+                "source": "measured (MEASURED_PEAKS.json: copy bandwidth, burst)"}
     except Exception:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
 
@@ -100,38 +109,66 @@ def _cores():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_baseline(cfg, seconds_target: float = 12.0):
-    """The CPU oracle as it stands, on a bounded row sample of the same workload, all host cores."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _sample_rows(N: int, count: int, seed: int, extra=()):
+    rng = np.random.default_rng(seed)
+    r = set(rng.choice(N, size=min(count, N), replace=False).tolist()) if N else set()
+    r.update(x for x in (0, N - 1, *extra) if 0 <= x < N)
+    return np.array(sorted(r), dtype=np.int64)
+
+
+def cpu_baseline(cfg, seconds_target: float = 12.0, one_core_seconds: float = 3.0, rows_from=None):
+    """The CPU oracle as it stands, on a bounded row sample of the same workload: all host cores,
+    then 1 core. rows_from(lo, hi) supplies the rows (default: the synthetic
+    generator on the host)."""
     import oracle
     from fastlsh_inputs import data, fastlsh_arrays
     idx, a, b = fastlsh_arrays(cfg.n, cfg.m, cfg.k, cfg.w, cfg.seed)
     cores = _cores()
+    get = rows_from or (lambda lo, hi: data.generate(cfg.data, cfg.n, lo, hi, seed=cfg.seed).numpy())
     # calibrate on a small sample, then size the measured sample to ~seconds_target
     rows0 = 256
-    X0 = data.generate(cfg.data, cfg.n, 0, rows0, seed=cfg.seed).numpy()
+    X0 = get(0, rows0)
     t = time.perf_counter()
     oracle.fastlsh(X0, idx, a, b, cfg.w, threads=cores)
     dt = max(time.perf_counter() - t, 1e-4)
     rows = int(min(cfg.N, max(rows0, rows0 * seconds_target / dt)))
-    X = data.generate(cfg.data, cfg.n, 0, rows, seed=cfg.seed).numpy()
+    X = get(0, rows)
     t = time.perf_counter()
     oracle.fastlsh(X, idx, a, b, cfg.w, threads=cores)
     dt = time.perf_counter() - t
+    rows1 = int(min(rows, max(64, rows0 * one_core_seconds / (dt / rows * rows0 * cores))))
+    t = time.perf_counter()
+    oracle.fastlsh(X[:rows1], idx, a, b, cfg.w, threads=1)
+    dt1 = time.perf_counter() - t
     return {"value": rows * cfg.k / dt, "unit": "hashes/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {rows} of {cfg.N} rows ({cfg.name}), double-precision oracle, OpenMP "
-                      f"{cores} threads, {dt:.2f} s (codes only; keys not included)",
+            "value_1core": rows1 * cfg.k / dt1, "cpu_model": _cpu_model(),
+            "sample": f"first {rows} of {cfg.N} rows ({cfg.name}), double-precision oracle (oracle/fastlsh_oracle.c), "
+                      f"OpenMP {cores} threads, {dt:.2f} s; 1-core rate on the first {rows1} rows, {dt1:.2f} s "
+                      f"(codes only; keys not included)",
             "seconds": dt}
 
 
 def run_reference(args, cfg):
+    """The reference arm of this tier: the CPU oracle as it stands, on the host cores."""
     world, rank, _ = _dist_env()
     if rank != 0:
         return
     steps = []
     for _ in range(args.warmup):
-        cpu_baseline(cfg, seconds_target=2.0)
+        cpu_baseline(cfg, seconds_target=2.0, one_core_seconds=0.2)
     for _ in range(args.steps):
-        steps.append(cpu_baseline(cfg, seconds_target=args.ref_seconds))
+        steps.append(cpu_baseline(cfg, seconds_target=args.ref_seconds, one_core_seconds=0.5))
     vals = [s["value"] for s in steps]
     v = statistics.median(vals)
     cb = dict(steps[-1])
@@ -140,17 +177,18 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "hashes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in steps),
-            "higher_is_better": True, "scaling": "strong" if cfg.name == "C3" else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(cfg, world),
+            "higher_is_better": True, "scaling": "strong" if cfg.name == "C3" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": _config_dict(cfg, world),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "hashes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1):
+def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1, strong=None):
+    strong = (cfg.name == "C3") if strong is None else strong
     n_rank = cfg.N if n_rank is None else n_rank
-    n_total = cfg.N * world if n_total is None else n_total
-    d = {"workload": f"{cfg.name}: N={n_rank} rows/GPU, n={cfg.n}, k={cfg.k}, m={cfg.m}, w={cfg.w}, "
+    n_total = cfg.N * (1 if strong else world) if n_total is None else n_total
+    d = {"workload": f"{cfg.name}: N={n_total} rows ({n_rank} per GPU), n={cfg.n}, k={cfg.k}, m={cfg.m}, w={cfg.w}, "
                      f"keys L={cfg.L} x K={cfg.K}, recipe {cfg.data}",
          "N_per_gpu": n_rank, "n": cfg.n, "k": cfg.k, "m": cfg.m, "w": cfg.w, "L": cfg.L, "K": cfg.K,
          "global_rows": n_total, "parallelism": f"row-sharded x{world}, params replicated",
@@ -160,9 +198,34 @@ def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1):
     return d
 
 
-def _packing_summary(P, info, fused_keys):
-    """The GPU layout of the kernel that ran (K1r's row packing, else K1's)."""
-    rp = P.row_packing() if info["kernel"] == 3 and not fused_keys else None
+def _kernel_name(info, fused):
+    if info["kernel"] == 4:
+        return ("k1j (K1j fastlsh_hash_keys: params-specialised lane = row kernel, codes + keys in one launch)"
+                if fused else "k1j (K1j fastlsh_hash: params-specialised lane = row kernel)")
+    return {1: "gather_kernel (K1 fastlsh_hash)", 2: "tmem_gather_kernel (K1t fastlsh_hash)",
+            3: "rows_kernel (K1r fastlsh_hash: row-major stages, LDS.32)"}[info["kernel"]]
+
+
+def _launches_per_call(P, info, Kobj) -> int:
+    """Kernel launches of one fastlsh_hash_keys call (api.cu's dispatch rules): K1j and K1r with the
+    keys built from its code tile (one CTA hash block, key work small next to the gathers) are one
+    launch; otherwise hash + the key kernel."""
+    if Kobj is None or info["kernel"] == 4:
+        return 1
+    rp = P.row_packing() if info["kernel"] == 3 else None
+    if rp is not None and rp["hash_blocks"] == 1 and \
+            Kobj.L * Kobj.K <= 0.75 * rp["hash_blocks"] * rp["warps"] * rp["slots"]:
+        return 1
+    return 2
+
+
+def _packing_summary(P, info):
+    """The GPU layout of the kernel that ran."""
+    if info["kernel"] == 4:
+        return {"kernel": "K1j", "lane": "row (32 rows per warp, row in registers)",
+                "code": "S_i register operands, a_i / b_i / 1/w immediates (NVRTC, sm_100a)",
+                "jit": P.jit_status()}
+    rp = P.row_packing() if info["kernel"] == 3 else None
     if rp is not None:
         lanes = rp["hash_blocks"] * rp["warps"] * 32 * rp["slots"]
         return {"kernel": "K1r", "parts": rp["parts"], "slots": rp["slots"], "warps_per_block": rp["warps"],
@@ -172,42 +235,75 @@ def _packing_summary(P, info, fused_keys):
                                                     "bank_efficiency", "conflict_wavefronts")}}
 
 
-def _traffic_from_profiles(cfg, rows: int):
+def _traffic_from_profiles(cfg, kernel: str, rows: int):
     """DRAM bytes per launch of the dominant kernel, from the committed `ncu --set full` capture
-    (profiles/ncu_gather_full.json: dram__bytes_read + dram__bytes_write of one K1 launch on the
-    same params), scaled per row to this launch's row count. None if no capture is committed."""
-    path = os.path.join(ROOT, "profiles", "ncu_gather_full.json")
+    (profiles/ncu_traffic.json: dram__bytes_read + dram__bytes_write per row, per config and kernel),
+    scaled to this launch's row count. None if no capture is committed for this config/kernel."""
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        if d.get("config", "C1") != cfg.name:
-            return None
-        return d["dram_bytes_per_row"] * rows
+        e = d[f"{cfg.name}/{kernel}"]
+        return {"bytes_per_launch": e["dram_bytes_per_row"] * rows, "source": e["source"]}
     except Exception:
         return None
+
+
+def _roofline(cfg, info, fused, N_launch, t_launch_s, step_ms, peaks, with_codes=True):
+    """Dominant-kernel roofline. K1j reads X and writes codes (+ keys) with no shared-memory
+    gather, so its bound is HBM: achieved = algorithmic bytes per launch / launch time. K1r / K1 are
+    shared-memory-bound: achieved gathers/s against G_s. Both also report the north_star fraction
+    t_roof / t_kernel with t_roof = max(HBM time of X + codes, N k m / G_s)."""
+    gathers = N_launch * cfg.k * cfg.m
+    g_peak = NUM_SMS * SMEM_GATHERS_PER_CLK_PER_SM * peaks["sm_max_mhz"] * 1e6
+    hbm_ns = 4.0 * N_launch * cfg.n + (4.0 * N_launch * cfg.k if with_codes else 0.0)
+    t_roof = max(hbm_ns / (peaks["hbm_gbs"] * 1e9), gathers / g_peak)
+    t_roof_nominal = max(hbm_ns / 8.0e12, gathers / g_peak)
+    kern = "K1j" if info["kernel"] == 4 else {1: "K1", 2: "K1t", 3: "K1r"}[info["kernel"]]
+    if info["kernel"] == 4:
+        alg = hbm_ns + (8.0 * N_launch * cfg.L if (fused and cfg.L) else 0.0)
+        r = {"bound": "hbm", "achieved": alg / t_launch_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": alg / t_launch_s / (peaks["hbm_gbs"] * 1e9),
+             "algorithmic_per_launch": {"hbm_bytes": alg, "rows": N_launch,
+                                        "bytes_per_row": {"X": 4 * cfg.n, "codes": 4 * cfg.k if with_codes else 0,
+                                                          "keys": 8 * cfg.L if (fused and cfg.L) else 0},
+                                        "gathers": gathers}}
+    else:
+        r = {"bound": "smem", "achieved": gathers / t_launch_s / 1e9, "peak": g_peak / 1e9, "unit": "Ggather/s",
+             "frac": (gathers / t_launch_s) / g_peak,
+             "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_ns, "rows": N_launch}}
+    tr = _traffic_from_profiles(cfg, kern + ("+keys" if fused else "") + ("" if with_codes else "-keysonly"), N_launch)
+    r.update({"traffic": tr["bytes_per_launch"] if tr else None,
+              "traffic_source": tr["source"] if tr else "no committed ncu capture for this config/kernel",
+              "kernel": _kernel_name(info, fused),
+              "launch_ms": t_launch_s * 1e3,
+              "gathers_per_s": gathers / t_launch_s, "smem_gather_peak_per_s": g_peak,
+              "north_star_frac": t_roof / t_launch_s, "north_star_frac_nominal_8TBs": t_roof_nominal / t_launch_s,
+              "hbm_achieved_gbs": (hbm_ns + (8.0 * N_launch * cfg.L if fused and cfg.L else 0.0)) / t_launch_s / 1e9,
+              "peak_source": peaks["source"] + f"; smem peak = {NUM_SMS} SM x 32 words/clk x {peaks['sm_max_mhz']:.0f} MHz",
+              "kernel_share_of_step": (t_launch_s * 1e3) / step_ms if step_ms else None})
+    return r
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C1")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
-    ap.add_argument("--fused-keys", action="store_true",
-                    help="K1 with keys built in its epilogue (set_table_size; measured slower than K1r)")
-    ap.add_argument("--keys-from-tile", action="store_true",
-                    help="time the step with K1r building the keys from its code tile (one launch) instead of "
-                         "codes + the key kernel; the default reports it as a side measurement")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem"],
+                    help="pin the hashing kernel (auto: K1j for n <= 128, else K1r)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1: wait for each step's key all-gather before the next step hashes")
-    ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk")
+    ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk (launch)")
     ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build and query measurements")
     ap.add_argument("--queries", type=int, default=10_000, help="queries answered in the query measurement")
+    ap.add_argument("--stream", action="store_true", help="C4 streaming rebuild (see stream_main)")
+    ap.add_argument("--batches", type=int, default=None, help="--stream: batches per step (default: the config's)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -217,11 +313,15 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg)
         return
+    if args.stream:
+        import stream_bench
+        stream_bench.main(args, cfg)
+        return
 
     import torch
     import torch.distributed as dist
     import paper_2309_15479_b200 as fl
-    from paper_2309_15479_b200.distributed import allgather_keys
+    from paper_2309_15479_b200.distributed import allgather_keys, shard_rows
     from fastlsh_inputs import data
 
     world, rank, local = _dist_env()
@@ -229,16 +329,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
 
     P = fl.Params.create(cfg.n, cfg.m, cfg.k, cfg.w, seed=cfg.seed)
+    if args.kernel != "auto":
+        P.set_kernel(args.kernel)
     Kobj = fl.Keys.create(cfg.L, cfg.K, seed=cfg.seed) if cfg.L else None
-    if Kobj is not None and args.fused_keys:
-        P.set_table_size(cfg.K)  # whole tables per CTA: keys are built in K1's epilogue
     info = P.info()
-    # C3 is a fixed 2e8-row dataset sharded over the ranks (strong scaling) and hashed in chunks:
-    # its codes (204.8 GB) do not fit one GPU, so only a chunk of codes lives at a time while the
-    # keys of all rows are built into [L][N]. Other configs are per-GPU workloads.
-    from paper_2309_15479_b200.distributed import shard_rows
+    jit = info["kernel"] == 4
+    t_prep = time.perf_counter()
+    P.prepare(keys=Kobj, codes=True)  # K1j: NVRTC compile outside the timed region (no-op otherwise)
+    prep_s = time.perf_counter() - t_prep
+
+    # C3 is a fixed 2e8-row dataset sharded over the ranks (strong scaling) and hashed in chunks; other
+    # configs are per-GPU workloads (weak scaling).
     strong = cfg.name == "C3"
     if strong:
         N_total = cfg.N
@@ -252,67 +356,42 @@ def main():
     X = data.generate(cfg.data, cfg.n, lo, hi, seed=cfg.seed, device=dev)
     codes = torch.empty((chunk, cfg.k), dtype=torch.int32, device=dev)
     keys = torch.empty((cfg.L, N), dtype=torch.int64, device=dev) if Kobj else None
-    gathered = torch.empty((cfg.L, world * N), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
+    gathered = torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
     # N > 1: the key all-gather of step j runs on NCCL's stream while step j+1 hashes into the other
     # keys buffer (double-buffered); step j+1 waits for it before launching its own all-gather
     overlap = gathered is not None and not args.no_overlap
     keys_bufs = [keys, torch.empty_like(keys)] if overlap else [keys]
-    pending = []  # NCCL works of the previous step's all-gather
+    pending = []
     step_no = [0]
-    stream = torch.cuda.current_stream()
-
-    fused_keys = bool(Kobj) and args.fused_keys
-    # default: K1r builds the keys from its shared-memory code tile (one launch per chunk) when one
-    # CTA hash block covers all k hashes (C1, C3)
-    rp = P.row_packing() if info["kernel"] == 3 else None
-    tile_keys_ok = (bool(Kobj) and not fused_keys and rp is not None and rp["hash_blocks"] == 1
-                    # the library's rule (api.cu rows_keys_pay): key work small next to the gathers
-                    and cfg.L * cfg.K <= 0.75 * rp["hash_blocks"] * rp["warps"] * rp["slots"])
-    # Default step: K1r codes, then the key kernel, so the dominant kernel's roofline is the hashing
-    # kernel's own. The one-launch variant (keys from K1r's code tile) is timed on the side.
-    rows_fused = tile_keys_ok and args.keys_from_tile
-    launches_per_step = len(bounds) * (1 + (1 if (Kobj and not fused_keys and not rows_fused) else 0))
+    fused = bool(Kobj)  # fastlsh_hash_keys: one launch where K1j / K1r-tile keys apply, else hash + keys
     ev = []
 
     def step(record: bool):
-        marks = []  # per chunk: (before hash, after hash, after keys)
-        keys = keys_bufs[step_no[0] % len(keys_bufs)]
+        marks = []
+        kb = keys_bufs[step_no[0] % len(keys_bufs)]
         step_no[0] += 1
         for c0, c1 in bounds:
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if record else None
             if record:
                 e[0].record(stream)
             cb = codes[:c1 - c0]
-            if rows_fused:
-                fl.hash_keys(P, Kobj, X[c0:c1], codes=cb, keys_out=keys, col0=c0)  # one launch: codes + keys
-                if record:
-                    e[1].record(stream)
-            elif Kobj and args.fused_keys:
-                if strong:  # keys only: the codes of the 2e8 rows never reach HBM
-                    fl.hash_keys(P, Kobj, X[c0:c1], keys_out=keys, with_codes=False, col0=c0)
-                else:
-                    fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)  # one launch: codes + keys
-                if record:
-                    e[1].record(stream)
+            if Kobj is not None:
+                fl.hash_keys(P, Kobj, X[c0:c1], codes=cb, keys_out=kb, col0=c0)
             else:
                 fl.fastlsh_hash(P, X[c0:c1], out=cb)
-                if record:
-                    e[1].record(stream)
-                if Kobj:
-                    fl.build_keys(Kobj, cb, out=keys, col0=c0)
             if record:
-                e[2].record(stream)
+                e[1].record(stream)
                 marks.append(e)
         ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if record else None
         if record:
             ea[0].record(stream)
         if gathered is not None:
             if overlap:
-                for w in pending:  # the previous step's all-gather (overlapped with this step's hashing)
+                for w in pending:
                     w.wait()
-                pending[:] = allgather_keys(keys, out=gathered, wait=False)
+                pending[:] = allgather_keys(kb, out=gathered, wait=False, n_total=N_total)
             else:
-                allgather_keys(keys, out=gathered)
+                allgather_keys(kb, out=gathered, n_total=N_total)
         if record:
             ea[1].record(stream)
             ev.append((marks, ea))
@@ -350,70 +429,74 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
+    launch_ms = [m[0].elapsed_time(m[1]) for marks, _ in ev for m in marks]  # one entry per chunk launch
+    launch_rows = [c1 - c0 for _ in ev for c0, c1 in bounds]
     hash_ms = [sum(m[0].elapsed_time(m[1]) for m in marks) for marks, _ in ev]
-    keys_ms = [sum(m[1].elapsed_time(m[2]) for m in marks) for marks, _ in ev]
     ag_ms = [ea[0].elapsed_time(ea[1]) for _, ea in ev]
     tt = torch.tensor([total_ms, statistics.mean(hash_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_ms_max, hash_ms_max = float(tt[0]), float(tt[1])
     ms_per_step = total_ms_max / args.steps
-    hashes_per_step = N_total * cfg.k
-    value = hashes_per_step / (ms_per_step / 1e3)
-
-    # roofline of the dominant kernel (K1): smem gathers vs the north_star bound
+    value = N_total * cfg.k / (ms_per_step / 1e3)
     peaks = _peaks()
-    t_hash = statistics.mean(hash_ms) / 1e3
-    gathers = N * cfg.k * cfg.m
-    g_peak = 148 * SMEM_GATHERS_PER_CLK_PER_SM * peaks["sm_max_mhz"] * 1e6
-    hbm_bytes = 4.0 * N * cfg.n + 4.0 * N * cfg.k
-    t_roof = max(hbm_bytes / (peaks["hbm_gbs"] * 1e9), gathers / g_peak)
-    t_roof_nominal = max(hbm_bytes / 8.0e12, gathers / g_peak)
-    roofline = {"bound": "smem", "achieved": gathers / t_hash / 1e9, "peak": g_peak / 1e9,
-                "unit": "Ggather/s", "frac": (gathers / t_hash) / g_peak,
-                "traffic": _traffic_from_profiles(cfg, N),
-                "kernel": ("gather_kernel (K1 fastlsh_hash, keys fused in its epilogue)" if fused_keys else
-                           "rows_kernel (K1r fastlsh_hash_keys: row-major stages, LDS.32; keys built from its "
-                           "shared-memory code tile)" if rows_fused else
-                           {1: "gather_kernel (K1 fastlsh_hash)", 2: "tmem_gather_kernel (K1t fastlsh_hash)",
-                            3: "rows_kernel (K1r fastlsh_hash: row-major stages, LDS.32)"}[info["kernel"]]),
-                "algorithmic_per_launch": {"gathers": gathers, "hbm_bytes": hbm_bytes},
-                "north_star_frac": t_roof / t_hash, "north_star_frac_nominal_8TBs": t_roof_nominal / t_hash,
-                "hbm_achieved_gbs": hbm_bytes / t_hash / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"],
-                "peak_source": peaks["source"] + f"; smem peak = 148 SM x 32 x {peaks['sm_max_mhz']:.0f} MHz",
-                "kernel_share_of_step": statistics.mean(hash_ms) / ms_per_step if ms_per_step else None}
+    # the dominant kernel: the per-chunk launch, averaged over full-size chunks
+    full = [t for t, r in zip(launch_ms, launch_rows) if r == chunk] or launch_ms
+    t_launch = statistics.mean(full) / 1e3
+    lpc = _launches_per_call(P, info, Kobj)
+    roofline = _roofline(cfg, info, fused and lpc == 1, chunk, t_launch, ms_per_step, peaks)
+    if lpc > 1:
+        roofline["note"] = "the per-chunk time covers the hashing kernel and the key kernel (two launches)"
+    roofline["launch_ms_min_max"] = [min(full), max(full)]
 
-    # side measurement: the same step with the keys built from K1r's code tile (one launch)
-    tile_keys = None
-    if tile_keys_ok and not rows_fused and not strong:
-        torch.cuda.synchronize()
-        for _ in range(2):
-            fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t_ms = e0.elapsed_time(e1) / args.steps
-        tile_keys = {"ms_per_step": t_ms, "value": N * cfg.k / (t_ms / 1e3), "unit": "hashes/s",
-                     "note": "hash + keys in one K1r launch (fastlsh_hash_keys), rank-local, same inputs; "
-                             "not the headline step"}
+    # parity sample of the timed step's own output (the last chunk's codes, the keys of those rows),
+    # copied out now, before any side measurement reuses the buffers; checked in the CPU leg below
+    c0p, c1p = bounds[-1]
+    prow = _sample_rows(c1p - c0p, 512, seed=11, extra=[1, 31, 32, 33, (c1p - c0p) // 2])
+    pri = torch.as_tensor(prow, device=dev)
+    psample = {"X": X[c0p:c1p][pri].cpu().numpy(), "codes": codes[:c1p - c0p][pri].cpu().numpy(),
+               "keys": (keys_bufs[(step_no[0] - 1) % len(keys_bufs)][:, c0p + pri].cpu().numpy().view(np.uint64)
+                        if Kobj is not None else None),
+               "proj": fl.fastlsh_project(P, X[c0p:c1p][pri].contiguous()).cpu().numpy()}
 
-    # bucket tables of this rank's keys: stable radix sort of
-    # (key, id) per table + bucket starts — timed separately, not part of the hashing step
+    # side measurement: keys only (codes never leave the SM; K1j / K1r code tile), same chunks
+    keys_only = None
+    if Kobj is not None and (jit or info["kernel"] == 3):
+        try:
+            kk = keys_bufs[0]
+            for _ in range(2):
+                for c0, c1 in bounds:
+                    fl.hash_keys(P, Kobj, X[c0:c1], keys_out=kk, with_codes=False, col0=c0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 5))
+            e0.record(stream)
+            for _ in range(reps):
+                for c0, c1 in bounds:
+                    fl.hash_keys(P, Kobj, X[c0:c1], keys_out=kk, with_codes=False, col0=c0)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = e0.elapsed_time(e1) / reps
+            keys_only = {"ms_per_step": t_ms, "value": N * cfg.k / (t_ms / 1e3), "unit": "hashes/s",
+                         "roofline": {k: v for k, v in _roofline(cfg, info, True, N, t_ms / 1e3, t_ms, peaks,
+                                                                  with_codes=False).items()
+                                      if k in ("bound", "achieved", "peak", "unit", "frac", "north_star_frac")},
+                         "note": "hash + keys with codes kept on chip (fastlsh_hash_keys, codes=NULL), rank-local; "
+                                 "not the headline step (which also stores every code)"}
+        except Exception as ex:  # noqa: BLE001
+            keys_only = {"error": str(ex)}
+
+    # bucket tables of this rank's keys — timed separately, per-GPU
+    # workloads only (C3's 16 x 2e8 entries would need ~100 GB of sort workspace on one GPU)
     tables = None
-    if Kobj is not None and not args.no_tables:
-        ws = None
-        out_t = None
+    if Kobj is not None and not args.no_tables and not strong:
         try:
             out_t = fl.build_tables(keys)
-            need = out_t  # allocate once, then time re-builds into the same buffers
             t_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             torch.cuda.synchronize()
             t_ev[0].record(stream)
             for _ in range(3):
-                fl.build_tables(keys, out=out_t, workspace=ws)
+                fl.build_tables(keys, out=out_t)
             t_ev[1].record(stream)
             torch.cuda.synchronize()
             tms = t_ev[0].elapsed_time(t_ev[1]) / 3
@@ -422,14 +505,15 @@ def main():
                       "buckets_table0": int(out_t[3][0].item()),
                       "hbm_bytes_algorithmic": entries * (8 * 8 + 8 * 24 + 8 + 4),
                       "note": "8 LSD radix passes (hist 8 B + scatter 12 B in / 12 B out per entry) + bucket starts"}
-            tables["hbm_frac"] = tables["hbm_bytes_algorithmic"] / (tms / 1e3) / (_peaks()["hbm_gbs"] * 1e9)
-            del out_t, need
+            tables["hbm_frac"] = tables["hbm_bytes_algorithmic"] / (tms / 1e3) / (peaks["hbm_gbs"] * 1e9)
+            del out_t
         except Exception as ex:  # noqa: BLE001 (report, never hide a failure)
             tables = {"error": str(ex)}
+    elif strong:
+        tables = {"skipped": "C3: per-GPU table build of 16 x N entries not run (sort workspace); "
+                             "measured on C1 (python bench.py --config C1)"}
 
-    # queries: fresh rows of the same distribution are hashed,
-    # keyed and answered against the tables (exact re-ranking, top-10); recall@10 against exact
-    # nearest neighbours on a 100-query sample (rank 0). Timed separately from the hashing step.
+    # queries, per-GPU workloads only, rank 0
     queries = None
     if Kobj is not None and not args.no_tables and not strong and rank == 0:
         try:
@@ -453,7 +537,6 @@ def main():
             qms = q0.elapsed_time(q1)
             qids = res[0].cpu().numpy()
             ncand = res[2].double().cpu().numpy()
-            # exact 10-NN of the first 100 queries (fp64 on the host) for recall@10
             ns = min(100, nq)
             Xh64 = X.cpu().numpy()
             Qh = Qd[:ns].cpu().numpy().astype(np.float64)
@@ -476,10 +559,11 @@ def main():
     # on-box comparator: the dense E2LSH GEMM (tcgen05, m = n) on the same rows, k and w
     dense = None
     if not args.no_dense:
-        Pd = fl.Params.e2lsh(cfg.n, cfg.k, cfg.w, seed=cfg.seed)
+        Pd = fl.Params.e2lsh(cfg.n, cfg.k, cfg.w, seed=cfg.seed).set_kernel("smem")
         dense = {}
-        Nd = min(N, chunk)  # C3: the comparator runs on one chunk of rows
+        Nd = min(N, chunk)
         Xd, cd = X[:Nd], codes[:Nd]
+        t_codes = statistics.mean(full) / chunk  # FastLSH ms per row (the headline launch)
         for prec in (3, 1):
             fl.e2lsh_hash(Pd, Xd, out=cd, precision=prec)
             d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -493,9 +577,10 @@ def main():
             kpad = (cfg.k + 255) // 256 * 256
             dense[f"tf32x{prec}"] = {"ms": ms, "rows": Nd, "hashes_per_s": Nd * cfg.k / (ms / 1e3),
                                      "mma_tflops": 2.0 * Nd * cfg.n * kpad * prec / (ms / 1e3) / 1e12,
-                                     "fastlsh_hash_speedup": (ms / Nd) / (statistics.mean(hash_ms) / N)}
-        dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows; tf32x3 is the "
-                         "parity-gated comparator (3xTF32), tf32x1 the ungated reference point")
+                                     "fastlsh_speedup": (ms / Nd) / t_codes}
+        dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows (codes only); tf32x3 is the "
+                         "parity-gated comparator (3xTF32), tf32x1 the ungated reference point; speedup vs the "
+                         "headline FastLSH launch per row (which also builds the keys)")
         del Pd
 
     # end to end through the public host-buffer API: H2D of X, hash + keys, D2H of codes + keys
@@ -504,12 +589,12 @@ def main():
     Xh = X[:Ne].cpu().pin_memory()
     codes_h = torch.empty((Ne, cfg.k), dtype=torch.int32).pin_memory()
     keys_h = torch.empty((cfg.L, Ne), dtype=torch.int64).pin_memory() if Kobj else None
-    fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=131072)  # warm (workspace allocation)
+    fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=262144)  # warm (workspace allocation)
     if world > 1:
         dist.barrier()
     te = time.perf_counter()
     for _ in range(args.e2e_steps):
-        fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=131072)
+        fl.hash_host(P, Kobj, Xh, codes_h, keys_h, chunk_rows=262144)
     e2e_s = (time.perf_counter() - te) / args.e2e_steps
     et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -518,29 +603,57 @@ def main():
            "h2d_bytes_per_step": int(Xh.numel() * 4),
            "d2h_bytes_per_step": int(codes_h.numel() * 4 + (keys_h.numel() * 8 if keys_h is not None else 0)),
            "api": "fastlsh_hash_host (pinned host buffers, 2-stream chunked pipeline)", "steps": args.e2e_steps,
-           "rows_per_gpu": Ne}
+           "rows_per_gpu": Ne, "pcie_gbs": (Xh.numel() * 4 + codes_h.numel() * 4 +
+                                            (keys_h.numel() * 8 if keys_h is not None else 0)) / float(et[0]) / 1e9}
     del Xh, codes_h, keys_h
 
-    cb = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(cfg)
-        cb.pop("seconds", None)
+    # CPU leg (rank 0, N = 1 only): the oracle timed on the host cores, and the parity of sampled rows
+    # of the timed step's own output (the last chunk's codes, the keys of those rows) vs the oracle
+    cb, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        try:
+            import oracle
+            from fastlsh_inputs import fastlsh_arrays, philox
+            from oracle import keys as okeys
+            from parity import stats
+            idx, a, b = fastlsh_arrays(cfg.n, cfg.m, cfg.k, cfg.w, cfg.seed)
+            p, s, code = oracle.fastlsh(psample["X"], idx, a, b, cfg.w, threads=_cores())
+            cg, pg, kg, kr = psample["codes"], psample["proj"], psample["keys"], None
+            if Kobj is not None:
+                kr = okeys.build_keys(cg.astype(np.int64), philox.key_multipliers(cfg.L, cfg.K, cfg.seed), cfg.L, cfg.K)
+            parity = stats(cg, pg, p, s, code, b, cfg.w, kg, kr)
+            parity["sample"] = (f"{len(prow)} rows of the last chunk of the timed step (its codes and keys); "
+                                "projections re-run on the same rows; oracle/fastlsh_oracle.c in double")
+        except Exception as ex:  # noqa: BLE001
+            parity = {"error": str(ex)}
+        if world == 1:
+            try:
+                cb = cpu_baseline(cfg)
+                cb.pop("seconds", None)
+            except Exception as ex:  # noqa: BLE001
+                cb = {"error": str(ex)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "hashes/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, resident in HBM)",
-                "config": _config_dict(cfg, world, N, N_total, len(bounds)), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-                "gpu_launches": launches_per_step * args.steps,
+                "config": _config_dict(cfg, world, N, N_total, len(bounds), strong), "roofline": roofline,
+                "cpu_baseline": cb, "e2e": e2e, "parity": parity,
+                "gpu_launches": len(bounds) * args.steps * lpc,
                 "clocks": clocks,
-                "keys_fused": "K1 epilogue" if fused_keys else "K1r code tile" if rows_fused else False,
-                "keys_from_code_tile": tile_keys,
-                "breakdown_ms": {"hash": statistics.mean(hash_ms), "keys": statistics.mean(keys_ms),
+                "step": ("per chunk one K1j launch (fastlsh_hash_keys): X read, codes + keys written" if jit and Kobj
+                         else "per chunk fastlsh_hash_keys (kernel as in roofline.kernel)") +
+                        (f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})"
+                         if world > 1 else ""),
+                "keys_only": keys_only,
+                "breakdown_ms": {"hash_keys": statistics.mean(hash_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
-                                 "hash_max_over_ranks": hash_ms_max},
+                                 "hash_keys_max_over_ranks": hash_ms_max},
+                "jit_prepare_s": prep_s,
                 "dense_e2lsh": dense, "tables": tables, "queries": queries,
-                "packing": _packing_summary(P, info, fused_keys)}
+                "packing": _packing_summary(P, info)}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

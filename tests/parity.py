@@ -48,3 +48,30 @@ def check_codes(codes_gpu, p, scale, code_oracle, b, w):
     if out_of_range.any():
         assert (codes_gpu[out_of_range] == INT32_MIN).all()
     return float(ambig.mean()) if ambig.size else 0.0
+
+
+def stats(codes_gpu, proj_gpu, p, scale, code_oracle, b, w, keys_gpu=None, keys_ref=None):
+    """The per-config parity record of BASELINE.md §3 / VERDICT r1 item 1, on one row sample:
+    max relative projection error (vs ||a|| ||S(v)||), ambiguous fraction (oracle projection inside
+    the band of DESIGN.md R5), code mismatches outside the band (must be 0), codes outside their
+    band, sentinel mismatches, and key mismatches given the GPU's codes (must be 0)."""
+    codes_gpu = np.asarray(codes_gpu, np.int64)
+    b = np.asarray(b, np.float64)
+    lo, hi = expected_code_band(p, scale, b, w)
+    out_of_range = (code_oracle <= INT32_MIN) | (code_oracle > 2 ** 31 - 1)
+    ambig = (lo != hi) & ~out_of_range
+    exact = ~ambig & ~out_of_range
+    rec = {"rows": int(codes_gpu.shape[0]), "hashes": int(codes_gpu.size),
+           "ambiguous_frac": float(ambig.mean()) if ambig.size else 0.0,
+           "out_of_band_mismatches": int((exact & (codes_gpu != code_oracle)).sum()),
+           "in_band_outside_band": int((ambig & ((codes_gpu < lo) | (codes_gpu > hi))).sum()),
+           "in_band_differ_from_oracle": int((ambig & (codes_gpu != code_oracle)).sum()),
+           "sentinel_mismatches": int((out_of_range & (codes_gpu != INT32_MIN)).sum())}
+    if proj_gpu is not None:
+        err = np.abs(np.asarray(proj_gpu, np.float64) - p)
+        rel = err / np.maximum(scale, 1e-300)
+        rec["max_rel_proj_err"] = float(rel.max()) if rel.size else 0.0
+        rec["proj_outside_tol"] = int((err > 1e-5 * scale).sum())
+    if keys_gpu is not None:
+        rec["key_mismatches_given_codes"] = int((np.asarray(keys_gpu) != np.asarray(keys_ref)).sum())
+    return rec

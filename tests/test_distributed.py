@@ -33,39 +33,49 @@ def test_shard_rows_cover_and_balance():
         shard_rows(10, 2, 2)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, N):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from fastlsh_inputs import philox
         from oracle import keys as okeys
-        L, K, N = 5, 4, 12
+        L, K = 5, 4
         lo, hi = shard_rows(N, world, rank)
         rng = np.random.default_rng(0)
         codes = rng.integers(-50, 50, size=(N, L * K)).astype(np.int32)  # same on every rank
         r = philox.key_multipliers(L, K, seed=9)
         # each rank computes keys of its own rows (here with the exact oracle: host logic test)
         local = okeys.build_keys(codes[lo:hi], r, L, K).view(np.int64)
-        out = allgather_keys(torch.from_numpy(local.copy()))
+        out = allgather_keys(torch.from_numpy(local.copy()), n_total=N)
         full = okeys.build_keys(codes, r, L, K).view(np.int64)
         ok_layout = np.array_equal(out.numpy(), full)
-        # the bench's overlapped form: works returned unwaited, waited before the buffer is reused
-        out2 = torch.zeros_like(out)
-        works = allgather_keys(torch.from_numpy(local.copy()), out=out2, wait=False)
-        for w in works:
-            w.wait()
-        ok_layout = ok_layout and len(works) == L and np.array_equal(out2.numpy(), full)
+        if N % world == 0:
+            # the bench's overlapped form: works returned unwaited, waited before the buffer is reused
+            out2 = torch.zeros_like(out)
+            works = allgather_keys(torch.from_numpy(local.copy()), out=out2, wait=False)
+            for w in works:
+                w.wait()
+            ok_layout = ok_layout and len(works) == L and np.array_equal(out2.numpy(), full)
+        else:
+            try:
+                allgather_keys(torch.from_numpy(local.copy()), wait=False, n_total=N)
+                ok_layout = False  # unequal shards must refuse the unwaited form
+            except ValueError:
+                pass
         m = max_over_ranks(1.0 + rank)
         q.put((rank, ok_layout, m))
     finally:
         dist.destroy_process_group()
 
 
-def test_allgather_keys_layout_gloo_world2():
-    world, port = 2, _free_port()
+@pytest.mark.parametrize("world,N", [(2, 12), (3, 13), (3, 2)])
+def test_allgather_keys_layout_gloo(world, N):
+    """World sizes 2 and 3, equal and unequal shards (N % world != 0: sizes differ by one, and a
+    rank with no rows at all for N < world): the gathered [L][N] is the table-major global layout."""
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, N)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
@@ -74,4 +84,4 @@ def test_allgather_keys_layout_gloo_world2():
         assert p.exitcode == 0
     for rank, ok, m in res:
         assert ok, f"rank {rank}: gathered keys are not the table-major global layout"
-        assert m == 2.0
+        assert m == float(world)
