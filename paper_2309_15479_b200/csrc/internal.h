@@ -113,11 +113,16 @@ void build_row_packing(const fastlsh_params& p, RPacking& out);
 
 namespace jit {
 struct Module;  // a compiled K1j variant (jit.cpp)
-// K1j variants of one params object: (mode, L, K) -> module; compiled on first use
+// K1j variants of one params object: (mode, keys multipliers) -> module; compiled on first use
+struct Variant {
+    int mode = 0, L = 0, K = 0;
+    std::vector<uint64_t> r;  // key multipliers compiled into the module (empty: no keys)
+    std::shared_ptr<Module> mod;
+};
 struct State {
     std::mutex mu;
     int applicable = -1;  // -1 not decided yet
-    std::vector<std::pair<std::array<int, 3>, std::shared_ptr<Module>>> variants;
+    std::vector<Variant> variants;
     std::string last_error;
     double compile_seconds = 0;  // total NVRTC time spent for this params object
 };
@@ -256,6 +261,7 @@ struct Spec {
     const float* a;      // [k][m]
     const float* b;      // [k]
     int L, K;            // fused compound keys (L = 0: none)
+    const uint64_t* r;   // their multipliers [L][K+1] (compiled in as immediates)
     int warps, ncb;      // warps per CTA, code boxes per warp
     int mode;            // 0: codes (+ keys when L > 0), 1: projections
 };

@@ -115,15 +115,16 @@ __device__ __forceinline__ void bulk_wait_read_ring() { asm volatile("cp.async.b
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// one group of 32 outputs of the warp's tile -> swizzled box -> TMA tensor store
-__device__ __forceinline__ void store_group(const int (&cv)[32], unsigned char* cring, u32 cring_s, int& cbi, int lane,
-                                            u32 sw, const TMap* om, int g, long long t) {
-    if (lane == 0) bulk_wait_read_ring();  // the store that last read box cbi has read it
+// Codes leave in groups of 32 hashes: a swizzled 32 x 32 box of the warp's ring, written 4 codes
+// (one STS.128) at a time as they are produced, then one TMA tensor store per group.
+__device__ __forceinline__ void group_begin(int lane) {
+    if (lane == 0) bulk_wait_read_ring();  // the store that last read this ring box has read it
     __syncwarp();
-    unsigned char* dst = cring + cbi * 4096 + lane * 128;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<int4*>(dst + (((u32)q << 4) ^ sw)) = make_int4(cv[4 * q], cv[4 * q + 1], cv[4 * q + 2], cv[4 * q + 3]);
+}
+__device__ __forceinline__ void put4(unsigned char* box_lane, u32 q, u32 sw, int c0, int c1, int c2, int c3) {
+    *reinterpret_cast<int4*>(box_lane + ((q << 4) ^ sw)) = make_int4(c0, c1, c2, c3);
+}
+__device__ __forceinline__ void group_end(u32 cring_s, int& cbi, int lane, const TMap* om, int g, long long t) {
     fence_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -141,9 +142,9 @@ __device__ __noinline__ void fix_row(const JArgs& a, float* scr, long long row, 
     for (int i = lane; i < FL_K; i += 32) {
         const int* id = a.idx + (long long)i * FL_M;
         const float* co = a.a + (long long)i * FL_M;
-        float p = __fmul_rn(scr[id[0]], co[0]);
-        for (int j = 1; j < FL_M; ++j) p = __fmaf_rn(scr[id[j]], co[j], p);
-        const float q = FL_QUANT(__fadd_rn(p, a.b[i]));
+        float p = __fmul_rn(scr[id[0]], FL_COEF(co[0]));
+        for (int j = 1; j < FL_M; ++j) p = __fmaf_rn(scr[id[j]], FL_COEF(co[j]), p);
+        const float q = FL_Q(p, a.b[i]);
         int c = __float2int_rd(q);
         if (!(fabsf(q) < 2147483648.0f)) {
             c = (int)0x80000000;
@@ -249,21 +250,22 @@ std::string k1j_source(const Spec& s) {
         const char* dbg = std::getenv("FASTLSH_JIT_DEBUG");  // experiment knob (tools/dbg_keys*.py)
         def("FL_DEBUG", dbg ? std::atoi(dbg) : 0);
     }
+    // Quantisation: q = (p + b) / w. For w a power of two, 1/w is folded into the
+    // coefficients and b: every fp32 step then carries an exact power-of-two scale, so
+    // fma-chain(a/w) + b/w == RN(p + b) / w bit for bit (outside subnormal / overflow ranges) and the
+    // final multiply disappears. Otherwise IEEE division after the add, as in K1r.
     if (p2) {
-        src += "#define FL_QUANT(v) __fmul_rn((v), ";
+        src += "#define FL_COEF(c) __fmul_rn((c), ";
         add_float(src, 1.0f / s.w);
-        src += ")\n";
+        src += ")\n#define FL_Q(p, b) __fadd_rn((p), __fmul_rn((b), ";
+        add_float(src, 1.0f / s.w);
+        src += "))\n";
     } else {
-        src += "#define FL_QUANT(v) __fdiv_rn((v), ";
+        src += "#define FL_COEF(c) (c)\n#define FL_Q(p, b) __fdiv_rn(__fadd_rn((p), (b)), ";
         add_float(src, s.w);
         src += ")\n";
     }
     src += kPrelude;
-    if (s.L > 0) {
-        src += "struct KArgs { u32 limb[" + std::to_string(s.L * s.K * 3) + "]; u64 r0[" + std::to_string(s.L) + "]; };\n";
-    } else {
-        src += "struct KArgs { u32 unused; };\n";
-    }
 
     // One hash as one inline-PTX block: p in the paper's slot order with immediate coefficients,
     // then (codes) p + b, * 1/w or / w, floor. NVVM does not re-optimise asm: with plain C++
@@ -280,26 +282,34 @@ std::string k1j_source(const Spec& s) {
                 ops.push_back(id[t]);
             }
         const char* P = s.mode == 0 ? "%1" : "%0";  // register holding p (q is reused for p)
-        char buf[96];
-        std::string h = s.mode == 0 ? "            { float q; asm(\"" : "            { float p; asm(\"";
+        const float scale = (s.mode == 0 && p2) ? 1.0f / s.w : 1.0f;
+        char buf[112];
+        std::string h = s.mode == 0 ? "{ float q; asm(\"" : "{ float p; asm(\"";
         for (int t = 0; t < s.m; ++t) {
+            const float c = co[t] * scale;  // exact: power-of-two scale
             uint32_t u;
-            std::memcpy(&u, &co[t], 4);
+            std::memcpy(&u, &c, 4);
             if (t == 0)
                 std::snprintf(buf, sizeof buf, "mul.rn.f32 %s, %%%d, 0f%08X;", P, opnum[id[t]], u);
             else
                 std::snprintf(buf, sizeof buf, " fma.rn.f32 %s, %%%d, 0f%08X, %s;", P, opnum[id[t]], u, P);
             h += buf;
         }
+        const std::string cj = "c" + std::to_string(j & 3);
         if (s.mode == 0) {
             uint32_t ub, uw;
-            std::memcpy(&ub, &s.b[i], 4);
-            const float wq = p2 ? 1.0f / s.w : s.w;
-            std::memcpy(&uw, &wq, 4);
-            std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; %s.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;",
-                          ub, p2 ? "mul" : "div", uw);
+            if (p2) {
+                const float bs = s.b[i] * scale;
+                std::memcpy(&ub, &bs, 4);
+                std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;", ub);
+            } else {
+                std::memcpy(&ub, &s.b[i], 4);
+                std::memcpy(&uw, &s.w, 4);
+                std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; div.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;",
+                              ub, uw);
+            }
             h += buf;
-            h += "\" : \"=r\"(cv[" + std::to_string(j) + "]), \"=f\"(q) :";
+            h += "\" : \"=r\"(" + cj + "), \"=f\"(q) :";
         } else {
             h += "\" : \"=f\"(p) :";
         }
@@ -311,48 +321,52 @@ std::string k1j_source(const Spec& s) {
         if (s.mode == 0)
             h += " bad |= !(fabsf(q) < 2147483648.0f);";
         else
-            h += " cv[" + std::to_string(j) + "] = __float_as_int(p);";
-        return h;
+            h += " " + cj + " = __float_as_int(p);";
+        return h + " }";
     };
 
     const bool keys = s.mode == 0 && s.L > 0;
-    src += s.mode == 0 ? "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
-                         "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, "
-                         "const __grid_constant__ JArgs a, const __grid_constant__ KArgs ka) {\n"
-                       : "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
-                         "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, "
-                         "const __grid_constant__ JArgs a) {\n";
+    src += "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
+           "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, const __grid_constant__ JArgs a) {\n";
     src += kTileHead;
     if (s.mode == 0) src += "        bool bad = false;\n";
     if (keys) src += "        u64 s0 = 0, s1 = 0, s2 = 0;\n        const bool live = row < a.N;\n        u64* kp = a.keys + a.col0 + row;\n";
+    char buf[160];
     for (int g = 0; g < groups; ++g) {
-        src += "        {\n            int cv[32];\n";
-        for (int j = 0; j < 32; ++j) {
-            const int i = 32 * g + j;
-            if (i >= s.k) {
-                src += "            cv[" + std::to_string(j) + "] = 0;\n";
-                continue;
+        src += "        {\n            if (a.write_out) group_begin(lane);\n"
+               "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n";
+        for (int q = 0; q < 8 && 32 * g + 4 * q < s.k; ++q) {
+            src += "            { int c0, c1, c2, c3;\n";
+            for (int j = 4 * q; j < 4 * q + 4; ++j) {
+                const int i = 32 * g + j;
+                src += "              " + hash_asm(i, j);
+                if (keys && i < s.L * s.K) {
+                    // key term (R9): the three 21-bit limbs of r[l][jj+1] (instruction
+                    // immediates) times u32(code), exact 64-bit sums
+                    const int l = i / s.K, jj = i % s.K;
+                    const uint64_t r = s.r[(size_t)l * (s.K + 1) + jj + 1];
+                    std::snprintf(buf, sizeof buf,
+                                  " { const u64 u = (u32)c%d; s0 += 0x%llxull * u; s1 += 0x%llxull * u; s2 += 0x%llxull * u; }",
+                                  j & 3, (unsigned long long)(r & 0x1fffff), (unsigned long long)((r >> 21) & 0x1fffff),
+                                  (unsigned long long)(r >> 42));
+                    src += buf;
+                    // key = (r0 + S0 + S1*2^21 + S2*2^42) mod 2^61-1; for K < 256 every S_q < K*2^53 < 2^61-1
+                    // is already reduced, so only the final sum (< 2^63) needs a reduction
+                    if (jj == s.K - 1) {
+                        std::snprintf(buf, sizeof buf, "\n              { const u64 key = mod61(0x%llxull + ",
+                                      (unsigned long long)s.r[(size_t)l * (s.K + 1)]);
+                        src += buf;
+                        src += (s.K < 256 ? "s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
+                                          : "mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42)); ");
+                        src += "if (live && !(FL_DEBUG & 2)) kp[" + std::to_string(l) +
+                               "ll * a.ldk] = key; s0 = 0; s1 = 0; s2 = 0; }";
+                    }
+                }
+                src += "\n";
             }
-            src += hash_asm(i, j);
-            if (keys && i < s.L * s.K) {
-                // key term: three 21-bit limbs of r[l][jj+1] times u32(code), exact 64-bit sums
-                const int l = i / s.K, jj = i % s.K;
-                const int li = (l * s.K + jj) * 3;
-                src += " { const u32 u = (u32)cv[" + std::to_string(j) + "]; s0 += (u64)ka.limb[" + std::to_string(li) +
-                       "] * u; s1 += (u64)ka.limb[" + std::to_string(li + 1) + "] * u; s2 += (u64)ka.limb[" +
-                       std::to_string(li + 2) + "] * u; }";
-                // key = (r0 + S0 + S1*2^21 + S2*2^42) mod 2^61-1; for K < 256 every S_q < K*2^53 < 2^61-1
-                // is already reduced, so only the final sum (< 2^63) needs a reduction
-                if (jj == s.K - 1)
-                    src += "\n            { const u64 key = mod61(ka.r0[" + std::to_string(l) + "] + " +
-                           (s.K < 256 ? "s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
-                                      : "mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42)); ") +
-                           "if (live && !(FL_DEBUG & 2)) kp[" + std::to_string(l) + "ll * a.ldk] = key; s0 = 0; s1 = 0; s2 = 0; }";
-            }
-            src += " }\n";
+            src += "              if (a.write_out) put4(box, " + std::to_string(q) + "u, sw, c0, c1, c2, c3); }\n";
         }
-        src += "            if (a.write_out) store_group(cv, cring, cring_s, cbi, lane, sw, &omap, " + std::to_string(g) +
-               ", t);\n        }\n";
+        src += "            if (a.write_out) group_end(cring_s, cbi, lane, &omap, " + std::to_string(g) + ", t);\n        }\n";
     }
     if (s.mode == 0) {
         src += R"FL(
@@ -462,6 +476,7 @@ bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string
 }
 
 
+#ifndef FASTLSH_JIT_MAIN  // the standalone generator check below needs no CUDA runtime
 // ------------------------------------------------------------------------------------------
 // runtime: variants, module cache, tensor maps, launch
 // ------------------------------------------------------------------------------------------
@@ -537,38 +552,19 @@ int sm_count(int dev) {
     return cnt[dev];
 }
 
-// key multipliers as kernel-parameter operands: 21-bit limbs of r[l][j+1], then r[l][0]
-std::vector<unsigned char> key_args(const fastlsh_keys* ks) {
-    const int L = ks->L, K = ks->K;
-    const size_t limb_bytes = (size_t)L * K * 3 * 4;
-    const size_t r0_off = (limb_bytes + 7) / 8 * 8;
-    std::vector<unsigned char> buf(r0_off + (size_t)L * 8, 0);
-    uint32_t* limb = reinterpret_cast<uint32_t*>(buf.data());
-    for (int l = 0; l < L; ++l) {
-        for (int j = 0; j < K; ++j) {
-            const uint64_t r = ks->r[(size_t)l * (K + 1) + j + 1];
-            limb[(l * K + j) * 3 + 0] = (uint32_t)(r & 0x1fffff);
-            limb[(l * K + j) * 3 + 1] = (uint32_t)((r >> 21) & 0x1fffff);
-            limb[(l * K + j) * 3 + 2] = (uint32_t)(r >> 42);
-        }
-        const uint64_t r0 = ks->r[(size_t)l * (K + 1)];
-        std::memcpy(buf.data() + r0_off + 8 * l, &r0, 8);
-    }
-    return buf;
-}
-
 bool keys_fit(const fastlsh_params& p, const fastlsh_keys* ks) {
-    // kernel parameters <= 32 KB: two tensor maps, JArgs and the limbs
-    return (int64_t)ks->L * ks->K <= p.k && (size_t)ks->L * ks->K * 12 + (size_t)ks->L * 8 + 512 <= 31 * 1024;
+    return (int64_t)ks->L * ks->K <= p.k && ks->K <= 1024;  // K <= 1024: the 64-bit limb sums are exact
 }
 
-std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, int L, int K, fastlsh_status* st) {
+std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fastlsh_keys* ks, fastlsh_status* st) {
     State& js = p->jit;
     std::lock_guard<std::mutex> g(js.mu);
+    const int L = ks ? ks->L : 0, K = ks ? ks->K : 0;
     for (auto& v : js.variants)
-        if (v.first[0] == mode && v.first[1] == L && v.first[2] == K) return v.second;
+        if (v.mode == mode && v.L == L && v.K == K && (!ks || v.r == ks->r)) return v.mod;
     const int warps = warps_for(p->n);
-    Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), L, K, warps, kNcb, mode};
+    Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), L, K, ks ? ks->r.data() : nullptr,
+           warps, kNcb, mode};
     std::string src = k1j_source(s);
     std::shared_ptr<Module> mod;
     {
@@ -599,7 +595,13 @@ std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, int L, in
         std::lock_guard<std::mutex> gc(g_cache_mu);
         cache().emplace_back(std::move(src), mod);
     }
-    js.variants.push_back({{mode, L, K}, mod});
+    Variant v;
+    v.mode = mode;
+    v.L = L;
+    v.K = K;
+    if (ks) v.r = ks->r;
+    v.mod = mod;
+    js.variants.push_back(std::move(v));
     return mod;
 }
 
@@ -622,7 +624,7 @@ fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks
     if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
     if (ks && (mode != 0 || !keys_fit(*p, ks))) return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    return get_variant(p, mode, ks ? ks->L : 0, ks ? ks->K : 0, &st) ? FASTLSH_OK : st;
+    return get_variant(p, mode, ks, &st) ? FASTLSH_OK : st;
 }
 
 fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
@@ -638,7 +640,7 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
         N > (int64_t)0x7fffffff - 64)
         return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    std::shared_ptr<Module> mod = get_variant(p, mode, ks ? ks->L : 0, ks ? ks->K : 0, &st);
+    std::shared_ptr<Module> mod = get_variant(p, mode, ks, &st);
     if (!mod) return st;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -682,15 +684,16 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
     a.a = d.j_a;
     a.b = d.b;
     a.kr = dev_r;
-    std::vector<unsigned char> kargs = ks ? key_args(ks) : std::vector<unsigned char>(4, 0);
     const long long ctas_needed = (a.tiles + mod->warps - 1) / mod->warps;
     const int grid = (int)(ctas_needed < sm_count(dev) ? ctas_needed : sm_count(dev));
-    void* args[4] = {&xmap, &omap, &a, kargs.data()};
+    void* args[3] = {&xmap, &omap, &a};
     e = cudaLaunchKernel(reinterpret_cast<const void*>(mod->kern), dim3(grid), dim3(mod->warps * 32), args, mod->smem,
                          stream);
     if (e != cudaSuccess) return set_cuda_error(e);
     return FASTLSH_OK;
 }
+
+#endif  // FASTLSH_JIT_MAIN
 
 }  // namespace jit
 }  // namespace fastlsh
@@ -712,7 +715,10 @@ int main(int argc, char** argv) {
         }
         b[i] = fastlsh::draw_offset(1, i, w);
     }
-    fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, 8, 2, argc > 6 ? atoi(argv[6]) : 0};
+    std::vector<uint64_t> r((size_t)L * (K + 1));
+    for (int l = 0; l < L; ++l)
+        for (int j = 0; j <= K; ++j) r[(size_t)l * (K + 1) + j] = fastlsh::draw_key_multiplier(1, l, j);
+    fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, r.data(), 8, 2, argc > 6 ? atoi(argv[6]) : 0};
     const std::string src = fastlsh::jit::k1j_source(s);
     FILE* f = fopen("/tmp/k1j.cu", "w");
     fwrite(src.data(), 1, src.size(), f);
