@@ -449,6 +449,26 @@ def main():
         roofline["note"] = "the per-chunk time covers the hashing kernel and the key kernel (two launches)"
     roofline["launch_ms_min_max"] = [min(full), max(full)]
 
+    # the HBM ceiling of the dominant kernel's own traffic mix (a plain streaming kernel reading and
+    # writing the same bytes per row: roofline.mix_ceiling), on the same rows
+    if jit:
+        rb, wbytes = 4 * cfg.n, 4 * cfg.k + (8 * cfg.L if Kobj is not None else 0)
+        scratch = torch.empty((chunk * wbytes + 15) // 16 * 4, dtype=torch.int32, device=dev)
+        fl.bandwidth_probe(X, scratch, chunk, rb, wbytes)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(5):
+            fl.bandwidth_probe(X, scratch, chunk, rb, wbytes)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / 5
+        ceil_gbs = chunk * (rb + wbytes) / (pms / 1e3) / 1e9
+        roofline["mix_ceiling"] = {"gbs": ceil_gbs, "frac_of_ceiling": roofline["achieved"] / ceil_gbs,
+                                   "pattern": f"{rb} B read + {wbytes} B written per row, {chunk} rows, plain "
+                                              "16-byte vector stream (fastlsh_bandwidth_probe)",
+                                   "ms": pms}
+        del scratch
+
     # parity sample of the timed step's own output (the last chunk's codes, the keys of those rows),
     # copied out now, before any side measurement reuses the buffers; checked in the CPU leg below
     c0p, c1p = bounds[-1]

@@ -276,6 +276,13 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* keys, co
 fastlsh_status fastlsh_read_flags(const fastlsh_params* p, uint64_t* nonfinite,
                                   uint64_t* saturated, int32_t reset, fastlsh_stream_t stream);
 
+/* Diagnostic (probe.cu): a plain streaming kernel that reads read_bytes and writes write_bytes per
+ * row for `rows` rows (16-byte multiples; in / out 16-byte aligned device buffers of rows*read_bytes
+ * and rows*write_bytes; out receives junk). Timing it gives the HBM ceiling of a hashing kernel's
+ * own traffic mix, reported beside its roofline fraction (bench.py `roofline.mix_ceiling`). */
+fastlsh_status fastlsh_bandwidth_probe(const void* in, void* out, int64_t rows, int32_t read_bytes,
+                                       int32_t write_bytes, fastlsh_stream_t stream);
+
 const char* fastlsh_status_string(fastlsh_status s);
 const char* fastlsh_last_cuda_error(void); /* thread-local text of the last ECUDA */
 int32_t fastlsh_abi_version(void);         /* 1 */

@@ -27,7 +27,7 @@ EXPORTED = [
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables",
     "fastlsh_query_workspace", "fastlsh_query", "fastlsh_normalize_rows", "fastlsh_max_row_norm",
     "fastlsh_mips_transform", "fastlsh_hash_host", "fastlsh_read_flags",
-    "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
+    "fastlsh_bandwidth_probe", "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
 ]
 
 
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_query": [P, i64, i32, P, P, i32, P, P, i64, i64, i32, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_hash_host": [P, P, P, i64, P, P, i64],
         "fastlsh_read_flags": [P, P, P, i32, P],
+        "fastlsh_bandwidth_probe": [P, P, i64, i32, i32, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -579,3 +580,13 @@ def read_flags(params: Params, reset: bool = False, stream=None):
     _check(params._lib.fastlsh_read_flags(params._h, ctypes.byref(nf), ctypes.byref(sat), int(reset),
                                           _stream_ptr(stream)), "fastlsh_read_flags")
     return nf.value, sat.value
+
+
+def bandwidth_probe(inp, out, rows: int, read_bytes: int, write_bytes: int, stream=None):
+    """Diagnostic streaming kernel (fastlsh_bandwidth_probe): `rows` rows of read_bytes read from
+    `inp` and write_bytes written to `out` (CUDA tensors of at least rows * bytes)."""
+    lib = load_library()
+    if inp.numel() * inp.element_size() < rows * read_bytes or out.numel() * out.element_size() < rows * write_bytes:
+        raise ValueError("probe buffers too small")
+    _check(lib.fastlsh_bandwidth_probe(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), rows,
+                                       read_bytes, write_bytes, _stream_ptr(stream)), "fastlsh_bandwidth_probe")

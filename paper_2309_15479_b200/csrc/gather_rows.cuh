@@ -17,7 +17,8 @@
 //  * a5 quantise: __fadd_rn(p, b), IEEE division by w (an exact multiply when w is a power of two),
 //    floor toward -inf, INT32_MIN + a device counter for non-finite or out-of-range quotients.
 //    Codes go to a ring of NC shared-memory buffers (conflict-free: the hash in lane j is j mod
-//    32/P); D = NC-2 groups later every warp copies a share of the group's tile to global memory
+//    32/P); D groups later (D per stride class: kRClasses[].D in internal.h) every warp copies a
+//    share of the group's tile to global memory
 //    with coalesced 16-byte stores (no thread waits on a TMA store: a single flushing warp made the
 //    whole CTA run at its pace).
 //  * mbarriers only (no CTA barrier in the loop): stage full, code-buffer full/empty.
@@ -126,8 +127,8 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     constexpr int NC = kRClasses[CLS].NC;
     // A warp flushes its share of group j-D at iteration j: it waits for every warp to have written
     // group j-D (slack D), and buffer reuse waits for every warp's flush of group j-NC, done at its
-    // iteration j-NC+D (slack NC-D). D = NC/2 balances the two (measured: D = NC-2 left 1-2 groups of
-    // slack whatever NC, and C3's warps waited there 18% of the time).
+    // iteration j-NC+D (slack NC-D). D is set per stride class in kRClasses (internal.h) from
+    // measurements (D = NC-1 beat NC-2 and NC/2 on C1 / C2).
     constexpr int D = kRClasses[CLS].D;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t row_bytes = 4u * S;  // compile-time: row r of a stage is an immediate offset

@@ -12,6 +12,9 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "internal.h"
 
@@ -346,20 +349,40 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
     // TMA-staged path: rows 16-byte multiples, codes 16-byte aligned, every table owns >= 1 thread
     // (k % 32 == 0 puts every staged row on the same banks, so the lanes of one table read one bank:
     // C3, k = 256, measured 7.7 vs 2.3 ms — those shapes keep the register-batched kernel)
-    TmaKeysFn tk = (k % 4 == 0 && k % 32 != 0 && base % 16 == 0 && L <= kTKThreads &&
-                    !std::getenv("FASTLSH_KEYS_NO_TMA"))
+    static const bool no_tma = std::getenv("FASTLSH_KEYS_NO_TMA") != nullptr;  // experiment knob, read once
+    TmaKeysFn tk = (k % 4 == 0 && k % 32 != 0 && base % 16 == 0 && L <= kTKThreads && !no_tma)
                        ? tma_keys_for(K) : nullptr;
     if (tk) {
         int RB = (int)((56 * 1024) / ((long long)k * 4)) & ~7;  // ~56 KB per stage, multiple of 8 rows
         if (RB > 64) RB = 64;
         const size_t smem = (size_t)kTKStages * RB * k * 4 + kTKStages * 8;
         if (RB >= 8 && smem <= 227 * 1024) {
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(tk),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return set_cuda_error(e);
+            int dev = 0;
+            cudaError_t e = cudaGetDevice(&dev);
+            if (e != cudaSuccess || dev < 0 || dev >= kMaxDevices) return e != cudaSuccess ? set_cuda_error(e) : FASTLSH_EUNSUPPORTED;
+            // per device: SM count once, and the dynamic shared-memory opt-in once per kernel at the
+            // device maximum (every later launch needs <= that), instead of one attribute call per launch
+            static int sms_of[kMaxDevices] = {};
+            static std::mutex mu;
+            static std::vector<std::pair<const void*, int>> attr_done;
+            {
+                std::lock_guard<std::mutex> g(mu);
+                if (!sms_of[dev]) {
+                    int sms = 0;
+                    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                    if (e != cudaSuccess) return set_cuda_error(e);
+                    sms_of[dev] = sms;
+                }
+                const void* fn = reinterpret_cast<const void*>(tk);
+                bool done = false;
+                for (auto& d : attr_done) done |= d.first == fn && d.second == dev;
+                if (!done) {
+                    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                    if (e != cudaSuccess) return set_cuda_error(e);
+                    attr_done.push_back({fn, dev});
+                }
+            }
+            const int sms = sms_of[dev];
             long long blocks = (N + RB - 1) / RB;
             if (blocks > sms) blocks = sms;
             tk<<<(unsigned)blocks, kTKThreads, smem, stream>>>(dev_r, codes, N, k, L, out, ldk, RB);

@@ -75,3 +75,15 @@ def stats(codes_gpu, proj_gpu, p, scale, code_oracle, b, w, keys_gpu=None, keys_
     if keys_gpu is not None:
         rec["key_mismatches_given_codes"] = int((np.asarray(keys_gpu) != np.asarray(keys_ref)).sum())
     return rec
+
+
+def record(rec: dict):
+    """Append one parity record (JSON line) to $FASTLSH_PARITY_LOG when set (the GPU runs collect
+    them into profiles/r02_parity.jsonl)."""
+    import json
+    import os
+    path = os.environ.get("FASTLSH_PARITY_LOG")
+    if path:
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")

@@ -17,7 +17,7 @@ import oracle
 import paper_2309_15479_b200 as fl
 from fastlsh_inputs import configs, data, fastlsh_arrays, philox
 from oracle import keys as okeys
-from parity import check_codes, check_projections
+from parity import check_codes, check_projections, record, stats
 
 pytestmark = pytest.mark.gpu
 THREADS = max(1, min(16, len(os.sched_getaffinity(0))))
@@ -31,7 +31,7 @@ def _jit_params(n, m, k, w, seed=1):
     return P, idx, a, b
 
 
-def _check(P, idx, a, b, w, X, rows=None):
+def _check(P, idx, a, b, w, X, rows=None, tag=None):
     codes = fl.fastlsh_hash(P, X)
     proj = fl.fastlsh_project(P, X)
     torch.cuda.synchronize()
@@ -45,6 +45,10 @@ def _check(P, idx, a, b, w, X, rows=None):
     p, scale, code = oracle.fastlsh(Xh, idx, a, b, w, threads=THREADS)
     rel = check_projections(pg, p, scale)
     amb = check_codes(cg, p, scale, code, b, w)
+    if tag is not None:
+        rec = dict(tag, kernel="K1j", N=int(X.shape[0]), sampled=rows is not None)
+        rec.update(stats(cg, pg, p, scale, code, b, w))
+        record(rec)
     return rel, amb, codes
 
 
@@ -67,7 +71,7 @@ def test_jit_parity_configs(name, N):
     if N > 5000:
         rng = np.random.default_rng(3)
         rows = np.unique(np.concatenate([rng.choice(N, 1500, replace=False), [0, 31, 32, 33, N - 33, N - 1]]))
-    rel, amb, _ = _check(P, idx, a, b, c.w, X, rows)
+    rel, amb, _ = _check(P, idx, a, b, c.w, X, rows, tag={"config": name, "m": c.m, "test": "jit_pinned"})
     assert rel < 1e-6 and amb < 5e-3
 
 

@@ -14,7 +14,7 @@ import oracle
 import paper_2309_15479_b200 as fl
 from fastlsh_inputs import configs, data, fastlsh_arrays, e2lsh_arrays, philox
 from oracle import keys as okeys
-from parity import check_codes, check_projections
+from parity import check_codes, check_projections, record, stats
 
 pytestmark = pytest.mark.gpu
 THREADS = max(1, min(16, len(os.sched_getaffinity(0))))
@@ -25,21 +25,39 @@ def _params(n, m, k, w, seed=1):
     return fl.Params.from_arrays(n, w, idx, a, b), idx, a, b
 
 
-def _run_and_check(P, idx, a, b, w, X_dev, rows=None):
-    """Hash X_dev on the GPU; compare all rows (rows=None) or the given row sample with the oracle."""
-    codes = fl.fastlsh_hash(P, X_dev)
+def _run_and_check(P, idx, a, b, w, X_dev, rows=None, tag=None, keys=None):
+    """Hash X_dev on the GPU; compare all rows (rows=None) or the given row sample with the oracle.
+    With `tag` (a dict naming the config) the parity statistics are recorded (parity.record); with
+    `keys` the compound keys of the same launch are checked bit-exact against Python big integers
+    on the GPU's codes."""
+    if keys is not None:
+        codes, gkeys = fl.hash_keys(P, keys, X_dev)
+    else:
+        codes, gkeys = fl.fastlsh_hash(P, X_dev), None
     proj = fl.fastlsh_project(P, X_dev)
     torch.cuda.synchronize()
     if rows is None:
         Xh = X_dev.cpu().numpy()
         cg, pg = codes.cpu().numpy(), proj.cpu().numpy()
+        kg = gkeys.cpu().numpy().view(np.uint64) if gkeys is not None else None
     else:
         ri = torch.as_tensor(rows, device=X_dev.device)
         Xh = X_dev[ri].cpu().numpy()
         cg, pg = codes[ri].cpu().numpy(), proj[ri].cpu().numpy()
+        kg = gkeys[:, ri].cpu().numpy().view(np.uint64) if gkeys is not None else None
     p, scale, code = oracle.fastlsh(Xh, idx, a, b, w, threads=THREADS)
     rel = check_projections(pg, p, scale)
     amb = check_codes(cg, p, scale, code, b, w)
+    kr = None
+    if keys is not None:
+        kr = okeys.build_keys(cg.astype(np.int64), keys.export(), keys.L, keys.K)
+        assert np.array_equal(kg, kr), "keys differ from big-integer keys on the GPU's codes"
+    if tag is not None:
+        rec = dict(tag)
+        rec.update(kernel=fl.Params.KERNELS.get(P.info()["kernel"], "?"), N=int(X_dev.shape[0]),
+                   sampled=rows is not None)
+        rec.update(stats(cg, pg, p, scale, code, b, w, kg, kr))
+        record(rec)
     return rel, amb, codes
 
 
@@ -56,7 +74,8 @@ def test_c0_full_parity():
     c = configs.get("C0")
     P, idx, a, b = _params(c.n, c.m, c.k, c.w, c.seed)
     X = data.generate(c.data, c.n, 0, c.N, seed=c.seed, device="cuda")
-    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X)
+    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X, tag={"config": "C0", "m": c.m, "test": "full"},
+                                 keys=fl.Keys.create(4, 16, seed=1))
     assert rel < 1e-6
     assert amb < 5e-3
 
@@ -73,11 +92,13 @@ def test_small_full_parity(name, m, N):
     m = m or c.m
     P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
     X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
-    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1) if c.L else None
+    rel, amb, _ = _run_and_check(P, idx, a, b, c.w, X, tag={"config": name, "m": m, "test": "small_all_rows"}, keys=Kobj)
     assert amb < 1e-2
 
 
-FULL = [("C1", None, None, 2048), ("C2", 32, None, 1024), ("C2", 4096, None, 64), ("C3", None, 4_000_000, 2048),
+FULL = [("C1", None, None, 2048), ("C2", 32, None, 1024), ("C2", 128, None, 1024), ("C2", 512, None, 512),
+        ("C2", 4096, None, 256), ("C3", None, 4_000_000, 2048),
         ("C4", None, None, 2048)]
 
 
@@ -91,7 +112,8 @@ def test_full_size_sampled_parity(name, m, N, sample):
     P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
     X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
     rows = _sample_rows(N, sample, seed=7, extra=[N // 2, N - 2, 4 * (N // 8) - 1])
-    _run_and_check(P, idx, a, b, c.w, X, rows=rows)
+    Kobj = fl.Keys.create(c.L, c.K, seed=1) if c.L else None
+    _run_and_check(P, idx, a, b, c.w, X, rows=rows, tag={"config": name, "m": m, "test": "full_size_sampled"}, keys=Kobj)
     del X
     torch.cuda.empty_cache()
 
@@ -457,18 +479,35 @@ def test_tables_empty():
 
 # ---- query with exact re-ranking (R16) ----------------------------------
 
-def _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o):
+def _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o, X, Q, cands):
+    """GPU query result vs the oracle's (R16), checked on its own terms:
+    every returned id is a distinct member of the query's candidate set, its reported distance is its
+    true squared distance (recomputed here in fp64 from X and Q), the list is ordered by (distance,
+    id), and where the GPU's id at a rank differs from the oracle's, its TRUE distance ties the
+    oracle's distance at that rank within the fp32 tolerance (a near-tie may swap ids, never admit a
+    farther point)."""
     ids_g, d_g, nc_g = ids_g.cpu().numpy(), d_g.cpu().numpy().astype(np.float64), nc_g.cpu().numpy()
+    X = np.asarray(X, np.float64)
+    Q = np.asarray(Q, np.float64)
     assert np.array_equal(nc_g, nc_o)  # the distinct candidate counts are integers: exact
     assert np.array_equal(ids_g < 0, ids_o < 0)
-    tol = 1e-5 * np.maximum(1.0, np.abs(d_o))  # fp32 distance vs the double oracle
-    live = ids_o >= 0
-    assert (np.abs(d_g[live] - d_o[live]) <= tol[live]).all()
-    # ids may differ only where the oracle's distances are tied within that tolerance
-    for q in range(ids_o.shape[0]):
-        for r in np.flatnonzero((ids_g[q] != ids_o[q]) & live[q]):
-            near = np.abs(d_o[q] - d_o[q, r]) <= 2 * tol[q, r]
-            assert ids_g[q, r] in set(ids_o[q][near].tolist()) or r >= 1 and near[-1], (q, r)
+    assert np.isinf(d_g[ids_g < 0]).all()
+    tol = 1e-5 * np.maximum(1.0, np.abs(np.where(np.isfinite(d_o), d_o, 0.0)))  # fp32 vs double
+    for q in range(ids_g.shape[0]):
+        live = ids_g[q] >= 0
+        got = ids_g[q][live].astype(np.int64)
+        assert len(set(got.tolist())) == len(got), f"query {q}: duplicated ids {got}"
+        assert set(got.tolist()) <= cands[q], f"query {q}: ids outside the candidate set"
+        true = ((X[got] - Q[q]) ** 2).sum(1)
+        assert (np.abs(d_g[q][live] - true) <= tol[q][live]).all(), f"query {q}: reported != true distance"
+        # ordered by (distance, id): non-decreasing distances, ids ascending among equal distances
+        dg = d_g[q][live]
+        assert (np.diff(dg) >= 0).all(), f"query {q}: distances not sorted"
+        for r in range(len(got) - 1):
+            if dg[r] == dg[r + 1]:
+                assert got[r] < got[r + 1], f"query {q}: equal distances not ordered by id"
+        for r in np.flatnonzero(got != ids_o[q][live]):
+            assert abs(true[r] - d_o[q, r]) <= 2 * tol[q, r], (q, r, true[r], d_o[q, r])
 
 
 @pytest.mark.parametrize("n,N,k,m,w,L,K,topk", [(64, 6000, 24, 8, 2.0, 6, 4, 10), (128, 3000, 16, 16, 8.0, 4, 4, 32),
@@ -492,7 +531,8 @@ def test_query_matches_oracle(n, N, k, m, w, L, K, topk):
     ids_o, d_o, nc_o = oq.query(X.numpy(), Q.numpy(), sk, si, qkeys_o, topk)
     tables = fl.build_tables(torch.as_tensor(keys_o.view(np.int64)).cuda())
     ids_g, d_g, nc_g = fl.query(X.cuda(), tables, Q.cuda(), torch.as_tensor(qkeys_o.view(np.int64)).cuda(), topk)
-    _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o)
+    cands = [oq.candidates_brute(keys_o, qkeys_o, q) for q in range(Q.shape[0])]
+    _check_query(ids_g, d_g, nc_g, ids_o, d_o, nc_o, X.numpy(), Q.numpy(), cands)
     assert (ids_g.cpu().numpy()[:Qn, 0] >= 0).all()
 
 
