@@ -297,6 +297,9 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem"],
                     help="pin the hashing kernel (auto: K1j for n <= 128, else K1r)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl"],
+                    help="N > 1 key all-gather: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
+                         "multicast table (fused), nccl = all_gather_into_tensor after hashing; auto tries nvls")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1: wait for each step's key all-gather before the next step hashes")
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk (launch)")
@@ -356,10 +359,21 @@ def main():
     X = data.generate(cfg.data, cfg.n, lo, hi, seed=cfg.seed, device=dev)
     codes = torch.empty((chunk, cfg.k), dtype=torch.int32, device=dev)
     keys = torch.empty((cfg.L, N), dtype=torch.int64, device=dev) if Kobj else None
-    gathered = torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev) if (Kobj and world > 1) else None
-    # N > 1: the key all-gather of step j runs on NCCL's stream while step j+1 hashes into the other
-    # keys buffer (double-buffered); step j+1 waits for it before launching its own all-gather
-    overlap = gathered is not None and not args.no_overlap
+    # N > 1, K1j: the keys go straight into every GPU's copy of the [L][N_total] table with multimem
+    # stores from the hashing kernel (NVSwitch multicast, torch symmetric memory); finishing the
+    # all-gather is one group barrier. Otherwise (no multicast / not K1j): NCCL all-gather, where the
+    # all-gather of step j runs on NCCL's stream while step j+1 hashes into the other keys buffer
+    # (double-buffered); step j+1 waits for it before launching its own all-gather.
+    ktable = None
+    if Kobj and world > 1 and jit and args.exchange != "nccl":
+        from paper_2309_15479_b200.distributed import KeyTable
+        ktable = KeyTable(cfg.L, N_total, device=dev, mode=args.exchange)
+        if ktable.mode != "nvls":
+            ktable = None
+    nvls = ktable is not None
+    gathered = (ktable.table if nvls else torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev)) \
+        if (Kobj and world > 1) else None
+    overlap = gathered is not None and not nvls and not args.no_overlap
     keys_bufs = [keys, torch.empty_like(keys)] if overlap else [keys]
     pending = []
     step_no = [0]
@@ -375,7 +389,9 @@ def main():
             if record:
                 e[0].record(stream)
             cb = codes[:c1 - c0]
-            if Kobj is not None:
+            if nvls:
+                fl.hash_keys_multicast(P, Kobj, X[c0:c1], ktable.multicast_ptr, N_total, lo + c0, codes=cb)
+            elif Kobj is not None:
                 fl.hash_keys(P, Kobj, X[c0:c1], codes=cb, keys_out=kb, col0=c0)
             else:
                 fl.fastlsh_hash(P, X[c0:c1], out=cb)
@@ -385,7 +401,9 @@ def main():
         ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if record else None
         if record:
             ea[0].record(stream)
-        if gathered is not None:
+        if nvls:
+            ktable.handle.barrier()  # every rank's multicast key stores are complete and visible
+        elif gathered is not None:
             if overlap:
                 for w in pending:
                     w.wait()
@@ -475,8 +493,8 @@ def main():
     prow = _sample_rows(c1p - c0p, 512, seed=11, extra=[1, 31, 32, 33, (c1p - c0p) // 2])
     pri = torch.as_tensor(prow, device=dev)
     psample = {"X": X[c0p:c1p][pri].cpu().numpy(), "codes": codes[:c1p - c0p][pri].cpu().numpy(),
-               "keys": (keys_bufs[(step_no[0] - 1) % len(keys_bufs)][:, c0p + pri].cpu().numpy().view(np.uint64)
-                        if Kobj is not None else None),
+               "keys": ((gathered[:, lo + c0p + pri] if nvls else keys_bufs[(step_no[0] - 1) % len(keys_bufs)][:, c0p + pri])
+                        .cpu().numpy().view(np.uint64) if Kobj is not None else None),
                "proj": fl.fastlsh_project(P, X[c0p:c1p][pri].contiguous()).cpu().numpy()}
 
     # side measurement: keys only (codes never leave the SM; K1j / K1r code tile), same chunks
@@ -665,8 +683,11 @@ def main():
                 "clocks": clocks,
                 "step": ("per chunk one K1j launch (fastlsh_hash_keys): X read, codes + keys written" if jit and Kobj
                          else "per chunk fastlsh_hash_keys (kernel as in roofline.kernel)") +
-                        (f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})"
+                        ((f"; keys written by K1j with multimem.st into every GPU's copy of the [L][N] table "
+                          f"(NVSwitch multicast, symmetric memory), then one group barrier" if nvls else
+                          f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
+                "key_exchange": ("nvls" if nvls else "nccl") if world > 1 and Kobj else None,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash_keys": statistics.mean(hash_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,

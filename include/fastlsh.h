@@ -23,6 +23,7 @@
 #ifndef FASTLSH_H
 #define FASTLSH_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -267,6 +268,27 @@ fastlsh_status fastlsh_mips_transform(const float* X, int64_t N, int32_t n, cons
 fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* keys, const float* X_host,
                                  int64_t N, int32_t* codes_host, uint64_t* keys_host,
                                  int64_t chunk_rows);
+
+/* Hash + keys with the key all-gather fused into the hashing kernel (a8): as
+ * fastlsh_hash_keys, but `keys_mc` is the MULTICAST device address (NVSwitch / NVLS, e.g. torch
+ * symmetric memory's multicast_ptr) of a [L][ldk] u64 table replicated on every GPU of the group,
+ * already offset to this call's first column (global row offset of the rank's chunk). Every key is
+ * written with multimem.st, so each GPU's copy of the table receives it; a group barrier after the
+ * launches (on every rank) completes the all-gather. codes may be NULL (keys only). K1j only:
+ * EUNSUPPORTED when the params are served by another kernel (use fastlsh_hash_keys + an NCCL
+ * all-gather then). */
+fastlsh_status fastlsh_hash_keys_multicast(const fastlsh_params* p, const fastlsh_keys* keys, const float* X,
+                                           int64_t N, int32_t* codes, uint64_t* keys_mc, int64_t ldk,
+                                           fastlsh_stream_t stream);
+
+/* NVLS multicast table for the CURRENT device alone (mc.cpp): `bytes` of device memory mapped twice —
+ * a unicast address (ordinary loads/stores, *unicast_ptr) and the address of an NVSwitch multicast
+ * object bound to it (*multicast_ptr, for multimem.st, e.g. fastlsh_hash_keys_multicast). In a
+ * multi-GPU job the multicast table comes from torch symmetric memory instead; this single-device
+ * form lets the multimem path be exercised on one GPU. EUNSUPPORTED when the device or driver offers
+ * no multicast (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, fabric). Release with fastlsh_multicast_free. */
+fastlsh_status fastlsh_multicast_alloc(size_t bytes, void** unicast_ptr, void** multicast_ptr, void** handle);
+void fastlsh_multicast_free(void* handle);
 
 /* ---- flags / errors --------------------------------------------------------------------------- */
 

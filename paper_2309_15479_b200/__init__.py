@@ -24,10 +24,11 @@ EXPORTED = [
     "fastlsh_params_prepare", "fastlsh_params_jit_status",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
-    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_tables_workspace", "fastlsh_build_tables",
+    "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_keys_multicast", "fastlsh_tables_workspace",
+    "fastlsh_build_tables",
     "fastlsh_query_workspace", "fastlsh_query", "fastlsh_normalize_rows", "fastlsh_max_row_norm",
     "fastlsh_mips_transform", "fastlsh_hash_host", "fastlsh_read_flags",
-    "fastlsh_bandwidth_probe", "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
+    "fastlsh_bandwidth_probe", "fastlsh_multicast_alloc", "fastlsh_multicast_free", "fastlsh_status_string", "fastlsh_last_cuda_error", "fastlsh_abi_version",
 ]
 
 
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_keys_export": [P, P],
         "fastlsh_build_keys": [P, P, i64, i32, P, i64, P],
         "fastlsh_hash_keys": [P, P, P, i64, P, P, i64, P],
+        "fastlsh_hash_keys_multicast": [P, P, P, i64, P, P, i64, P],
         "fastlsh_tables_workspace": [i32, i64, ctypes.POINTER(ctypes.c_size_t)],
         "fastlsh_build_tables": [P, i32, i64, i64, P, P, P, P, P, ctypes.c_size_t, P],
         "fastlsh_query_workspace": [i64, i64, ctypes.POINTER(ctypes.c_size_t)],
@@ -101,6 +103,10 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
+    lib.fastlsh_multicast_alloc.argtypes = [ctypes.c_size_t, PP, PP, PP]
+    lib.fastlsh_multicast_alloc.restype = ctypes.c_int
+    lib.fastlsh_multicast_free.argtypes = [P]
+    lib.fastlsh_multicast_free.restype = None
     lib.fastlsh_params_destroy.argtypes = [P]
     lib.fastlsh_params_destroy.restype = None
     lib.fastlsh_keys_destroy.argtypes = [P]
@@ -541,6 +547,30 @@ def hash_keys(params: Params, keys: Keys | None, X, codes=None, keys_out=None, s
     return codes, keys_out
 
 
+def hash_keys_multicast(params: Params, keys: Keys, X, mc_ptr: int, ldk: int, col0: int = 0, codes=None,
+                        with_codes: bool = True, stream=None):
+    """Hash + keys with the key all-gather fused in (fastlsh_hash_keys_multicast): the keys of X's rows
+    are written with multimem.st to columns [col0, col0 + N) of the [L, ldk] u64 table whose multicast
+    address is mc_ptr (torch symmetric memory), i.e. into every GPU's copy of the table. K1j only."""
+    import torch
+    params._ready()
+    _check_X(params, X)
+    N = X.shape[0]
+    if keys.L * keys.K > params.k:
+        raise ValueError(f"keys need L*K={keys.L * keys.K} <= k={params.k} codes")
+    if col0 < 0 or col0 + N > ldk or not mc_ptr:
+        raise ValueError("need a multicast pointer and col0 + N <= ldk")
+    if with_codes and codes is None:
+        codes = torch.empty((N, params.k), dtype=torch.int32, device=X.device)
+    if codes is not None:
+        _check_out(codes, N, params.k, "codes")
+    cp = _dev_ptr(codes, torch.int32, "codes") if codes is not None else ctypes.c_void_p(0)
+    _check(params._lib.fastlsh_hash_keys_multicast(params._h, keys._h, _dev_ptr(X, torch.float32, "X"), N, cp,
+                                                   ctypes.c_void_p(int(mc_ptr) + 8 * col0), ldk, _stream_ptr(stream)),
+           "fastlsh_hash_keys_multicast")
+    return codes
+
+
 def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_host=None,
               chunk_rows: int = 65536):
     """End-to-end entry point on HOST buffers (numpy or pinned torch CPU tensors)."""
@@ -590,3 +620,36 @@ def bandwidth_probe(inp, out, rows: int, read_bytes: int, write_bytes: int, stre
         raise ValueError("probe buffers too small")
     _check(lib.fastlsh_bandwidth_probe(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), rows,
                                        read_bytes, write_bytes, _stream_ptr(stream)), "fastlsh_bandwidth_probe")
+
+
+class MulticastTable:
+    """An [L, ldk] int64 table on the current GPU mapped both normally (`table`, a torch view) and
+    through an NVSwitch multicast object (`mc_ptr`, for fastlsh_hash_keys_multicast):
+    fastlsh_multicast_alloc. Raises FastLSHError(EUNSUPPORTED) where multicast is unavailable."""
+
+    def __init__(self, L: int, ldk: int):
+        import torch
+        lib = load_library()
+        self._lib = lib
+        uc, mc, h = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib.fastlsh_multicast_alloc(L * ldk * 8, ctypes.byref(uc), ctypes.byref(mc), ctypes.byref(h)),
+               "fastlsh_multicast_alloc")
+        self._h = h
+        self.mc_ptr = mc.value
+
+        class _Arr:  # zero-copy torch view of the unicast mapping
+            __cuda_array_interface__ = {"shape": (L, ldk), "typestr": "<i8", "data": (uc.value, False),
+                                        "version": 3, "strides": None}
+        self.table = torch.as_tensor(_Arr(), device="cuda")
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            self.table = None
+            self._lib.fastlsh_multicast_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -684,6 +684,23 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
 }
 
+fastlsh_status fastlsh_hash_keys_multicast(const fastlsh_params* p, const fastlsh_keys* ks, const float* X,
+                                           int64_t N, int32_t* codes, uint64_t* keys_mc, int64_t ldk,
+                                           fastlsh_stream_t stream) {
+    if (!p || !ks || N < 0 || (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
+    if (N == 0) return FASTLSH_OK;
+    if (!X || !keys_mc || ldk < N || (reinterpret_cast<uintptr_t>(keys_mc) & 7)) return FASTLSH_EINVAL;
+    int dev = 0;
+    fastlsh_status st = ready_params(p, &dev);
+    if (st != FASTLSH_OK) return st;
+    if (!jit_selected(p)) return FASTLSH_EUNSUPPORTED;  // only K1j stores keys with multimem.st
+    const uint64_t* dr = nullptr;
+    st = keys_device(ks, dev, &dr);
+    if (st != FASTLSH_OK) return st;
+    return jit::launch(p, p->dev[dev], X, N, codes, nullptr, ks, dr, keys_mc, ldk,
+                       reinterpret_cast<cudaStream_t>(stream), true);
+}
+
 fastlsh_status fastlsh_params_prepare(const fastlsh_params* p, const fastlsh_keys* ks, int32_t what) {
     if (!p || what < 0 || what > 7) return FASTLSH_EINVAL;
     if (!jit_selected(p)) return FASTLSH_OK;  // nothing to compile: K1r / K1 are built in

@@ -63,9 +63,13 @@ struct RowArgs {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// The "memory" clobber keeps every gather load ordered (in the compiler) before the stage's refill
+// protocol — the __syncwarp + shared-counter atomicAdd + TMA issue that follows the slot loop — and
+// after the mbarrier wait that precedes it. The loop's FFMAs are register-only,
+// so the clobber does not constrain their scheduling (C1 timing unchanged).
 __device__ __forceinline__ float lds32(uint32_t addr) {
     float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
 }
 

@@ -117,6 +117,7 @@ struct Module;  // a compiled K1j variant (jit.cpp)
 struct Variant {
     int mode = 0, L = 0, K = 0;
     std::vector<uint64_t> r;  // key multipliers compiled into the module (empty: no keys)
+    bool mc = false;          // keys stored to a multicast address
     std::shared_ptr<Module> mod;
 };
 struct State {
@@ -264,6 +265,7 @@ struct Spec {
     const uint64_t* r;   // their multipliers [L][K+1] (compiled in as immediates)
     int warps, ncb;      // warps per CTA, code boxes per warp
     int mode;            // 0: codes (+ keys when L > 0), 1: projections
+    int mc;              // keys stored with multimem.st to a multicast (NVLS) address
 };
 std::string k1j_source(const Spec& s);
 bool nvrtc_available();
@@ -275,7 +277,7 @@ bool applicable(const fastlsh_params& p);
 // failure): the caller then uses K1r / K1.
 fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
                       float* proj, const fastlsh_keys* ks, const uint64_t* dev_r, uint64_t* keys, int64_t ldk,
-                      cudaStream_t stream);
+                      cudaStream_t stream, bool keys_mc = false);
 // compile (if needed) the variant a call with these arguments would use
 fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks);
 }  // namespace jit

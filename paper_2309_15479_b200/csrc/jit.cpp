@@ -115,6 +115,17 @@ __device__ __forceinline__ void bulk_wait_read_ring() { asm volatile("cp.async.b
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// A compound key leaves either as a plain store into this GPU's [L][ldk] table or, with FL_MC, as a
+// multimem store to the multicast address of a table replicated on every GPU of the NVLink domain
+// (NVSwitch multicast: the key all-gather of SURVEY.md §8(a) a8 happens inside the hashing kernel).
+__device__ __forceinline__ void key_store(u64* p, u64 key) {
+#if FL_MC
+    asm volatile("multimem.st.global.b64 [%0], %1;" ::"l"(p), "l"(key) : "memory");
+#else
+    *p = key;
+#endif
+}
+
 // Codes leave in groups of 32 hashes: a swizzled 32 x 32 box of the warp's ring, written 4 codes
 // (one STS.128) at a time as they are produced, then one TMA tensor store per group.
 __device__ __forceinline__ void group_begin(int lane) {
@@ -167,7 +178,7 @@ __device__ __noinline__ void fix_row(const JArgs& a, float* scr, long long row, 
             s2 += (rv >> 42) * u;
         }
         const u64 key = mod61(rl[0] + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
-        if (row < a.N && !(FL_DEBUG & 1)) a.keys[l * a.ldk + a.col0 + row] = key;
+        if (row < a.N && !(FL_DEBUG & 1)) key_store(a.keys + l * a.ldk + a.col0 + row, key);
     }
 #endif
 }
@@ -246,6 +257,7 @@ std::string k1j_source(const Spec& s) {
     def("FL_WB", wb);
     def("FL_L", s.L);
     def("FL_KT", s.K > 0 ? s.K : 1);
+    def("FL_MC", s.mc ? 1 : 0);
     {
         const char* dbg = std::getenv("FASTLSH_JIT_DEBUG");  // experiment knob (tools/dbg_keys*.py)
         def("FL_DEBUG", dbg ? std::atoi(dbg) : 0);
@@ -358,8 +370,8 @@ std::string k1j_source(const Spec& s) {
                         src += buf;
                         src += (s.K < 256 ? "s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
                                           : "mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42)); ");
-                        src += "if (live && !(FL_DEBUG & 2)) kp[" + std::to_string(l) +
-                               "ll * a.ldk] = key; s0 = 0; s1 = 0; s2 = 0; }";
+                        src += "if (live && !(FL_DEBUG & 2)) key_store(kp + " + std::to_string(l) +
+                               "ll * a.ldk, key); s0 = 0; s1 = 0; s2 = 0; }";
                     }
                 }
                 src += "\n";
@@ -556,15 +568,16 @@ bool keys_fit(const fastlsh_params& p, const fastlsh_keys* ks) {
     return (int64_t)ks->L * ks->K <= p.k && ks->K <= 1024;  // K <= 1024: the 64-bit limb sums are exact
 }
 
-std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fastlsh_keys* ks, fastlsh_status* st) {
+std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fastlsh_keys* ks, bool mc,
+                                    fastlsh_status* st) {
     State& js = p->jit;
     std::lock_guard<std::mutex> g(js.mu);
     const int L = ks ? ks->L : 0, K = ks ? ks->K : 0;
     for (auto& v : js.variants)
-        if (v.mode == mode && v.L == L && v.K == K && (!ks || v.r == ks->r)) return v.mod;
+        if (v.mode == mode && v.L == L && v.K == K && v.mc == mc && (!ks || v.r == ks->r)) return v.mod;
     const int warps = warps_for(p->n);
     Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), L, K, ks ? ks->r.data() : nullptr,
-           warps, kNcb, mode};
+           warps, kNcb, mode, mc ? 1 : 0};
     std::string src = k1j_source(s);
     std::shared_ptr<Module> mod;
     {
@@ -599,6 +612,7 @@ std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fas
     v.mode = mode;
     v.L = L;
     v.K = K;
+    v.mc = mc;
     if (ks) v.r = ks->r;
     v.mod = mod;
     js.variants.push_back(std::move(v));
@@ -624,13 +638,14 @@ fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks
     if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
     if (ks && (mode != 0 || !keys_fit(*p, ks))) return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    return get_variant(p, mode, ks, &st) ? FASTLSH_OK : st;
+    return get_variant(p, mode, ks, false, &st) ? FASTLSH_OK : st;
 }
 
 fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
                       float* proj, const fastlsh_keys* ks, const uint64_t* dev_r, uint64_t* keys, int64_t ldk,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, bool keys_mc) {
     if (!applicable(*p) || !d.j_idx) return FASTLSH_EUNSUPPORTED;
+    if (keys_mc && !ks) return FASTLSH_EINVAL;
     void* out = proj ? static_cast<void*>(proj) : static_cast<void*>(codes);
     const int mode = proj ? 1 : 0;
     if (proj && ks) return FASTLSH_EUNSUPPORTED;
@@ -640,7 +655,7 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
         N > (int64_t)0x7fffffff - 64)
         return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    std::shared_ptr<Module> mod = get_variant(p, mode, ks, &st);
+    std::shared_ptr<Module> mod = get_variant(p, mode, ks, keys_mc, &st);
     if (!mod) return st;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -718,7 +733,8 @@ int main(int argc, char** argv) {
     std::vector<uint64_t> r((size_t)L * (K + 1));
     for (int l = 0; l < L; ++l)
         for (int j = 0; j <= K; ++j) r[(size_t)l * (K + 1) + j] = fastlsh::draw_key_multiplier(1, l, j);
-    fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, r.data(), 8, 2, argc > 6 ? atoi(argv[6]) : 0};
+    fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, r.data(), 8, 2, argc > 6 ? atoi(argv[6]) : 0,
+                         argc > 7 ? atoi(argv[7]) : 0};
     const std::string src = fastlsh::jit::k1j_source(s);
     FILE* f = fopen("/tmp/k1j.cu", "w");
     fwrite(src.data(), 1, src.size(), f);

@@ -81,3 +81,64 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t[0])
+
+
+class KeyTable:
+    """The global [L][N_total] key table of a row-sharded build.
+
+    mode "nvls": the table lives in torch symmetric memory with an NVSwitch multicast mapping; K1j
+    writes every key with multimem.st straight into all GPUs' copies while it hashes
+    (fastlsh_hash_keys_multicast), so the all-gather overlaps the hashing tile by tile and finishing
+    it is one group barrier. mode "nccl": keys are built into a rank-local [L][N_r] buffer and
+    all-gathered with NCCL (allgather_keys) — used when multicast is unavailable or the params are not
+    served by K1j. `mode` is decided at construction ("auto" tries nvls first)."""
+
+    def __init__(self, L: int, n_total: int, group=None, device=None, mode: str = "auto"):
+        import torch
+        import torch.distributed as dist
+        self.L, self.n_total, self.group = L, n_total, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.lo, self.hi = shard_rows(n_total, self.world, self.rank)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.mode, self.handle, self.table, self.local = None, None, None, None
+        self.why = ""
+        if mode in ("auto", "nvls"):
+            try:
+                import torch.distributed._symmetric_memory as symm
+                t = symm.empty((L, n_total), dtype=torch.int64, device=self.device)
+                name = (group or dist.group.WORLD).group_name
+                h = symm.rendezvous(t, name)
+                if not getattr(h, "multicast_ptr", 0):
+                    raise RuntimeError("symmetric memory has no multicast mapping on this system")
+                self.mode, self.handle, self.table = "nvls", h, t
+            except Exception as ex:  # noqa: BLE001 (fall back, record why)
+                self.why = f"{type(ex).__name__}: {ex}"
+                if mode == "nvls":
+                    raise
+        if self.mode is None:
+            self.mode = "nccl"
+            self.local = torch.empty((L, self.hi - self.lo), dtype=torch.int64, device=self.device)
+            self.table = torch.empty((L, n_total), dtype=torch.int64, device=self.device)
+
+    @property
+    def multicast_ptr(self) -> int:
+        return int(self.handle.multicast_ptr) if self.handle is not None else 0
+
+    def hash_keys(self, fl, params, keys, X, col0: int, codes=None, stream=None):
+        """Hash rows [col0, col0 + N) of this rank's shard (X) and place their keys (global columns
+        lo + col0 ...). Returns the codes tensor (or None)."""
+        if self.mode == "nvls":
+            return fl.hash_keys_multicast(params, keys, X, self.multicast_ptr, self.n_total, self.lo + col0,
+                                          codes=codes, with_codes=codes is not None, stream=stream)
+        c, _ = fl.hash_keys(params, keys, X, codes=codes, keys_out=self.local, col0=col0,
+                            with_codes=codes is not None, stream=stream)
+        return c
+
+    def finish(self, wait: bool = True):
+        """Complete the exchange: nvls — a group barrier (every rank's multicast stores are visible
+        afterwards); nccl — the all-gather of the local keys into the table."""
+        if self.mode == "nvls":
+            self.handle.barrier()
+            return []
+        return allgather_keys(self.local, out=self.table, group=self.group, wait=wait, n_total=self.n_total)
