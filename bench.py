@@ -643,6 +643,21 @@ def main():
            "api": "fastlsh_hash_host (pinned host buffers, 2-stream chunked pipeline)", "steps": args.e2e_steps,
            "rows_per_gpu": Ne, "pcie_gbs": (Xh.numel() * 4 + codes_h.numel() * 4 +
                                             (keys_h.numel() * 8 if keys_h is not None else 0)) / float(et[0]) / 1e9}
+    # the same through the host API with only the keys coming back (codes stay on the device; with
+    # K1j they never leave the SM): the streaming-rebuild form of the step's result
+    e2e_keys = None
+    if Kobj is not None:
+        fl.hash_host(P, Kobj, Xh, None, keys_h, chunk_rows=262144, with_codes=False)
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            fl.hash_host(P, Kobj, Xh, None, keys_h, chunk_rows=262144, with_codes=False)
+        ek = torch.tensor([(time.perf_counter() - te) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ek, op=dist.ReduceOp.MAX)
+        e2e_keys = {"value": world * Ne * cfg.k / float(ek[0]), "unit": "hashes/s",
+                    "h2d_bytes_per_step": int(Xh.numel() * 4), "d2h_bytes_per_step": int(keys_h.numel() * 8),
+                    "api": "fastlsh_hash_host with codes_host = NULL (keys only cross PCIe)"}
+    e2e["keys_only"] = e2e_keys
     del Xh, codes_h, keys_h
 
     # CPU leg (rank 0, N = 1 only): the oracle timed on the host cores, and the parity of sampled rows

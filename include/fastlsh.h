@@ -261,7 +261,8 @@ fastlsh_status fastlsh_mips_transform(const float* X, int64_t N, int32_t n, cons
 /* ---- host-buffer entry point (end-to-end; SURVEY.md §3 "config 4 streaming") ----------------- */
 
 /* Hash HOST rows: X_host f32[N*n] (pinned or pageable), codes_host int32[N*k], keys_host
- * uint64[L*N] table-major (may be NULL; `keys` may be NULL). Rows are streamed in chunks of
+ * uint64[L*N] table-major (may be NULL; `keys` may be NULL). codes_host may be NULL when keys are
+ * requested: the codes then never cross PCIe (with K1j they never leave the SM). Rows are streamed in chunks of
  * `chunk_rows` through a double-buffered device workspace owned by the params object, with H2D
  * copies, hashing and D2H copies overlapped on two streams. Synchronous: returns when the host
  * outputs are complete. */

@@ -572,8 +572,9 @@ def hash_keys_multicast(params: Params, keys: Keys, X, mc_ptr: int, ldk: int, co
 
 
 def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_host=None,
-              chunk_rows: int = 65536):
-    """End-to-end entry point on HOST buffers (numpy or pinned torch CPU tensors)."""
+              chunk_rows: int = 65536, with_codes: bool = True):
+    """End-to-end entry point on HOST buffers (numpy or pinned torch CPU tensors). with_codes=False
+    (keys required): only the keys come back to the host."""
     import torch
     params._ready()
     if isinstance(X_host, np.ndarray):
@@ -582,11 +583,14 @@ def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_h
         raise TypeError("X_host must be a contiguous float32 host tensor")
     _check_X(params, X_host, "X_host")
     N = X_host.shape[0]
-    if codes_host is None:
+    if not with_codes and keys is None:
+        raise ValueError("with_codes=False needs keys")
+    if codes_host is None and with_codes:
         codes_host = torch.empty((N, params.k), dtype=torch.int32, pin_memory=X_host.is_pinned())
-    if codes_host.is_cuda or codes_host.dtype != torch.int32 or not codes_host.is_contiguous():
-        raise TypeError("codes_host must be a contiguous int32 host tensor")
-    _check_out(codes_host, N, params.k, "codes_host")
+    if codes_host is not None:
+        if codes_host.is_cuda or codes_host.dtype != torch.int32 or not codes_host.is_contiguous():
+            raise TypeError("codes_host must be a contiguous int32 host tensor")
+        _check_out(codes_host, N, params.k, "codes_host")
     kp = ctypes.c_void_p(0)
     if keys is not None:
         if keys.L * keys.K > params.k:
@@ -599,7 +603,8 @@ def hash_host(params: Params, keys: Keys | None, X_host, codes_host=None, keys_h
         kp = ctypes.c_void_p(keys_host.data_ptr())
     _check(params._lib.fastlsh_hash_host(params._h, keys._h if keys is not None else None,
                                          ctypes.c_void_p(X_host.data_ptr()), N,
-                                         ctypes.c_void_p(codes_host.data_ptr()), kp, chunk_rows),
+                                         ctypes.c_void_p(codes_host.data_ptr() if codes_host is not None else 0), kp,
+                                         chunk_rows),
            "fastlsh_hash_host")
     return codes_host, keys_host
 

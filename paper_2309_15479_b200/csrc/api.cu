@@ -749,7 +749,7 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
                                  int64_t chunk_rows) {
     if (!p || N < 0 || chunk_rows <= 0) return FASTLSH_EINVAL;
     if (N == 0) return FASTLSH_OK;
-    if (!X_host || !codes_host) return FASTLSH_EINVAL;
+    if (!X_host || (!codes_host && !(ks && keys_host))) return FASTLSH_EINVAL;  // codes optional with keys
     if (ks && keys_host && (int64_t)ks->L * ks->K > p->k) return FASTLSH_EINVAL;
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
@@ -787,8 +787,9 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         FL_CUDA(cudaMemcpyAsync(d.ws_x[b], X_host + r0 * p->n, (size_t)rows * p->n * sizeof(float),
                                 cudaMemcpyHostToDevice, s));
         bool fused_here = false;
-        if (want_keys && jit_selected(p)) {
-            st = jit::launch(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, ks, dr, d.ws_keys[b], rows, s);
+        if (want_keys && jit_selected(p)) {  // codes not wanted on the host: they never leave the SM
+            st = jit::launch(p, d, d.ws_x[b], rows, codes_host ? d.ws_codes[b] : nullptr, nullptr, ks, dr, d.ws_keys[b],
+                             rows, s);
             fused_here = st == FASTLSH_OK;
             if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
         }
@@ -808,8 +809,9 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
             st = launch_hash(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s);
         }
         if (st != FASTLSH_OK) return st;
-        FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, s));
+        if (codes_host)
+            FL_CUDA(cudaMemcpyAsync(codes_host + r0 * p->k, d.ws_codes[b], (size_t)rows * p->k * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s));
         if (want_keys) {
             if (!fused_here) st = launch_build_keys(ks, dr, d.ws_codes[b], rows, p->k, d.ws_keys[b], rows, s);
             if (st != FASTLSH_OK) return st;

@@ -152,6 +152,8 @@ def test_jit_determinism_chunking_and_host_path():
     codes_d, keys_d = fl.hash_keys(P, Kobj, X)
     codes_h, keys_h = fl.hash_host(P, Kobj, X.cpu().pin_memory(), chunk_rows=3000)
     assert torch.equal(codes_d.cpu(), codes_h) and torch.equal(keys_d.cpu(), keys_h)
+    none, keys_h2 = fl.hash_host(P, Kobj, X.cpu().pin_memory(), chunk_rows=3000, with_codes=False)
+    assert none is None and torch.equal(keys_d.cpu(), keys_h2)
 
 
 def test_jit_unaligned_falls_back_in_auto_mode():

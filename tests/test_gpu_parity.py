@@ -239,6 +239,8 @@ def test_host_entry_point_matches_device_path(fused):
     codes_h, keys_h = fl.hash_host(P, K, Xh, chunk_rows=3000)
     assert torch.equal(codes_d.cpu(), codes_h)
     assert torch.equal(keys_d.cpu(), keys_h)
+    _, keys_h2 = fl.hash_host(P, K, Xh, chunk_rows=3000, with_codes=False)  # codes stay on the device
+    assert torch.equal(keys_d.cpu(), keys_h2)
 
 
 # ---- compound keys: bit-exact vs Python big integers, on seeded code matrices ------------------------
