@@ -616,8 +616,37 @@ def main():
             dense[f"tf32x{prec}"] = {"ms": ms, "rows": Nd, "hashes_per_s": Nd * cfg.k / (ms / 1e3),
                                      "mma_tflops": 2.0 * Nd * cfg.n * kpad * prec / (ms / 1e3) / 1e12,
                                      "fastlsh_speedup": (ms / Nd) / t_codes}
+        # library reference points (cuBLAS through torch.matmul: plumbing, not the product): the same
+        # dense X . A^T in 1xTF32 (cublasLt tensor cores) and full FP32 (SIMT SGEMM, parity-clean), with
+        # the +b, /w, floor epilogue in torch
+        try:
+            from fastlsh_inputs import e2lsh_arrays
+            _, Ad, bd = e2lsh_arrays(cfg.n, cfg.k, cfg.w, cfg.seed)
+            At = torch.as_tensor(Ad, device=dev).t().contiguous()
+            bt = torch.as_tensor(bd, device=dev)
+            prev = torch.backends.cuda.matmul.allow_tf32
+            for name, tf32 in (("cublas_tf32", True), ("cublas_fp32", False)):
+                torch.backends.cuda.matmul.allow_tf32 = tf32
+                run = lambda: (Xd @ At).add_(bt).div_(cfg.w).floor_().to(torch.int32)  # noqa: E731
+                run()
+                d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                d0.record(stream)
+                for _ in range(3):
+                    run()
+                d1.record(stream)
+                torch.cuda.synchronize()
+                ms = d0.elapsed_time(d1) / 3
+                dense[name] = {"ms": ms, "rows": Nd, "hashes_per_s": Nd * cfg.k / (ms / 1e3),
+                               "fastlsh_speedup": (ms / Nd) / t_codes,
+                               "note": "torch.matmul + torch epilogue (cuBLAS reference point)"}
+            torch.backends.cuda.matmul.allow_tf32 = prev
+            del At, bt
+        except Exception as ex:  # noqa: BLE001
+            dense["cublas_error"] = str(ex)
         dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows (codes only); tf32x3 is the "
-                         "parity-gated comparator (3xTF32), tf32x1 the ungated reference point; speedup vs the "
+                         "parity-gated comparator (3xTF32), tf32x1 the ungated reference point; cublas_fp32 the "
+                         "parity-clean library reference, cublas_tf32 the ungated library one; speedup vs the "
                          "headline FastLSH launch per row (which also builds the keys)")
         del Pd
 

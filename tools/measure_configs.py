@@ -55,7 +55,7 @@ CASES = [  # name, m override, rows, note
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.jsonl"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.jsonl"))
     args = ap.parse_args()
     bw = hbm_peak()
     out = open(args.out, "w")
@@ -79,17 +79,24 @@ def main():
         rp = P.row_packing()
         if rp is not None:
             rec["row_packing"] = {kk: rp[kk] for kk in ("parts", "slots", "warps", "hash_blocks", "S", "n1")}
-        rec["auto_kernel"] = {1: "K1", 2: "K1t", 3: "K1r"}[info["kernel"]]
-        for kern, key in (("rows", "K1r"), ("smem", "K1"), ("tmem", "K1t")):
+        rec["auto_kernel"] = {1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}[info["kernel"]]
+        for kern, key in (("jit", "K1j"), ("rows", "K1r"), ("smem", "K1"), ("tmem", "K1t")):
             try:
                 P.set_kernel(kern)
                 ms = timed(lambda: fl.fastlsh_hash(P, X, out=codes), iters)
                 rec[key] = {"ms": ms, "hashes_per_s": N * c.k / (ms / 1e3), "roofline_frac": t_roof / (ms / 1e3),
-                            "smem_frac": t_smem / (ms / 1e3)}
+                            "smem_frac": t_smem / (ms / 1e3), "hbm_frac": t_hbm / (ms / 1e3)}
             except fl.FastLSHError as ex:
                 rec[key] = {"unavailable": str(ex)}
         P.set_kernel("auto")
-        best = min((rec[k]["ms"] for k in ("K1r", "K1") if "ms" in rec[k]))
+        best = min((rec[k]["ms"] for k in ("K1j", "K1r", "K1") if "ms" in rec[k]))
+        if c.L:  # the bench's step: hash + keys through fastlsh_hash_keys with the automatic kernel
+            Kobj = fl.Keys.create(c.L, c.K, seed=c.seed)
+            keys = torch.empty((c.L, N), dtype=torch.int64, device="cuda")
+            ms = timed(lambda: fl.hash_keys(P, Kobj, X, codes=codes, keys_out=keys), iters)
+            rec["hash_keys_auto"] = {"ms": ms, "hashes_per_s": N * c.k / (ms / 1e3),
+                                     "hbm_bytes_per_row": 4 * c.n + 4 * c.k + 8 * c.L}
+            del keys
         try:
             Pd = fl.Params.e2lsh(c.n, c.k, c.w, seed=c.seed)
             for prec in (3, 1):
