@@ -364,12 +364,15 @@ def main():
     # all-gather is one group barrier. Otherwise (no multicast / not K1j): NCCL all-gather, where the
     # all-gather of step j runs on NCCL's stream while step j+1 hashes into the other keys buffer
     # (double-buffered); step j+1 waits for it before launching its own all-gather.
-    ktable = None
+    ktable, nvls_why = None, None
     if Kobj and world > 1 and jit and args.exchange != "nccl":
         from paper_2309_15479_b200.distributed import KeyTable
-        ktable = KeyTable(cfg.L, N_total, device=dev, mode=args.exchange)
-        if ktable.mode != "nvls":
-            ktable = None
+        try:
+            ktable = KeyTable(cfg.L, N_total, device=dev, mode="nvls")  # raises (allocating nothing) without multicast
+        except Exception as ex:  # noqa: BLE001 (fall back to NCCL; reported in the JSON)
+            if args.exchange == "nvls":
+                raise
+            ktable, nvls_why = None, f"{type(ex).__name__}: {ex}"
     nvls = ktable is not None
     gathered = (ktable.table if nvls else torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev)) \
         if (Kobj and world > 1) else None
@@ -732,6 +735,7 @@ def main():
                           f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
                 "key_exchange": ("nvls" if nvls else "nccl") if world > 1 and Kobj else None,
+                "nvls_unavailable": nvls_why,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash_keys": statistics.mean(hash_ms),
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,

@@ -331,7 +331,7 @@ std::string k1j_source(const Spec& s) {
         }
         h += ");";
         if (s.mode == 0)
-            h += " bad |= !(fabsf(q) < 2147483648.0f);";
+            h += " bad" + std::to_string(j & 3) + " |= !(fabsf(q) < 2147483648.0f);";
         else
             h += " " + cj + " = __float_as_int(p);";
         return h + " }";
@@ -341,7 +341,9 @@ std::string k1j_source(const Spec& s) {
     src += "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
            "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, const __grid_constant__ JArgs a) {\n";
     src += kTileHead;
-    if (s.mode == 0) src += "        bool bad = false;\n";
+    // four flag accumulators (one predicate chain each): a single `bad |= ...` serialises all k
+    // FSETP.OR instructions of a tile through one predicate register
+    if (s.mode == 0) src += "        bool bad0 = false, bad1 = false, bad2 = false, bad3 = false;\n";
     if (keys) src += "        u64 s0 = 0, s1 = 0, s2 = 0;\n        const bool live = row < a.N;\n        u64* kp = a.keys + a.col0 + row;\n";
     char buf[160];
     for (int g = 0; g < groups; ++g) {
@@ -382,6 +384,7 @@ std::string k1j_source(const Spec& s) {
     }
     if (s.mode == 0) {
         src += R"FL(
+        const bool bad = (bad0 | bad1) | (bad2 | bad3);
         if (__any_sync(0xffffffffu, bad)) {
             unsigned bm = __ballot_sync(0xffffffffu, bad);
             if (lane == 0) {

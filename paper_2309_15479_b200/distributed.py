@@ -106,6 +106,9 @@ class KeyTable:
         if mode in ("auto", "nvls"):
             try:
                 import torch.distributed._symmetric_memory as symm
+                # ask before allocating: without multicast the [L][N_total] symmetric buffer would be wasted
+                if not symm._SymmetricMemory.has_multicast_support(symm.DeviceType.CUDA, self.device.index or 0):
+                    raise RuntimeError("no multicast support on this device (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED)")
                 t = symm.empty((L, n_total), dtype=torch.int64, device=self.device)
                 name = (group or dist.group.WORLD).group_name
                 h = symm.rendezvous(t, name)
