@@ -35,7 +35,7 @@ namespace {
 constexpr int BM = 256;         // rows per tile: two UMMA M=128 halves, two TMEM accumulators
 constexpr int BN = 256;         // hashes per tile (UMMA N)
 constexpr int BK = 16;          // floats per K-block (one 64-byte swizzle row)
-constexpr int kStagesE = 3;
+constexpr int kMaxStagesE = 6;  // 3 stages of X|Xlo|Ahi|Alo (3xTF32) or 6 of X|Ahi (1xTF32): ~192 KB in flight
 constexpr int kThreadsE = 320;  // 10 warps
 constexpr uint32_t kXTileBytes = BM * BK * 4;   // 16 KB
 constexpr uint32_t kATileBytes = BN * BK * 4;   // 16 KB
@@ -130,8 +130,12 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment for the swizzle atoms
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagesE * kStageBytesE);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStagesE + 1);
+    // 1xTF32 stages carry only X and Ahi (32 KB), so twice as many fit: the same bytes in flight for
+    // a third of the MMA work per stage (measured 4.19 ms on C1 with 3 stages: latency-bound)
+    const int kStagesE = a.precision == 3 ? 3 : 6;
+    const uint32_t kStageBytes = a.precision == 3 ? kStageBytesE : kXTileBytes + kATileBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagesE * kStageBytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStagesE + 1);
     constexpr int kConvThreads = kThreadsE - 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long m0 = (long long)blockIdx.x * BM;
@@ -139,15 +143,16 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
     const int KB = (a.n + BK - 1) / BK;
 
     const uint32_t sbase = smem_u32(smem);
-    auto XT = [&](int s) { return sbase + s * kStageBytesE; };
-    auto XL = [&](int s) { return sbase + s * kStageBytesE + kXTileBytes; };
-    auto AH = [&](int s) { return sbase + s * kStageBytesE + 2 * kXTileBytes; };
-    auto AL = [&](int s) { return sbase + s * kStageBytesE + 2 * kXTileBytes + kATileBytes; };
+    // stage layout: X | Ahi | Xlo | Alo (the last two only at 3xTF32)
+    auto XT = [&](int s) { return sbase + s * kStageBytes; };
+    auto AH = [&](int s) { return sbase + s * kStageBytes + kXTileBytes; };
+    auto XL = [&](int s) { return sbase + s * kStageBytes + kXTileBytes + kATileBytes; };
+    auto AL = [&](int s) { return sbase + s * kStageBytes + 2 * kXTileBytes + kATileBytes; };
     const uint32_t bar0 = smem_u32(bars);
     auto FULL = [&](int s) { return bar0 + 8u * s; };
-    auto CONV = [&](int s) { return bar0 + 8u * (kStagesE + s); };
-    auto EMPTY = [&](int s) { return bar0 + 8u * (2 * kStagesE + s); };
-    const uint32_t ACC = bar0 + 8u * (3 * kStagesE);
+    auto CONV = [&](int s) { return bar0 + 8u * (kMaxStagesE + s); };
+    auto EMPTY = [&](int s) { return bar0 + 8u * (2 * kMaxStagesE + s); };
+    const uint32_t ACC = bar0 + 8u * (3 * kMaxStagesE);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesE; ++s) {
@@ -218,8 +223,8 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
             const int s = kb % kStagesE;
             mbar_wait(FULL(s), (uint32_t)((kb / kStagesE) & 1));
             if (a.precision == 3) {
-                float4* xt = reinterpret_cast<float4*>(smem + s * kStageBytesE);
-                float4* xl = reinterpret_cast<float4*>(smem + s * kStageBytesE + kXTileBytes);
+                float4* xt = reinterpret_cast<float4*>(smem + s * kStageBytes);
+                float4* xl = reinterpret_cast<float4*>(smem + s * kStageBytes + kXTileBytes + kATileBytes);
 #pragma unroll
                 for (int i = 0; i < (int)(kXTileBytes / 16) / kConvThreads; ++i) {
                     float4 v = xt[t + kConvThreads * i];
@@ -378,7 +383,7 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     a.codes = codes;
     a.proj = proj;
     a.flags = d.flags;
-    const size_t smem = kStagesE * kStageBytesE + 1024 + 128;
+    const size_t smem = 3 * kStageBytesE + 1024 + 256;  // 3 x 64 KB (3xTF32) or 6 x 32 KB (1xTF32)
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
