@@ -737,9 +737,16 @@ def main():
                 "key_exchange": ("nvls" if nvls else "nccl") if world > 1 and Kobj else None,
                 "nvls_unavailable": nvls_why,
                 "keys_only": keys_only,
-                "breakdown_ms": {"hash_keys": statistics.mean(hash_ms),
+                "breakdown_ms": {"hash": statistics.mean(hash_ms),
+                                 "hash_note": "sum over the step's chunk launches of the hashing kernel(s), CUDA events; "
+                                              "with K1j each launch also writes the keys",
                                  "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
-                                 "hash_keys_max_over_ranks": hash_ms_max},
+                                 "hash_max_over_ranks": hash_ms_max,
+                                 "roofline_frac_from_hash": ((N * (4 * cfg.n + 4 * cfg.k + 8 * cfg.L) if jit else
+                                                              N * cfg.k * cfg.m) / (statistics.mean(hash_ms) / 1e3) /
+                                                             ((peaks["hbm_gbs"] * 1e9) if jit else
+                                                              (NUM_SMS * SMEM_GATHERS_PER_CLK_PER_SM *
+                                                               peaks["sm_max_mhz"] * 1e6)))},
                 "jit_prepare_s": prep_s,
                 "dense_e2lsh": dense, "tables": tables, "queries": queries,
                 "packing": _packing_summary(P, info)}
