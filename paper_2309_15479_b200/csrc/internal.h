@@ -118,6 +118,7 @@ struct Variant {
     int mode = 0, L = 0, K = 0;
     std::vector<uint64_t> r;  // key multipliers compiled into the module (empty: no keys)
     bool mc = false;          // keys stored to a multicast address
+    bool codes = true;        // codes stored (false: keys only)
     std::shared_ptr<Module> mod;
 };
 struct State {
@@ -266,6 +267,7 @@ struct Spec {
     int warps, ncb;      // warps per CTA, code boxes per warp
     int mode;            // 0: codes (+ keys when L > 0), 1: projections
     int mc;              // keys stored with multimem.st to a multicast (NVLS) address
+    int codes;           // mode 0: codes stored (1) or kept on chip, keys only (0)
 };
 std::string k1j_source(const Spec& s);
 bool nvrtc_available();

@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -123,6 +124,16 @@ __device__ __forceinline__ void key_store(u64* p, u64 key) {
     asm volatile("multimem.st.global.b64 [%0], %1;" ::"l"(p), "l"(key) : "memory");
 #else
     *p = key;
+#endif
+}
+// the fast path's form: one predicated store (rows past N skip it) instead of a branch per table
+__device__ __forceinline__ void key_store_if(u32 live, u64* p, u64 key) {
+#if FL_MC
+    asm volatile("{\n\t.reg .pred kp;\n\tsetp.ne.b32 kp, %2, 0;\n\t@kp multimem.st.global.b64 [%0], %1;\n\t}"
+                 ::"l"(p), "l"(key), "r"(live) : "memory");
+#else
+    asm volatile("{\n\t.reg .pred kp;\n\tsetp.ne.b32 kp, %2, 0;\n\t@kp st.global.b64 [%0], %1;\n\t}"
+                 ::"l"(p), "l"(key), "r"(live) : "memory");
 #endif
 }
 
@@ -285,18 +296,19 @@ std::string k1j_source(const Spec& s) {
     auto hash_asm = [&](int i, int j) {
         const int32_t* id = s.idx + (size_t)i * s.m;
         const float* co = s.a + (size_t)i * s.m;
-        const int base = s.mode == 0 ? 2 : 1;  // outputs: code, q (codes) or p (projections)
-        std::vector<int> ops;                  // distinct coordinates -> asm operand numbers
+        std::vector<int> ops;  // distinct coordinates -> asm operand numbers %1 ...
         std::vector<int> opnum(s.n, -1);
         for (int t = 0; t < s.m; ++t)
             if (opnum[id[t]] < 0) {
-                opnum[id[t]] = (int)ops.size() + base;
+                opnum[id[t]] = (int)ops.size() + 1;
                 ops.push_back(id[t]);
             }
-        const char* P = s.mode == 0 ? "%1" : "%0";  // register holding p (q is reused for p)
+        // codes: p and q live in a block-local register, only the code leaves; projections: p is %0
+        const char* P = s.mode == 0 ? "q" : "%0";
         const float scale = (s.mode == 0 && p2) ? 1.0f / s.w : 1.0f;
         char buf[112];
-        std::string h = s.mode == 0 ? "{ float q; asm(\"" : "{ float p; asm(\"";
+        const std::string cj = "c" + std::to_string(j & 3);
+        std::string h = s.mode == 0 ? "asm(\"{ .reg .f32 q; " : "{ float p; asm(\"";
         for (int t = 0; t < s.m; ++t) {
             const float c = co[t] * scale;  // exact: power-of-two scale
             uint32_t u;
@@ -307,21 +319,20 @@ std::string k1j_source(const Spec& s) {
                 std::snprintf(buf, sizeof buf, " fma.rn.f32 %s, %%%d, 0f%08X, %s;", P, opnum[id[t]], u, P);
             h += buf;
         }
-        const std::string cj = "c" + std::to_string(j & 3);
         if (s.mode == 0) {
             uint32_t ub, uw;
             if (p2) {
                 const float bs = s.b[i] * scale;
                 std::memcpy(&ub, &bs, 4);
-                std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;", ub);
+                std::snprintf(buf, sizeof buf, " add.rn.f32 q, q, 0f%08X; cvt.rmi.s32.f32 %%0, q; }", ub);
             } else {
                 std::memcpy(&ub, &s.b[i], 4);
                 std::memcpy(&uw, &s.w, 4);
-                std::snprintf(buf, sizeof buf, " add.rn.f32 %%1, %%1, 0f%08X; div.rn.f32 %%1, %%1, 0f%08X; cvt.rmi.s32.f32 %%0, %%1;",
+                std::snprintf(buf, sizeof buf, " add.rn.f32 q, q, 0f%08X; div.rn.f32 q, q, 0f%08X; cvt.rmi.s32.f32 %%0, q; }",
                               ub, uw);
             }
             h += buf;
-            h += "\" : \"=r\"(" + cj + "), \"=f\"(q) :";
+            h += "\" : \"=r\"(" + cj + ") :";
         } else {
             h += "\" : \"=f\"(p) :";
         }
@@ -330,25 +341,55 @@ std::string k1j_source(const Spec& s) {
             h += "\"f\"(x[" + std::to_string(ops[o]) + "])";
         }
         h += ");";
-        if (s.mode == 0)
-            h += " bad" + std::to_string(j & 3) + " |= !(fabsf(q) < 2147483648.0f);";
-        else
-            h += " " + cj + " = __float_as_int(p);";
-        return h + " }";
+        if (s.mode == 1) h += " " + cj + " = __float_as_int(p); }";
+        return h;
     };
 
     const bool keys = s.mode == 0 && s.L > 0;
     src += "\nextern \"C\" __global__ void __launch_bounds__(FL_NW * 32, 1)\n"
            "k1j(const __grid_constant__ TMap xmap, const __grid_constant__ TMap omap, const __grid_constant__ JArgs a) {\n";
     src += kTileHead;
-    // four flag accumulators (one predicate chain each): a single `bad |= ...` serialises all k
-    // FSETP.OR instructions of a tile through one predicate register
-    if (s.mode == 0) src += "        bool bad0 = false, bad1 = false, bad2 = false, bad3 = false;\n";
-    if (keys) src += "        u64 s0 = 0, s1 = 0, s2 = 0;\n        const bool live = row < a.N;\n        u64* kp = a.keys + a.col0 + row;\n";
+    // Flags (codes mode): a per-row range check replaces a per-hash one. With a' = a (or a/w for a
+    // power-of-two w) and S = sum_c |x_c| >= max_c |x_c|, every fp32 quotient obeys
+    // |q_i| <= (1 + 1e-4) (A_i max|x| + |b'_i|) with A_i = sum_j |a'_ij|; a row whose fp32 S is below
+    // T = (2^30 - max|b'|) / (1.01 max A_i) can therefore reach neither |q| >= 2^31 nor a non-finite
+    // value, while NaN / Inf / huge inputs fail `S < T` and take the exact per-hash slow path.
+    // (127 FADDs per row instead of k FSETPs.)
+    if (s.mode == 0) {
+        double amax = 0, bmax = 0;
+        for (int i = 0; i < s.k; ++i) {
+            double ai = 0;
+            for (int j = 0; j < s.m; ++j) ai += std::fabs((double)s.a[(size_t)i * s.m + j]);
+            amax = std::max(amax, ai / (p2 ? (double)s.w : 1.0));
+            bmax = std::max(bmax, std::fabs((double)s.b[i]) / (p2 ? (double)s.w : 1.0));
+        }
+        // non-power-of-two w: q = (p + b) / w, so the bound is on |p + b| < 2^30 w
+        const double lim = p2 ? 1073741824.0 : 1073741824.0 * (double)s.w;
+        double T = amax > 0 ? (lim - bmax) / (1.01 * amax) : 3.0e38;
+        if (!(T > 0)) T = 0;  // every row checked hash by hash
+        float Tf = (float)T;
+        if ((double)Tf > T) Tf = std::nextafter(Tf, 0.0f);
+        // pairwise tree of |x_c| (coordinates past n are zero)
+        std::vector<std::string> terms;
+        for (int c = 0; c < s.n; ++c) terms.push_back("fabsf(x[" + std::to_string(c) + "])");
+        while (terms.size() > 1) {
+            std::vector<std::string> nx;
+            for (size_t t = 0; t + 1 < terms.size(); t += 2) nx.push_back("(" + terms[t] + " + " + terms[t + 1] + ")");
+            if (terms.size() & 1) nx.push_back(terms.back());
+            terms.swap(nx);
+        }
+        src += "        const float sabs = " + terms[0] + ";\n        const bool bad = !(sabs < ";
+        add_float(src, Tf);
+        src += ");\n";
+    }
+    // codes stored (codes / projections) or kept on chip (keys only): a compile-time choice of the variant
+    const bool store = s.mode == 1 || s.codes;
+    if (keys) src += "        u64 s0, s1, s2;\n        const u32 live = row < a.N ? 1u : 0u;\n        u64* kp = a.keys + a.col0 + row;\n";
     char buf[160];
     for (int g = 0; g < groups; ++g) {
-        src += "        {\n            if (a.write_out) group_begin(lane);\n"
-               "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n";
+        src += store ? "        {\n            group_begin(lane);\n"
+                       "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n"
+                     : "        {\n";
         for (int q = 0; q < 8 && 32 * g + 4 * q < s.k; ++q) {
             src += "            { int c0, c1, c2, c3;\n";
             for (int j = 4 * q; j < 4 * q + 4; ++j) {
@@ -356,35 +397,39 @@ std::string k1j_source(const Spec& s) {
                 src += "              " + hash_asm(i, j);
                 if (keys && i < s.L * s.K) {
                     // key term (R9): the three 21-bit limbs of r[l][jj+1] (instruction
-                    // immediates) times u32(code), exact 64-bit sums
+                    // immediates) times u32(code), exact 64-bit sums; S0 starts at r[l][0]
                     const int l = i / s.K, jj = i % s.K;
                     const uint64_t r = s.r[(size_t)l * (s.K + 1) + jj + 1];
+                    if (jj == 0) {
+                        std::snprintf(buf, sizeof buf, " s0 = 0x%llxull; s1 = 0; s2 = 0;",
+                                      (unsigned long long)s.r[(size_t)l * (s.K + 1)]);
+                        src += buf;
+                    }
                     std::snprintf(buf, sizeof buf,
                                   " { const u64 u = (u32)c%d; s0 += 0x%llxull * u; s1 += 0x%llxull * u; s2 += 0x%llxull * u; }",
                                   j & 3, (unsigned long long)(r & 0x1fffff), (unsigned long long)((r >> 21) & 0x1fffff),
                                   (unsigned long long)(r >> 42));
                     src += buf;
-                    // key = (r0 + S0 + S1*2^21 + S2*2^42) mod 2^61-1; for K < 256 every S_q < K*2^53 < 2^61-1
-                    // is already reduced, so only the final sum (< 2^63) needs a reduction
+                    // key = (S0 + S1*2^21 + S2*2^42) mod 2^61-1 with S0 = r0 + ...: for K < 256, S1, S2 <
+                    // K*2^53 < 2^61-1 are already reduced and S0 < 2^62, so one final reduction of a sum
+                    // < 2^63 suffices
                     if (jj == s.K - 1) {
-                        std::snprintf(buf, sizeof buf, "\n              { const u64 key = mod61(0x%llxull + ",
-                                      (unsigned long long)s.r[(size_t)l * (s.K + 1)]);
-                        src += buf;
-                        src += (s.K < 256 ? "s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
-                                          : "mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42)); ");
-                        src += "if (live && !(FL_DEBUG & 2)) key_store(kp + " + std::to_string(l) +
-                               "ll * a.ldk, key); s0 = 0; s1 = 0; s2 = 0; }";
+                        src += s.K < 256 ? "\n              { const u64 key = mod61(s0 + rotl61(s1, 21) + rotl61(s2, 42)); "
+                                         : "\n              { const u64 key = mod61(mod61(s0) + rotl61(mod61(s1), 21) + "
+                                           "rotl61(mod61(s2), 42)); ";
+                        src += "key_store_if(live, kp + " + std::to_string(l) + "ll * a.ldk, key); }";
                     }
                 }
                 src += "\n";
             }
-            src += "              if (a.write_out) put4(box, " + std::to_string(q) + "u, sw, c0, c1, c2, c3); }\n";
+            src += store ? "              put4(box, " + std::to_string(q) + "u, sw, c0, c1, c2, c3); }\n"
+                         : "              (void)c0; (void)c1; (void)c2; (void)c3; }\n";
         }
-        src += "            if (a.write_out) group_end(cring_s, cbi, lane, &omap, " + std::to_string(g) + ", t);\n        }\n";
+        src += store ? "            group_end(cring_s, cbi, lane, &omap, " + std::to_string(g) + ", t);\n        }\n"
+                     : "        }\n";
     }
     if (s.mode == 0) {
         src += R"FL(
-        const bool bad = (bad0 | bad1) | (bad2 | bad3);
         if (__any_sync(0xffffffffu, bad)) {
             unsigned bm = __ballot_sync(0xffffffffu, bad);
             if (lane == 0) {
@@ -571,16 +616,18 @@ bool keys_fit(const fastlsh_params& p, const fastlsh_keys* ks) {
     return (int64_t)ks->L * ks->K <= p.k && ks->K <= 1024;  // K <= 1024: the 64-bit limb sums are exact
 }
 
-std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fastlsh_keys* ks, bool mc,
+std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fastlsh_keys* ks, bool mc, bool codes,
                                     fastlsh_status* st) {
+    codes = codes || mode == 1 || !ks;  // only the keys variant can keep its codes on chip
     State& js = p->jit;
     std::lock_guard<std::mutex> g(js.mu);
     const int L = ks ? ks->L : 0, K = ks ? ks->K : 0;
     for (auto& v : js.variants)
-        if (v.mode == mode && v.L == L && v.K == K && v.mc == mc && (!ks || v.r == ks->r)) return v.mod;
+        if (v.mode == mode && v.L == L && v.K == K && v.mc == mc && v.codes == codes && (!ks || v.r == ks->r))
+            return v.mod;
     const int warps = warps_for(p->n);
     Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), L, K, ks ? ks->r.data() : nullptr,
-           warps, kNcb, mode, mc ? 1 : 0};
+           warps, kNcb, mode, mc ? 1 : 0, codes ? 1 : 0};
     std::string src = k1j_source(s);
     std::shared_ptr<Module> mod;
     {
@@ -616,6 +663,7 @@ std::shared_ptr<Module> get_variant(const fastlsh_params* p, int mode, const fas
     v.L = L;
     v.K = K;
     v.mc = mc;
+    v.codes = codes;
     if (ks) v.r = ks->r;
     v.mod = mod;
     js.variants.push_back(std::move(v));
@@ -641,7 +689,7 @@ fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks
     if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
     if (ks && (mode != 0 || !keys_fit(*p, ks))) return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    return get_variant(p, mode, ks, false, &st) ? FASTLSH_OK : st;
+    return get_variant(p, mode, ks, false, true, &st) ? FASTLSH_OK : st;
 }
 
 fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
@@ -658,7 +706,7 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
         N > (int64_t)0x7fffffff - 64)
         return FASTLSH_EUNSUPPORTED;
     fastlsh_status st = FASTLSH_OK;
-    std::shared_ptr<Module> mod = get_variant(p, mode, ks, keys_mc, &st);
+    std::shared_ptr<Module> mod = get_variant(p, mode, ks, keys_mc, out != nullptr, &st);
     if (!mod) return st;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -737,7 +785,7 @@ int main(int argc, char** argv) {
     for (int l = 0; l < L; ++l)
         for (int j = 0; j <= K; ++j) r[(size_t)l * (K + 1) + j] = fastlsh::draw_key_multiplier(1, l, j);
     fastlsh::jit::Spec s{n, m, k, w, idx.data(), a.data(), b.data(), L, K, r.data(), 8, 2, argc > 6 ? atoi(argv[6]) : 0,
-                         argc > 7 ? atoi(argv[7]) : 0};
+                         argc > 7 ? atoi(argv[7]) : 0, argc > 8 ? atoi(argv[8]) : 1};
     const std::string src = fastlsh::jit::k1j_source(s);
     FILE* f = fopen("/tmp/k1j.cu", "w");
     fwrite(src.data(), 1, src.size(), f);
