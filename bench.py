@@ -435,6 +435,26 @@ def main():
         step(False)
     drain()
     torch.cuda.synchronize()
+    # NVLS self-check (first use of the multicast path on this system): the keys this rank wrote
+    # through the multicast table must equal the plain keys of the same rows; otherwise fall back
+    nvls_check = None
+    if nvls:
+        nck = min(N, 4096)
+        _, ref_keys = fl.hash_keys(P, Kobj, X[:nck])
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(gathered[:, lo:lo + nck], ref_keys))
+        okt = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        nvls_check = {"rows_checked_per_rank": nck, "ok": bool(okt.item())}
+        if not okt.item():
+            nvls, nvls_why = False, "multicast self-check failed: keys differ from the plain keys"
+            gathered = torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev)
+            overlap = not args.no_overlap
+            keys_bufs[:] = [keys, torch.empty_like(keys)] if overlap else [keys]
+            for _ in range(args.warmup):
+                step(False)
+            drain()
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -735,7 +755,7 @@ def main():
                           f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
                 "key_exchange": ("nvls" if nvls else "nccl") if world > 1 and Kobj else None,
-                "nvls_unavailable": nvls_why,
+                "nvls_unavailable": nvls_why, "nvls_selfcheck": nvls_check,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms),
                                  "hash_note": "sum over the step's chunk launches of the hashing kernel(s), CUDA events; "
