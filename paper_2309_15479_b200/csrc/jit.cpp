@@ -146,6 +146,28 @@ __device__ __forceinline__ void group_begin(int lane) {
 __device__ __forceinline__ void put4(unsigned char* box_lane, u32 q, u32 sw, int c0, int c1, int c2, int c3) {
     *reinterpret_cast<int4*>(box_lane + ((q << 4) ^ sw)) = make_int4(c0, c1, c2, c3);
 }
+// Paired form (k % 32 == 0): the codes are viewed as a 3D tensor [N rows][k/32 groups][32 codes] and
+// two consecutive groups leave in one box {32 codes, 2 groups, 32 rows} (8 KB, the whole ring), so each
+// row gets 256 contiguous bytes per store instead of 128 (tools/microbench_wpattern.cu: 128-B
+// segments at 1-KB stride reach 5.1-5.4 TB/s with 512 B/row of reads, 256-B segments 5.8).
+// Box layout with the 128-B swizzle: flattened 128-B line f = 2 * row + group, chunk c at
+// f * 128 + ((c ^ (f & 7)) << 4).
+__device__ __forceinline__ void tma_store3(const TMap* m, u32 src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 ::"l"((u64)m), "r"(src), "r"(x), "r"(y), "r"(z) : "memory");
+}
+__device__ __forceinline__ void pair_begin(int lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the previous pair is read
+    __syncwarp();
+}
+__device__ __forceinline__ void pair_end(u32 cring_s, int lane, const TMap* om, int g0, long long t) {
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store3(om, cring_s, 0, g0, (int)(32 * t));
+        bulk_commit();
+    }
+}
 __device__ __forceinline__ void group_end(u32 cring_s, int& cbi, int lane, const TMap* om, int g, long long t) {
     fence_async_smem();
     __syncwarp();
@@ -218,7 +240,8 @@ const char* kTileHead = R"FL(
         for (int bx = 0; bx < FL_NBX; ++bx) tma_load(xs + bx * 4096, &xmap, 32 * bx, (int)(32 * t), bar);
     }
     u32 ph = 0;
-    int cbi = 0;
+    int cbi = 0;  // ring box of the unpaired form
+    (void)cbi;
     const u32 sw = (u32)(lane & 7) << 4;
     for (; t < a.tiles; t += tstride) {
         mbar_wait(bar, ph);
@@ -384,12 +407,19 @@ std::string k1j_source(const Spec& s) {
     }
     // codes stored (codes / projections) or kept on chip (keys only): a compile-time choice of the variant
     const bool store = s.mode == 1 || s.codes;
+    const bool pair = s.k % 32 == 0;  // 256-byte row segments per store (see pair_end)
     if (keys) src += "        u64 s0, s1, s2;\n        const u32 live = row < a.N ? 1u : 0u;\n        u64* kp = a.keys + a.col0 + row;\n";
     char buf[160];
     for (int g = 0; g < groups; ++g) {
-        src += store ? "        {\n            group_begin(lane);\n"
-                       "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n"
-                     : "        {\n";
+        if (!store)
+            src += "        {\n";
+        else if (!pair)
+            src += "        {\n            group_begin(lane);\n"
+                   "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n";
+        else
+            src += std::string("        {\n") + ((g & 1) ? "" : "            pair_begin(lane);\n") +
+                   "            unsigned char* box = cring + lane * 256 + " + std::to_string((g & 1) * 128) + ";\n"
+                   "            const u32 swp = (u32)((2 * lane + " + std::to_string(g & 1) + ") & 7) << 4;\n";
         for (int q = 0; q < 8 && 32 * g + 4 * q < s.k; ++q) {
             src += "            { int c0, c1, c2, c3;\n";
             for (int j = 4 * q; j < 4 * q + 4; ++j) {
@@ -422,11 +452,17 @@ std::string k1j_source(const Spec& s) {
                 }
                 src += "\n";
             }
-            src += store ? "              put4(box, " + std::to_string(q) + "u, sw, c0, c1, c2, c3); }\n"
+            src += store ? "              put4(box, " + std::to_string(q) + (pair ? "u, swp" : "u, sw") + ", c0, c1, c2, c3); }\n"
                          : "              (void)c0; (void)c1; (void)c2; (void)c3; }\n";
         }
-        src += store ? "            group_end(cring_s, cbi, lane, &omap, " + std::to_string(g) + ", t);\n        }\n"
-                     : "        }\n";
+        if (!store)
+            src += "        }\n";
+        else if (!pair)
+            src += "            group_end(cring_s, cbi, lane, &omap, " + std::to_string(g) + ", t);\n        }\n";
+        else if ((g & 1) || g == groups - 1)
+            src += "            pair_end(cring_s, lane, &omap, " + std::to_string(g & ~1) + ", t);\n        }\n";
+        else
+            src += "        }\n";
     }
     if (s.mode == 0) {
         src += R"FL(
@@ -555,12 +591,16 @@ namespace {
 constexpr int kMaxN = 128;          // a row lives in registers: x[n] plus ~100 working registers
 constexpr int kMaxCode = 16384;     // k*m straight-line FFMAs (16 B each: 256 KB of code)
 constexpr int kNcb = 2;             // code boxes per warp (TMA store ring)
-constexpr size_t kSmemBudget = 220 * 1024;
+constexpr size_t kSmemBudget = 225 * 1024;
 
 int warps_for(int n) {
     const int wb = ((n + 31) / 32 + kNcb) * 4096;
     int w = (int)(kSmemBudget / (size_t)(wb + 8));
-    return w > 8 ? 8 : w;
+    static const int cap = [] {  // experiment knob (FASTLSH_JIT_WARPS), read once
+        const char* e = std::getenv("FASTLSH_JIT_WARPS");
+        return e ? std::atoi(e) : 8;
+    }();
+    return w > cap ? cap : w;
 }
 
 size_t smem_bytes(int n, int warps) {
@@ -587,6 +627,19 @@ EncodeTiledFn encode_fn() {
         return reinterpret_cast<EncodeTiledFn>(q);
     }();
     return fn;
+}
+
+// codes / projections viewed as [rows][cols/32][32]: boxes {32, 2 groups, 32 rows}, 128-byte swizzle
+bool make_map3(CUtensorMap* m, const void* base, long long rows, int cols, bool f32) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || cols % 32) return false;
+    cuuint64_t dims[3] = {32, (cuuint64_t)(cols / 32), (cuuint64_t)rows};
+    cuuint64_t strides[2] = {128, (cuuint64_t)cols * 4};
+    cuuint32_t box[3] = {32, 2, 32};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(base), dims,
+               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // [rows][cols] 4-byte elements, boxes of 32 rows x 32 elements (128 B), 128-byte swizzle
@@ -722,7 +775,9 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
     CUtensorMap xmap, omap;
     if (!make_map(&xmap, X, N, p->n, true)) return FASTLSH_EUNSUPPORTED;
     if (out) {
-        if (!make_map(&omap, out, N, p->k, proj != nullptr)) return FASTLSH_EUNSUPPORTED;
+        const bool ok = p->k % 32 == 0 ? make_map3(&omap, out, N, p->k, proj != nullptr)
+                                       : make_map(&omap, out, N, p->k, proj != nullptr);
+        if (!ok) return FASTLSH_EUNSUPPORTED;
     } else {
         omap = xmap;  // keys only: never used
     }
