@@ -127,27 +127,34 @@ def _sample_rows(N: int, count: int, seed: int, extra=()):
     return np.array(sorted(r), dtype=np.int64)
 
 
-def cpu_baseline(cfg, seconds_target: float = 12.0, one_core_seconds: float = 3.0, rows_from=None):
-    """The CPU oracle as it stands, on a bounded row sample of the same workload: all host cores,
-    then 1 core. rows_from(lo, hi) supplies the rows (default: the synthetic
-    generator on the host)."""
+def _oracle_sample(cfg, seconds_target: float):
+    """The oracle's inputs for a bounded sample of the workload: rows sized (by a 256-row calibration
+    on all host cores) to take about seconds_target, generated once on the host."""
     import oracle
     from fastlsh_inputs import data, fastlsh_arrays
     idx, a, b = fastlsh_arrays(cfg.n, cfg.m, cfg.k, cfg.w, cfg.seed)
     cores = _cores()
-    get = rows_from or (lambda lo, hi: data.generate(cfg.data, cfg.n, lo, hi, seed=cfg.seed).numpy())
-    # calibrate on a small sample, then size the measured sample to ~seconds_target
-    rows0 = 256
-    X0 = get(0, rows0)
+    rows0 = 4096
+    X0 = data.generate(cfg.data, cfg.n, 0, rows0, seed=cfg.seed).numpy()
+    oracle.fastlsh(X0[:256], idx, a, b, cfg.w, threads=cores)  # thread pool start-up outside the calibration
     t = time.perf_counter()
     oracle.fastlsh(X0, idx, a, b, cfg.w, threads=cores)
     dt = max(time.perf_counter() - t, 1e-4)
     rows = int(min(cfg.N, max(rows0, rows0 * seconds_target / dt)))
-    X = get(0, rows)
+    X = data.generate(cfg.data, cfg.n, 0, rows, seed=cfg.seed).numpy()
+    return {"X": X, "idx": idx, "a": a, "b": b, "rows": rows, "cores": cores}
+
+
+def cpu_baseline(cfg, seconds_target: float = 12.0, one_core_seconds: float = 3.0, sample=None):
+    """The CPU oracle as it stands, on a bounded row sample of the same workload: all host cores,
+    then 1 core."""
+    import oracle
+    smp = sample or _oracle_sample(cfg, seconds_target)
+    X, idx, a, b, rows, cores = smp["X"], smp["idx"], smp["a"], smp["b"], smp["rows"], smp["cores"]
     t = time.perf_counter()
     oracle.fastlsh(X, idx, a, b, cfg.w, threads=cores)
     dt = time.perf_counter() - t
-    rows1 = int(min(rows, max(64, rows0 * one_core_seconds / (dt / rows * rows0 * cores))))
+    rows1 = int(min(rows, max(64, rows * one_core_seconds / (dt * cores))))
     t = time.perf_counter()
     oracle.fastlsh(X[:rows1], idx, a, b, cfg.w, threads=1)
     dt1 = time.perf_counter() - t
@@ -160,15 +167,15 @@ def cpu_baseline(cfg, seconds_target: float = 12.0, one_core_seconds: float = 3.
 
 
 def run_reference(args, cfg):
-    """The reference arm of this tier: the CPU oracle as it stands, on the host cores."""
+    """The reference arm of this tier: the CPU oracle as it stands, on the host cores; each step runs
+    it over the same bounded row sample (generated once, ~ref_seconds of oracle work)."""
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    steps = []
+    smp = _oracle_sample(cfg, args.ref_seconds)
     for _ in range(args.warmup):
-        cpu_baseline(cfg, seconds_target=2.0, one_core_seconds=0.2)
-    for _ in range(args.steps):
-        steps.append(cpu_baseline(cfg, seconds_target=args.ref_seconds, one_core_seconds=0.5))
+        cpu_baseline(cfg, one_core_seconds=0.1, sample=smp)
+    steps = [cpu_baseline(cfg, one_core_seconds=0.3, sample=smp) for _ in range(args.steps)]
     vals = [s["value"] for s in steps]
     v = statistics.median(vals)
     cb = dict(steps[-1])
@@ -291,7 +298,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0, help="reference arm: oracle seconds per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
     ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem"],
