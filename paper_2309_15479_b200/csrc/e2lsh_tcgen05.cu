@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -327,6 +328,216 @@ bool make_map(CUtensorMap* m, const float* base, long long rows, int cols, int b
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ------------------------------------------------------------------------------------------
+// CTA-pair form (cta_group::2). A cluster of two CTAs on one TPC computes a
+// 256-row x 256-hash tile with M=256 UMMAs: each CTA stages its own 128 rows of X and its own half
+// (128 hashes) of the coefficient tile, so per SM the operand bytes per MMA FLOP are those of the
+// 256 x 256 single-CTA tile while each SM's TMEM holds only its 128 x 256 accumulator (256 columns).
+//   warp 0    : TMA producer of this CTA's halves (signals its own FULL barrier)
+//   warp 1    : TMEM allocation (cta_group::2) — and, in the leader CTA only, the MMA issue
+//   warps 2-9 : split X into Xhi / Xlo in place, then arrive on the LEADER's CONV barrier (remote
+//               mbarrier arrive through mapa); after the tile, the epilogue of this CTA's 128 rows
+// The leader's commits are multicast to both CTAs' EMPTY / ACC barriers. Per output element the
+// MMA sequence (K-blocks, k-steps, hi.hi / hi.lo / lo.hi) is the one of the single-CTA kernel.
+// 3 stages of 32 KB (3xTF32: X|Bhi|Xlo|Blo of 8 KB each) or 6 of 16 KB (1xTF32: X|Bhi): ~97 KB of
+// shared memory and 256 TMEM columns per CTA, so two pairs share each SM pair and one pair's prologue
+// and epilogue overlap the other's MMAs (measured 6 / 12 stages at one CTA per SM: 8.2 ms on C1)
+constexpr int kPairStages = 3;
+constexpr int kPairStages1 = 6;
+constexpr uint32_t kHalfTile = 128 * BK * 4;  // 8 KB: 128 rows (or hashes) x 16 floats
+constexpr uint32_t kIdescTF32Pair = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t local_bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_bar), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kIdescTF32Pair), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"((uint16_t)3) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreadsE, 1)
+e2lsh_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_ahi,
+                  const __grid_constant__ CUtensorMap map_alo, const E2Args a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const bool x3 = a.precision == 3;
+    const int NS = x3 ? kPairStages : kPairStages1;
+    const uint32_t stage_bytes = x3 ? 4 * kHalfTile : 2 * kHalfTile;  // X | Bhi | Xlo | Blo
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)NS * stage_bytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kPairStages1 + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const long long m0 = (long long)(blockIdx.x >> 1) * 256 + rank * 128;  // this CTA's 128 rows
+    const int h0 = blockIdx.y * BN;                                        // the pair's 256 hashes
+    const int hb = h0 + (int)rank * 128;                                   // this CTA's 128 of them
+    const int KB = (a.n + BK - 1) / BK;
+
+    const uint32_t sbase = smem_u32(smem);
+    auto XT = [&](int s) { return sbase + s * stage_bytes; };
+    auto BH = [&](int s) { return sbase + s * stage_bytes + kHalfTile; };
+    auto XL = [&](int s) { return sbase + s * stage_bytes + 2 * kHalfTile; };
+    auto BL = [&](int s) { return sbase + s * stage_bytes + 3 * kHalfTile; };
+    const uint32_t bar0 = smem_u32(bars);
+    auto FULL = [&](int s) { return bar0 + 8u * s; };
+    auto CONV = [&](int s) { return bar0 + 8u * (kPairStages1 + s); };   // used in the leader
+    auto EMPTY = [&](int s) { return bar0 + 8u * (2 * kPairStages1 + s); };
+    const uint32_t ACC = bar0 + 8u * (3 * kPairStages1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(FULL(s), 1);
+            mbar_init(CONV(s), 2 * 8);  // one arrival per converter warp of both CTAs
+            mbar_init(EMPTY(s), 1);
+        }
+        mbar_init(ACC, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(BN)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated before any remote arrive / MMA
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t bytes = x3 ? 3 * kHalfTile : 2 * kHalfTile;  // Xlo is produced on chip
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % NS;
+                if (kb >= NS) mbar_wait(EMPTY(s), (uint32_t)(((kb - NS) / NS) & 1));
+                mbar_arrive_tx(FULL(s), bytes);
+                tma_load_2d(XT(s), &map_x, kb * BK, (int)m0, FULL(s));
+                tma_load_2d(BH(s), &map_ahi, kb * BK, hb, FULL(s));
+                if (x3) tma_load_2d(BL(s), &map_alo, kb * BK, hb, FULL(s));
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % NS;
+                mbar_wait(CONV(s), (uint32_t)((kb / NS) & 1));  // both CTAs' stage s is converted
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint32_t off = kk * 32;
+                    const uint64_t dxh = umma_desc_sw64(XT(s) + off);
+                    const uint64_t dbh = umma_desc_sw64(BH(s) + off);
+                    const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+                    umma_tf32_pair(tmem, dxh, dbh, acc0);
+                    if (x3) {
+                        umma_tf32_pair(tmem, dxh, umma_desc_sw64(BL(s) + off), 1u);
+                        umma_tf32_pair(tmem, umma_desc_sw64(XL(s) + off), dbh, 1u);
+                    }
+                }
+                umma_commit_pair(EMPTY(s));  // stage s of both CTAs reusable once these MMAs complete
+            }
+            umma_commit_pair(ACC);  // both CTAs' accumulators complete
+        }
+    } else {
+        const int t = threadIdx.x - 64;  // 0..255
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % NS;
+            mbar_wait(FULL(s), (uint32_t)((kb / NS) & 1));
+            if (x3) {
+                float4* xt = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes);
+                float4* xl = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes + 2 * kHalfTile);
+#pragma unroll
+                for (int i = 0; i < (int)(kHalfTile / 16) / 256; ++i) {
+                    const float4 v = xt[t + 256 * i];
+                    float4 h, l;
+                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); l.x = v.x - h.x;
+                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); l.y = v.y - h.y;
+                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); l.z = v.z - h.z;
+                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); l.w = v.w - h.w;
+                    xt[t + 256 * i] = h;
+                    xl[t + 256 * i] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(CONV(s), 0);  // to the leader (also from the leader itself)
+        }
+        // epilogue: this CTA's 128 rows; TMEM lane quadrant = warp % 4, columns split by warp group
+        mbar_wait(ACC, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int quad = warp & 3;
+        const int chalf = (warp - 2) >> 2;  // columns [128 chalf, 128 chalf + 128)
+        const long long rbase = m0 + quad * 32;
+        const float w = a.w;
+        const float inv_w = 1.0f / w;
+        const bool w_pow2 = (__float_as_uint(w) & 0x007fffffu) == 0 && isfinite(inv_w) && inv_w != 0.0f;
+        uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + (warp - 2) * 32 * 33;  // stages are idle now
+#pragma unroll 1
+        for (int c0 = chalf * 128; c0 < chalf * 128 + 128; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+            if (h0 + c0 >= a.k) break;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int h = h0 + c0 + j;
+                const float p = __uint_as_float(v[j]);
+                uint32_t out = v[j];
+                if (!a.proj && h < a.k) {
+                    const float num = __fadd_rn(p, a.b[h]);
+                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                    const float f = floorf(qv);
+                    int code = (int)f;
+                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
+                        code = INT_MIN;
+                        if (rbase + lane < a.N) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                    }
+                    out = (uint32_t)code;
+                }
+                tb[lane * 33 + j] = out;
+            }
+            __syncwarp();
+            const int h = h0 + c0 + lane;
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+                const long long row = rbase + r;
+                if (row < a.N && h < a.k) {
+                    const uint32_t val = tb[r * 33 + lane];
+                    if (a.proj) a.proj[row * a.k + h] = __uint_as_float(val);
+                    else a.codes[row * a.k + h] = (int32_t)val;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // both CTAs are done with TMEM (and the leader's MMAs with both CTAs' smem)
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+    }
+}
+
 }  // namespace
 
 // Dense hi/lo coefficient matrices on the device (once per params object and device).
@@ -383,6 +594,39 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     a.codes = codes;
     a.proj = proj;
     a.flags = d.flags;
+    // The CTA pair wins at 3xTF32 (C1: 5.36 vs 5.49 ms; C3 chunk 8.2 vs 11.6 ms) and at 1xTF32 for short
+    // K loops (C3: 7.35 vs 10.8 ms), but its converter relay costs more than it saves on long K loops
+    // at 1xTF32 (C1: 4.54 vs 3.77 ms), where the single-CTA kernel stays.
+    static const bool single = std::getenv("FASTLSH_K4_SINGLE") != nullptr;  // experiment knob, read once
+    if (!single && (precision == 3 || p->n <= 256)) {
+        CUtensorMap px, ph, pl;
+        if (!make_map(&px, X, N, p->n, 128) || !make_map(&ph, d.dense_hi, d.dense_kpad, p->n, 128) ||
+            !make_map(&pl, d.dense_lo, d.dense_kpad, p->n, 128))
+            return FASTLSH_EUNSUPPORTED;
+        const size_t psmem = (size_t)kPairStages * 4 * kHalfTile + 1024 + 512;  // = 12 x 16 KB at 1xTF32
+        static bool attr_done = false;
+        cudaError_t pe = cudaSuccess;
+        if (!attr_done) {
+            pe = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_pair_kernel),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+            if (pe != cudaSuccess) return set_cuda_error(pe);
+            attr_done = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * ((N + 255) / 256)), (unsigned)(d.dense_kpad / BN));
+        cfg.blockDim = dim3(kThreadsE);
+        cfg.dynamicSmemBytes = psmem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        pe = cudaLaunchKernelEx(&cfg, e2lsh_pair_kernel, px, ph, pl, a);
+        return pe == cudaSuccess ? FASTLSH_OK : set_cuda_error(pe);
+    }
     const size_t smem = 3 * kStageBytesE + 1024 + 256;  // 3 x 64 KB (3xTF32) or 6 x 32 KB (1xTF32)
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
