@@ -152,6 +152,13 @@ fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
  * params do not use K1j. EUNSUPPORTED when NVRTC fails (see fastlsh_params_jit_status). */
 fastlsh_status fastlsh_params_prepare(const fastlsh_params* p, const fastlsh_keys* keys, int32_t what);
 
+/* K1j diagnostic (no GPU needed): generate and compile, without loading, the variants selected by
+ * `what` — bit 0 codes, 1 projections, 2 codes + keys, 3 keys only, 4 codes + keys with multicast key
+ * stores (bits 2-4 need `keys`). EUNSUPPORTED when K1j does not apply or a compile fails (first
+ * NVRTC log lines in msg), EINVAL for bad arguments. */
+fastlsh_status fastlsh_params_jit_check(const fastlsh_params* p, const fastlsh_keys* keys, int32_t what,
+                                       double* compile_seconds, char* msg, int64_t msg_len);
+
 /* K1j diagnostics: total NVRTC compile time spent for these params and the last compile / load
  * error (empty when none); msg receives at most msg_len-1 bytes plus a NUL. */
 fastlsh_status fastlsh_params_jit_status(const fastlsh_params* p, double* compile_seconds, char* msg,

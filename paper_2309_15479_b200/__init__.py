@@ -21,7 +21,7 @@ EXPORTED = [
     "fastlsh_params_destroy", "fastlsh_params_export", "fastlsh_params_info", "fastlsh_params_packing",
     "fastlsh_params_row_packing",
     "fastlsh_params_upload", "fastlsh_params_set_kernel", "fastlsh_params_set_table_size",
-    "fastlsh_params_prepare", "fastlsh_params_jit_status",
+    "fastlsh_params_prepare", "fastlsh_params_jit_status", "fastlsh_params_jit_check",
     "fastlsh_hash", "fastlsh_project", "e2lsh_hash", "e2lsh_project", "fastlsh_keys_create",
     "fastlsh_keys_create_from_arrays", "fastlsh_keys_destroy", "fastlsh_keys_export",
     "fastlsh_build_keys", "fastlsh_hash_keys", "fastlsh_hash_keys_multicast", "fastlsh_tables_workspace",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
         "fastlsh_params_set_table_size": [P, i32],
         "fastlsh_params_prepare": [P, P, i32],
         "fastlsh_params_jit_status": [P, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, i64],
+        "fastlsh_params_jit_check": [P, P, i32, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, i64],
         "fastlsh_params_packing": [P, P, P, P, P, P, P],
         "fastlsh_params_row_packing": [P, P, P, P, P, P, P],
         "fastlsh_hash": [P, P, i64, P, P],
@@ -263,6 +264,17 @@ class Params:
         _check(self._lib.fastlsh_params_jit_status(self._h, ctypes.byref(sec), buf, len(buf)),
                "fastlsh_params_jit_status")
         return {"compile_seconds": sec.value, "error": buf.value.decode(errors="replace")}
+
+    def jit_check(self, keys=None, what: int = 0b11) -> float:
+        """K1j: generate + compile (no load, no GPU needed) the variants in `what` (bit 0 codes,
+        1 projections, 2 codes + keys, 3 keys only, 4 multicast keys); returns NVRTC seconds."""
+        sec = ctypes.c_double()
+        buf = ctypes.create_string_buffer(4096)
+        st = self._lib.fastlsh_params_jit_check(self._h, keys._h if keys is not None else None, int(what),
+                                                ctypes.byref(sec), buf, len(buf))
+        if st != OK:
+            raise FastLSHError(st, "fastlsh_params_jit_check: " + buf.value.decode(errors="replace")[:500])
+        return sec.value
 
     def set_table_size(self, K: int):
         """Pack hash blocks as whole tables of K hashes so keys are built inside the hashing kernel

@@ -711,6 +711,19 @@ fastlsh_status fastlsh_params_prepare(const fastlsh_params* p, const fastlsh_key
     return FASTLSH_OK;
 }
 
+fastlsh_status fastlsh_params_jit_check(const fastlsh_params* p, const fastlsh_keys* ks, int32_t what,
+                                       double* compile_seconds, char* msg, int64_t msg_len) {
+    if (!p || what < 0 || what > 31) return FASTLSH_EINVAL;
+    std::string log;
+    const fastlsh_status st = jit::compile_check(p, ks, what, compile_seconds, &log);
+    if (msg && msg_len > 0) {
+        const size_t n = log.size() < (size_t)msg_len - 1 ? log.size() : (size_t)msg_len - 1;
+        std::memcpy(msg, log.data(), n);
+        msg[n] = 0;
+    }
+    return st;
+}
+
 fastlsh_status fastlsh_params_jit_status(const fastlsh_params* p, double* compile_seconds, char* msg, int64_t msg_len) {
     if (!p) return FASTLSH_EINVAL;
     std::lock_guard<std::mutex> g(p->jit.mu);

@@ -282,6 +282,9 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
                       cudaStream_t stream, bool keys_mc = false);
 // compile (if needed) the variant a call with these arguments would use
 fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks);
+// generate + compile the selected variants without loading them (no GPU needed)
+fastlsh_status compile_check(const fastlsh_params* p, const fastlsh_keys* ks, int what, double* seconds,
+                             std::string* log);
 }  // namespace jit
 
 }  // namespace fastlsh

@@ -745,6 +745,33 @@ fastlsh_status prepare(const fastlsh_params* p, int mode, const fastlsh_keys* ks
     return get_variant(p, mode, ks, false, true, &st) ? FASTLSH_OK : st;
 }
 
+fastlsh_status compile_check(const fastlsh_params* p, const fastlsh_keys* ks, int what, double* seconds,
+                             std::string* log) {
+    // generate and compile (no module load: works without a GPU) every variant selected by `what`:
+    // bit 0 codes, 1 projections, 2 codes + keys, 3 keys only, 4 codes + keys with multicast stores
+    if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
+    const int warps = warps_for(p->n);
+    double total = 0;
+    for (int bit = 0; bit < 5; ++bit) {
+        if (!(what & (1 << bit))) continue;
+        const bool with_keys = bit >= 2;
+        if (with_keys && (!ks || !keys_fit(*p, ks))) return FASTLSH_EINVAL;
+        const fastlsh_keys* kk = with_keys ? ks : nullptr;
+        Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), kk ? kk->L : 0, kk ? kk->K : 0,
+               kk ? kk->r.data() : nullptr, warps, kNcb, bit == 1 ? 1 : 0, bit == 4 ? 1 : 0, bit == 3 ? 0 : 1};
+        std::vector<char> cubin;
+        std::string lg;
+        double sec = 0;
+        if (!compile_cubin(k1j_source(s), cubin, lg, &sec)) {
+            if (log) *log = "variant " + std::to_string(bit) + ": " + lg.substr(0, 2000);
+            return FASTLSH_EUNSUPPORTED;
+        }
+        total += sec;
+    }
+    if (seconds) *seconds = total;
+    return FASTLSH_OK;
+}
+
 fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
                       float* proj, const fastlsh_keys* ks, const uint64_t* dev_r, uint64_t* keys, int64_t ldk,
                       cudaStream_t stream, bool keys_mc) {

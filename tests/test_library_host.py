@@ -373,3 +373,16 @@ def test_row_packing_stage_classes(lib, n, dual):
     assert S % 32 == 0 and S0 == 32 * ((n + 31) // 32) + 32
     assert n1 == (n if dual else 0)
     assert (S0 + 16 + n1 <= S) if dual else (S0 <= S)
+
+
+@pytest.mark.parametrize("n,m,k,w,L,K", [(128, 16, 256, 4.0, 16, 16), (36, 5, 100, 1.5, 4, 20), (64, 1, 32, 0.75, 1, 32)])
+def test_jit_variants_compile(lib, n, m, k, w, L, K):
+    """Every K1j variant's generated source compiles for sm_100a (NVRTC, no GPU): codes, projections,
+    codes + keys, keys only, multicast keys; k % 32 == 0 (paired 3D code stores) and k % 32 != 0
+    (2D boxes), power-of-two and IEEE-division w, m = 1."""
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import fastlsh_arrays
+    idx, a, b = fastlsh_arrays(n, m, k, w, 5)
+    P = fl.Params.from_arrays(n, w, idx, a, b)
+    Kobj = fl.Keys.create(L, K, seed=2)
+    assert P.jit_check(Kobj, what=0b11111) > 0
