@@ -304,9 +304,10 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem"],
                     help="pin the hashing kernel (auto: K1j for n <= 128, else K1r)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl"],
-                    help="N > 1 key all-gather: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
-                         "multicast table (fused), nccl = all_gather_into_tensor after hashing; auto tries nvls")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl", "alltoall"],
+                    help="N > 1 key exchange: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
+                         "multicast table (fused all-gather), nccl = all_gather_into_tensor after hashing; auto tries "
+                         "nvls then nccl; alltoall = tables sharded by id (rank l %% G owns table l: G x less traffic)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1: wait for each step's key all-gather before the next step hashes")
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk (launch)")
@@ -381,8 +382,9 @@ def main():
                 raise
             ktable, nvls_why = None, f"{type(ex).__name__}: {ex}"
     nvls = ktable is not None
+    a2a = bool(Kobj) and world > 1 and args.exchange == "alltoall"
     gathered = (ktable.table if nvls else torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev)) \
-        if (Kobj and world > 1) else None
+        if (Kobj and world > 1 and not a2a) else None
     overlap = gathered is not None and not nvls and not args.no_overlap
     keys_bufs = [keys, torch.empty_like(keys)] if overlap else [keys]
     pending = []
@@ -413,6 +415,9 @@ def main():
             ea[0].record(stream)
         if nvls:
             ktable.handle.barrier()  # every rank's multicast key stores are complete and visible
+        elif a2a:
+            from paper_2309_15479_b200.distributed import alltoall_keys_by_table
+            alltoall_keys_by_table(kb, N_total)
         elif gathered is not None:
             if overlap:
                 for w in pending:
@@ -759,15 +764,16 @@ def main():
                          else "per chunk fastlsh_hash_keys (kernel as in roofline.kernel)") +
                         ((f"; keys written by K1j with multimem.st into every GPU's copy of the [L][N] table "
                           f"(NVSwitch multicast, symmetric memory), then one group barrier" if nvls else
+                          "; then the table-sharded NCCL all-to-all (rank l % G receives table l for all rows)" if a2a else
                           f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
-                "key_exchange": ("nvls" if nvls else "nccl") if world > 1 and Kobj else None,
+                "key_exchange": ("nvls" if nvls else "alltoall" if a2a else "nccl") if world > 1 and Kobj else None,
                 "nvls_unavailable": nvls_why, "nvls_selfcheck": nvls_check,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms),
                                  "hash_note": "sum over the step's chunk launches of the hashing kernel(s), CUDA events; "
                                               "with K1j each launch also writes the keys",
-                                 "allgather": statistics.mean(ag_ms) if gathered is not None else 0.0,
+                                 "allgather": statistics.mean(ag_ms) if (gathered is not None or a2a) else 0.0,
                                  "hash_max_over_ranks": hash_ms_max,
                                  "roofline_frac_from_hash": ((N * (4 * cfg.n + 4 * cfg.k + 8 * cfg.L) if jit else
                                                               N * cfg.k * cfg.m) / (statistics.mean(hash_ms) / 1e3) /

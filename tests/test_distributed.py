@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2309_15479_b200.distributed import allgather_keys, max_over_ranks, shard_rows
+from paper_2309_15479_b200.distributed import allgather_keys, alltoall_keys_by_table, max_over_ranks, shard_rows
 
 
 def _free_port():
@@ -62,6 +62,10 @@ def _worker(rank, world, port, q, N):
                 ok_layout = False  # unequal shards must refuse the unwaited form
             except ValueError:
                 pass
+        # the table-sharded exchange: this rank receives its tables (l % world == rank) for all rows
+        mine, tab = alltoall_keys_by_table(torch.from_numpy(local.copy()), N)
+        ok_layout = ok_layout and mine == [l for l in range(L) if l % world == rank]
+        ok_layout = ok_layout and np.array_equal(tab.numpy(), full[mine])
         m = max_over_ranks(1.0 + rank)
         q.put((rank, ok_layout, m))
     finally:
