@@ -270,6 +270,7 @@ struct Spec {
     int codes;           // mode 0: codes stored (1) or kept on chip, keys only (0)
 };
 std::string k1j_source(const Spec& s);
+bool pair_stores(int k);
 bool nvrtc_available();
 bool compile_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, double* seconds);
 // K1j can serve this params object (shape limits, NVRTC present, not disabled by FASTLSH_NO_JIT)

@@ -264,6 +264,13 @@ const char* kTileHead = R"FL(
 
 }  // namespace
 
+// paired code stores (3D tensor map) need k % 32 == 0; FASTLSH_JIT_NOPAIR=1 keeps the 2D boxes
+// (experiment knob, read once)
+bool pair_stores(int k) {
+    static const bool off = std::getenv("FASTLSH_JIT_NOPAIR") != nullptr;
+    return k % 32 == 0 && !off;
+}
+
 std::string k1j_source(const Spec& s) {
     const int nbx = (s.n + 31) / 32;
     const int nx = (s.n + 3) / 4 * 4;
@@ -407,7 +414,7 @@ std::string k1j_source(const Spec& s) {
     }
     // codes stored (codes / projections) or kept on chip (keys only): a compile-time choice of the variant
     const bool store = s.mode == 1 || s.codes;
-    const bool pair = s.k % 32 == 0;  // 256-byte row segments per store (see pair_end)
+    const bool pair = pair_stores(s.k);  // 256-byte row segments per store (see pair_end)
     if (keys) src += "        u64 s0, s1, s2;\n        const u32 live = row < a.N ? 1u : 0u;\n        u64* kp = a.keys + a.col0 + row;\n";
     char buf[160];
     for (int g = 0; g < groups; ++g) {
@@ -802,7 +809,7 @@ fastlsh_status launch(const fastlsh_params* p, const DeviceCopy& d, const float*
     CUtensorMap xmap, omap;
     if (!make_map(&xmap, X, N, p->n, true)) return FASTLSH_EUNSUPPORTED;
     if (out) {
-        const bool ok = p->k % 32 == 0 ? make_map3(&omap, out, N, p->k, proj != nullptr)
+        const bool ok = pair_stores(p->k) ? make_map3(&omap, out, N, p->k, proj != nullptr)
                                        : make_map(&omap, out, N, p->k, proj != nullptr);
         if (!ok) return FASTLSH_EUNSUPPORTED;
     } else {
