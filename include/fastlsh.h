@@ -57,7 +57,8 @@ typedef struct {
     int32_t rows_per_group;    /* rows staged together per pipeline stage                        */
     double bank_efficiency;    /* useful gathers / (lanes * slots) over all warps                 */
     int64_t conflict_wavefronts; /* extra smem wavefronts per row left by the scheduler          */
-    int32_t kernel;            /* hashing kernel for 16-B aligned X: 1 = shared-memory gather K1,
+    int32_t kernel;            /* hashing kernel for 16-B aligned X: 0 = generic K0 (n > 4400),
+                                  1 = shared-memory gather K1,
                                   2 = tensor-memory gather K1t,
                                   3 = row-major gather K1r,
                                   4 = params-specialised lane = row kernel K1j */
@@ -71,8 +72,9 @@ typedef struct {
  *   idx[i][j] = hi64(u64(philox(j,i,1)) * n),  a[i][j] = BoxMuller(philox(j,i,2)) as f32,
  *   b[i] = f32(w * u53(philox(0,i,3))) clamped to [0, w).
  * n, m, k >= 1; w finite and > 0; m > n is legal (sampling with replacement).
- * EINVAL otherwise. EUNSUPPORTED if n > 4400 (three 4-row stages of X must fit in 227 KB of
- * shared memory) or m > 16384. */
+ * EINVAL otherwise; EUNSUPPORTED if k * m > 2^31. Params with n > 4400 (a 4-row stage of X no longer
+ * fits in shared memory) or m > 16384 are served by the generic kernel K0 (global-memory gathers,
+ * correctness path; fastlsh_params_info reports kernel 0). */
 fastlsh_status fastlsh_params_create(int32_t n, int32_t m, int32_t k, float w, uint64_t seed,
                                      fastlsh_params** out);
 

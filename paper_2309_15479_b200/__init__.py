@@ -240,7 +240,7 @@ class Params:
                     offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
                     lane_hash=lh.reshape(HB, W, 32), block_h0=h0, block_kb=kb)
 
-    KERNELS = {1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}
+    KERNELS = {0: "K0", 1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}
 
     def set_kernel(self, kernel):
         """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t), "rows" (3, K1r) or

@@ -19,7 +19,7 @@ COMMON = [*os.environ.get("FASTLSH_NVCC_EXTRA", "").split(), "-O3", "-lineinfo",
 SOURCES = ["api.cu", "gather.cu", "gather_inst0.cu", "gather_inst1.cu", "gather_inst2.cu", "gather_inst3.cu",
            "gather_tmem.cu", "tables.cu", "query.cu", "transforms.cu", "keys.cu", "e2lsh_tcgen05.cu", "packer.cpp",
            "gather_rows.cu", "gather_rows_inst0.cu", "gather_rows_inst1.cu", "gather_rows_inst2.cu",
-           "gather_rows_inst3.cu", "gather_rows_inst4.cu", "gather_rows_inst5.cu", "rpacker.cpp", "jit.cpp", "probe.cu", "mc.cpp"]
+           "gather_rows_inst3.cu", "gather_rows_inst4.cu", "gather_rows_inst5.cu", "rpacker.cpp", "jit.cpp", "probe.cu", "mc.cpp", "generic.cu"]
 
 
 def _stale(out: str, deps) -> bool:

@@ -55,8 +55,8 @@ fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_para
     if (!out) return FASTLSH_EINVAL;
     *out = nullptr;
     if (n <= 0 || m <= 0 || k <= 0 || !valid_w(w)) return FASTLSH_EINVAL;
-    if (n > kMaxN) return FASTLSH_EUNSUPPORTED;       // two 4-row stages must fit in shared memory
-    if ((int64_t)m > (int64_t)kMaxSlots * 256) return FASTLSH_EUNSUPPORTED;
+    // beyond these, no specialised kernel packs the params and the generic K0 serves them
+    if ((int64_t)k * m > ((int64_t)1 << 31)) return FASTLSH_EUNSUPPORTED;  // host arrays, int offsets
     fastlsh_params* p = new (std::nothrow) fastlsh_params();
     if (!p) return FASTLSH_ENOMEM;
     p->n = n; p->m = m; p->k = k; p->w = w;
@@ -72,8 +72,15 @@ fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_para
     return FASTLSH_OK;
 }
 
+// params K1 / K1t / K1r can pack (shared-memory stages of 4 rows, <= kMaxSlots * 256 slots a hash)
+bool packable(const fastlsh_params* p) { return p->n <= kMaxN && (int64_t)p->m <= (int64_t)kMaxSlots * 256; }
+
 fastlsh_status ensure_packed(fastlsh_params* p) {
     if (p->packed) return FASTLSH_OK;
+    if (!packable(p)) {  // only the generic K0 (and K1j where it applies) will serve these params
+        p->packed = true;
+        return FASTLSH_OK;
+    }
     try {
         build_packing(*p, p->pack);
     } catch (...) {
@@ -160,6 +167,7 @@ fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const f
         fastlsh_status st = launch_gather_rows(p, d, X, N, codes, proj, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 3) return st;
     }
+    if (!packable(p)) return launch_generic(p, d, X, N, codes, proj, stream);
     return launch_gather(p, d, X, N, codes, proj, stream);
 }
 
@@ -278,7 +286,7 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
-    info->kernel = jit_selected(p) ? 4 : tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
+    info->kernel = jit_selected(p) ? 4 : !packable(p) ? 0 : tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
     info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
     info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
@@ -382,8 +390,8 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
         free_device_copy(d);
         return st;
     }
-    if (jit::applicable(*p) && ((st = upload_vec(&d.j_idx, p->idx, s)) != FASTLSH_OK ||
-                                (st = upload_vec(&d.j_a, p->a, s)) != FASTLSH_OK)) {
+    if ((jit::applicable(*p) || !packable(p)) &&  // canonical arrays: K1j's slow path, K0
+        ((st = upload_vec(&d.j_idx, p->idx, s)) != FASTLSH_OK || (st = upload_vec(&d.j_a, p->a, s)) != FASTLSH_OK)) {
         free_device_copy(d);
         return st;
     }

@@ -172,7 +172,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
 }
 
 bool keys_fusable(const fastlsh_params* p, const fastlsh_keys* ks) {
-    if (!p->packed || p->table_align != ks->K || (int64_t)ks->L * ks->K > p->k) return false;
+    if (!p->packed || p->pack.slots <= 0 || p->table_align != ks->K || (int64_t)ks->L * ks->K > p->k) return false;
     const Packing& pk = p->pack;
     for (int bl = 0; bl < pk.hash_blocks; ++bl) {
         if (pk.block_h0[bl] % ks->K) return false;

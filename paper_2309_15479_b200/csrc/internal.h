@@ -225,6 +225,9 @@ struct FusedKeys;
 fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                                   int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
                                   const FusedKeys* fk = nullptr);
+// generic.cu: K0, the fallback for params no specialised kernel can pack (n > kMaxN, huge m)
+fastlsh_status launch_generic(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
+                              float* proj, cudaStream_t stream);
 // the hashing dispatcher (api.cu): K1t when selected/applicable, else K1
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream);

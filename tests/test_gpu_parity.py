@@ -624,3 +624,24 @@ def test_fused_keys_only_chunked_equals_separate():
         codes, _ = fl.hash_keys(Pf, Kobj, X[c0:c1], keys_out=keys, with_codes=False, col0=c0)
         assert codes is None
     assert torch.equal(keys, ref)
+
+
+# ---- K0: the generic kernel for params no specialised kernel packs (n > 4400, huge m) -------------
+
+@pytest.mark.parametrize("N,n,m,k,w", [(257, 5000, 24, 33, 1.5), (40, 64, 20_000, 3, 4.0), (1, 8192, 7, 100, 0.5)])
+def test_generic_kernel_parity(N, n, m, k, w):
+    P, idx, a, b = _params(n, m, k, w, seed=N + n)
+    assert P.info()["kernel"] == 0
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + m)
+    X = torch.randn((N, n), generator=g, device="cuda")
+    _run_and_check(P, idx, a, b, w, X)
+    X[0, :] = float("nan")
+    fl.read_flags(P, reset=True)
+    codes = fl.fastlsh_hash(P, X).cpu().numpy()
+    assert (codes[0] == -(2 ** 31)).all()
+    assert fl.read_flags(P, reset=True) == (k, 0)
+    Kobj = fl.Keys.create(1, min(k, 3), seed=1)
+    c2, keys = fl.hash_keys(P, Kobj, X)
+    ref = okeys.build_keys(c2.cpu().numpy().astype(np.int64), Kobj.export(), 1, min(k, 3))
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), ref)
