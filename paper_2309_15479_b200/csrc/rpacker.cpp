@@ -321,7 +321,15 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     const double smem = (double)cl.NS * cl.R * cl.S * 4 + (double)cl.NC * cl.R * kbp * 4 + 1024;
     const int by_regs = 65536 / (W * 32 * regs), by_smem = (int)(227.0 * 1024 / smem);
     const int warps_sm = W * std::max(1, std::min(by_regs, by_smem));
-    const double rate = warps_sm >= 16 ? 0.98 : 0.98 * (0.6 + 0.4 * warps_sm / 16.0);
+    // rate factor at 8 warps/SM (16 warps: 1): round 1 fitted 0.8; the round-2 part sweep
+    // (profiles/r02_sweep_parts.txt) measured P=1 / MS=128 / 8 warps beating P=2 / MS=64 / 16 warps on
+    // C2 m=128 (21.5 vs 23.5 ms) and P=4 / 8 warps beating P=8 / 16 warps on m=512 (25.2 vs 26.6 ms);
+    // 0.87 picks the measured-best packing on every config (FASTLSH_RPACK_8W overrides, experiment knob)
+    static const double low = [] {
+        const char* e = std::getenv("FASTLSH_RPACK_8W");
+        return e ? std::atof(e) : 0.87;
+    }();
+    const double rate = warps_sm >= 16 ? 0.98 : 0.98 * (1.0 - 2.0 * (1.0 - low) * (1.0 - warps_sm / 16.0));
     // per-group costs (waits, epilogue, flush) ~ 97 wavefront-equivalents per warp and group,
     // fitted to C1 single (R = 8) vs dual (R = 4) copies and checked on C4 (model 0.877, measured
     // 0.884 for the dual/single time ratio)
