@@ -211,7 +211,7 @@ __device__ __noinline__ void fix_row(const JArgs& a, float* scr, long long row, 
             s2 += (rv >> 42) * u;
         }
         const u64 key = mod61(rl[0] + mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
-        if (row < a.N && !(FL_DEBUG & 1)) key_store(a.keys + l * a.ldk + a.col0 + row, key);
+        if (row < a.N) key_store(a.keys + l * a.ldk + a.col0 + row, key);
     }
 #endif
 }
@@ -299,10 +299,6 @@ std::string k1j_source(const Spec& s) {
     def("FL_L", s.L);
     def("FL_KT", s.K > 0 ? s.K : 1);
     def("FL_MC", s.mc ? 1 : 0);
-    {
-        const char* dbg = std::getenv("FASTLSH_JIT_DEBUG");  // experiment knob (tools/dbg_keys*.py)
-        def("FL_DEBUG", dbg ? std::atoi(dbg) : 0);
-    }
     // Quantisation: q = (p + b) / w. For w a power of two, 1/w is folded into the
     // coefficients and b: every fp32 step then carries an exact power-of-two scale, so
     // fma-chain(a/w) + b/w == RN(p + b) / w bit for bit (outside subnormal / overflow ranges) and the
