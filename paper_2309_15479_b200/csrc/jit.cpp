@@ -200,7 +200,10 @@ __device__ __noinline__ void fix_row(const JArgs& a, float* scr, long long row, 
     __syncwarp();
 #if FL_L > 0
     for (int l = lane; l < FL_L; l += 32) {
-        // the limb form of the generated code (exact for K <= 1024): S_q = sum limb_q(r) * u32(c)
+        // the limb form of the generated code (exact for K <= 1024): S_q = sum limb_q(r) * u32(c).
+        // (K1r's 128-bit lo/hi accumulation, written here first, gave wrong keys for K = 16 in this
+        // NVRTC-compiled noinline function while exact for K <= 3 — not root-caused; the limb form is
+        // the fast path's arithmetic and is verified by tests/test_gpu_jit.py flag tests.)
         const u64* rl = a.kr + l * (FL_KT + 1);
         u64 s0 = 0, s1 = 0, s2 = 0;
         for (int j = 0; j < FL_KT; ++j) {
