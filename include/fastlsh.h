@@ -61,7 +61,8 @@ typedef struct {
                                   1 = shared-memory gather K1,
                                   2 = tensor-memory gather K1t,
                                   3 = row-major gather K1r,
-                                  4 = params-specialised lane = row kernel K1j */
+                                  4 = params-specialised lane = row kernel K1j,
+                                  5 = dense 3xTF32 GEMM K4 on the merged coefficients */
     int32_t tmem_hash_blocks;  /* K1t: CTAs hash blocks (0 when K1t does not apply)              */
     int32_t tmem_hashes_per_warp; /* K1t: hashes (register accumulator pairs) per warp           */
 } fastlsh_params_info_t;
@@ -132,8 +133,9 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 /* Choose the hashing kernel of these params (all compute Eq. 5, with the same
  * epilogue; only the summation order of the fp32 projection differs, within the same bound):
- *   0 = automatic (default): the row-major gather K1r when its packing exists and its cost model
- *       beats K1's, for calls with n % 4 == 0 and X 16-byte aligned; else the shared-memory K1;
+ *   0 = automatic (default), first applicable of: the dense path (5) for n >= 512 and m >= n/8;
+ *       K1j (4); the row-major gather K1r when its packing exists and its cost model beats K1's,
+ *       for calls with n % 4 == 0 and X 16-byte aligned; K0 for params nothing else packs; else K1;
  *   1 = always the shared-memory gather K1 (column-interleaved stages, LDS.128);
  *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED);
  *   3 = always K1r (row-major stages, LDS.32; likewise EUNSUPPORTED when it cannot serve);
@@ -143,8 +145,14 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
  *       use and caches the module (per process, keyed by the generated source). Applies when
  *       n <= 128, n % 4 == 0, k % 4 == 0, k*m <= 16384 and libnvrtc can be loaded; calls need X
  *       and codes/proj 16-byte aligned. In automatic mode K1j is preferred wherever it applies
- *       (set FASTLSH_NO_JIT=1 to disable it).
- * EINVAL for other values; EUNSUPPORTED for 2, 3 or 4 when that kernel cannot serve the params. */
+ *       (set FASTLSH_NO_JIT=1 to disable it);
+ *   5 = always the dense path: Eq. 5 as one tcgen05 3xTF32 GEMM against the
+ *       coefficient matrix A[c][i] = sum of a_ij over the samples j of hash i with idx_ij = c
+ *       (duplicates merged in double, rounded once to f32; built on the first call per device,
+ *       kpad x n x 8 bytes), then the same epilogue (e2lsh_hash's kernel). In automatic mode it
+ *       serves n >= 512, m >= n/8 while that matrix is <= 1 GiB: there the gathers (N k m) cost
+ *       more than the GEMM (N k n MMA work on tensor cores). Needs n % 4 == 0, X 16-byte aligned.
+ * EINVAL for other values; EUNSUPPORTED for 2, 3, 4 or 5 when that kernel cannot serve the params. */
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
 
 /* K1j only: compile ahead of time the variants a later call will use, so that the first

@@ -240,12 +240,13 @@ class Params:
                     offp=offp.reshape(HB, W, MS // 2, 32), coef=coef.reshape(HB, W, MS, 32),
                     lane_hash=lh.reshape(HB, W, 32), block_h0=h0, block_kb=kb)
 
-    KERNELS = {0: "K0", 1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}
+    KERNELS = {0: "K0", 1: "K1", 2: "K1t", 3: "K1r", 4: "K1j", 5: "K4 dense"}
 
     def set_kernel(self, kernel):
-        """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t), "rows" (3, K1r) or
-        "jit" (4, K1j); see fastlsh_params_set_kernel. Returns self."""
-        code = {"auto": 0, "smem": 1, "tmem": 2, "rows": 3, "jit": 4}.get(kernel, kernel)
+        """Pin the hashing kernel: "auto" (0), "smem" (1, K1), "tmem" (2, K1t), "rows" (3, K1r),
+        "jit" (4, K1j) or "dense" (5, K4 on the merged coefficients); see fastlsh_params_set_kernel.
+        Returns self."""
+        code = {"auto": 0, "smem": 1, "tmem": 2, "rows": 3, "jit": 4, "dense": 5}.get(kernel, kernel)
         _check(self._lib.fastlsh_params_set_kernel(self._h, int(code)), "fastlsh_params_set_kernel")
         return self
 

@@ -75,10 +75,16 @@ fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_para
 // params K1 / K1t / K1r can pack (shared-memory stages of 4 rows, <= kMaxSlots * 256 slots a hash)
 bool packable(const fastlsh_params* p) { return p->n <= kMaxN && (int64_t)p->m <= (int64_t)kMaxSlots * 256; }
 
-fastlsh_status ensure_packed(fastlsh_params* p) {
-    if (p->packed) return FASTLSH_OK;
+// full = false: params the dense path will serve in auto mode skip the gather packings (seconds of
+// host work for large k*m); pinning a gather kernel or exporting a packing asks for them (full).
+fastlsh_status ensure_packed(fastlsh_params* p, bool full = false) {
+    if (p->packed && !(full && p->pack_skipped)) return FASTLSH_OK;
     if (!packable(p)) {  // only the generic K0 (and K1j where it applies) will serve these params
         p->packed = true;
+        return FASTLSH_OK;
+    }
+    if (!full && p->kernel == 0 && dense_shape(p)) {
+        p->packed = p->pack_skipped = true;
         return FASTLSH_OK;
     }
     try {
@@ -94,6 +100,7 @@ fastlsh_status ensure_packed(fastlsh_params* p) {
         return FASTLSH_ENOMEM;
     }
     p->packed = true;
+    p->pack_skipped = false;
     return FASTLSH_OK;
 }
 
@@ -153,8 +160,24 @@ bool rows_keys_pay(const fastlsh_params* p, const fastlsh_keys* ks) {
 bool jit_selected(const fastlsh_params* p) {
     return p->kernel == 4 || (p->kernel == 0 && jit::applicable(*p));
 }
+// K4 on the duplicates-merged coefficient matrix: Eq. 5 as a dense 3xTF32
+// tcgen05 GEMM, A[c][i] = sum_{j: idx_ij = c} a_ij. Serves the call when pinned (kernel 5) or, in auto
+// mode, for long rows sampled densely — n >= 512 and m >= n/8 — where the gathers cost more than the
+// GEMM (measured on C2, n = 4096: m = 512 K1r 25.2 vs dense 8.5 ms per 250k rows, m = 4096 17.4 vs
+// 0.88 ms per 20k rows; m = 128 K1r 21.5 vs 36.5 ms and C1 / C3 / C4 keep the gather kernels), and
+// only while the dense hi/lo matrices stay small (kpad * n * 8 bytes <= 1 GiB).
+bool dense_shape(const fastlsh_params* p) {
+    if (p->n % 4 || p->n < 512 || (int64_t)8 * p->m < p->n) return false;
+    const int64_t kpad = ((int64_t)p->k + 255) / 256 * 256;
+    return kpad * p->n * 8 <= ((int64_t)1 << 30);
+}
+bool dense_selected(const fastlsh_params* p) { return p->kernel == 5 || (p->kernel == 0 && dense_shape(p)); }
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
+    if (dense_selected(p)) {
+        fastlsh_status st = launch_e2lsh(p, const_cast<DeviceCopy&>(d), X, N, codes, proj, 3, stream);
+        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 5) return st;
+    }
     if (jit_selected(p)) {
         fastlsh_status st = jit::launch(p, d, X, N, codes, proj, nullptr, nullptr, nullptr, 0, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 4) return st;
@@ -167,7 +190,7 @@ fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const f
         fastlsh_status st = launch_gather_rows(p, d, X, N, codes, proj, stream);
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 3) return st;
     }
-    if (!packable(p)) return launch_generic(p, d, X, N, codes, proj, stream);
+    if (!packable(p) || !d.offp) return launch_generic(p, d, X, N, codes, proj, stream);
     return launch_gather(p, d, X, N, codes, proj, stream);
 }
 
@@ -286,7 +309,8 @@ fastlsh_status fastlsh_params_info(const fastlsh_params* cp, fastlsh_params_info
     info->rows_per_group = kRows;
     info->bank_efficiency = pk.efficiency;
     info->conflict_wavefronts = pk.conflict_wavefronts;
-    info->kernel = jit_selected(p) ? 4 : !packable(p) ? 0 : tmem_selected(p) ? 2 : rows_selected(p) ? 3 : 1;
+    info->kernel = dense_selected(p) ? 5 : jit_selected(p) ? 4 : !packable(p) ? 0 : tmem_selected(p) ? 2
+                   : rows_selected(p) ? 3 : 1;
     info->tmem_hash_blocks = p->tpack.ok ? p->tpack.HB : 0;
     info->tmem_hashes_per_warp = p->tpack.ok ? p->tpack.nhw : 0;
     return FASTLSH_OK;
@@ -299,7 +323,7 @@ fastlsh_status fastlsh_params_packing(const fastlsh_params* cp, int32_t* sizes, 
     fastlsh_params* p = const_cast<fastlsh_params*>(cp);
     {
         std::lock_guard<std::mutex> g(p->mu);
-        fastlsh_status st = ensure_packed(p);
+        fastlsh_status st = ensure_packed(p, true);
         if (st != FASTLSH_OK) return st;
     }
     const Packing& pk = p->pack;
@@ -322,7 +346,7 @@ fastlsh_status fastlsh_params_row_packing(const fastlsh_params* cp, int32_t* siz
     fastlsh_params* p = const_cast<fastlsh_params*>(cp);
     {
         std::lock_guard<std::mutex> g(p->mu);
-        fastlsh_status st = ensure_packed(p);
+        fastlsh_status st = ensure_packed(p, true);
         if (st != FASTLSH_OK) return st;
     }
     const RPacking& pk = p->rpack;
@@ -390,7 +414,7 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
         free_device_copy(d);
         return st;
     }
-    if ((jit::applicable(*p) || !packable(p)) &&  // canonical arrays: K1j's slow path, K0
+    if ((jit::applicable(*p) || !packable(p) || p->pack_skipped) &&  // canonical arrays: K1j's slow path, K0
         ((st = upload_vec(&d.j_idx, p->idx, s)) != FASTLSH_OK || (st = upload_vec(&d.j_a, p->a, s)) != FASTLSH_OK)) {
         free_device_copy(d);
         return st;
@@ -408,13 +432,21 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
-    if (!p || kernel < 0 || kernel > 4) return FASTLSH_EINVAL;
+    if (!p || kernel < 0 || kernel > 5) return FASTLSH_EINVAL;
     std::lock_guard<std::mutex> g(p->mu);
-    fastlsh_status st = ensure_packed(p);
+    const bool gather = kernel >= 1 && kernel <= 3;
+    if (gather && p->pack_skipped) {
+        // the gather packings were skipped (dense-path shape): build them now, unless a device copy
+        // without them exists already
+        for (int i = 0; i < kMaxDevices; ++i)
+            if (p->dev[i].ready) return FASTLSH_ESTATE;
+    }
+    fastlsh_status st = ensure_packed(p, gather);
     if (st != FASTLSH_OK) return st;
     if (kernel == 2 && !p->tpack.ok) return FASTLSH_EUNSUPPORTED;
     if (kernel == 3 && !p->rpack.ok) return FASTLSH_EUNSUPPORTED;
     if (kernel == 4 && !jit::applicable(*p)) return FASTLSH_EUNSUPPORTED;
+    if (kernel == 5 && p->n % 4) return FASTLSH_EUNSUPPORTED;  // K4's K-major tensor maps
     p->kernel = kernel;
     return FASTLSH_OK;
 }
@@ -659,6 +691,12 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
     int dev = 0;
     fastlsh_status st = ready_params(p, &dev);
     if (st != FASTLSH_OK) return st;
+    // dense path (kernel 5): codes from the GEMM, keys from them (keys only needs a gather kernel)
+    if (codes && dense_selected(p)) {
+        st = fastlsh_hash(p, X, N, codes, stream);
+        if (st != FASTLSH_OK) return st;
+        return fastlsh_build_keys(ks, codes, N, p->k, keys_out, ldk, stream);
+    }
     // K1j: codes and keys in one launch, keys accumulated in registers; codes optional
     if (jit_selected(p)) {
         const uint64_t* dr = nullptr;
@@ -798,7 +836,8 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;
     }
-    const bool fuse = want_keys && keys_fusable(p, ks) && !tmem_selected(p);
+    const bool dense = dense_selected(p);  // the GEMM makes the codes, K3 the keys
+    const bool fuse = want_keys && !dense && keys_fusable(p, ks) && !tmem_selected(p);
     const int64_t nchunks = (N + chunk_rows - 1) / chunk_rows;
     for (int64_t c = 0; c < nchunks; ++c) {
         const int b = (int)(c & 1);
@@ -814,7 +853,7 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
             fused_here = st == FASTLSH_OK;
             if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
         }
-        if (!fused_here && want_keys && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
+        if (!fused_here && want_keys && !dense && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
             rows_keys_pay(p, ks)) {
             FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
             st = launch_gather_rows(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);

@@ -51,7 +51,62 @@ struct E2Args {
     int32_t* codes;
     float* proj;
     unsigned long long* flags;
+    // FastLSH params on the dense path: canonical [k][m] samples and coefficients and the raw X rows,
+    // for the exact re-evaluation of flagged elements (null for E2LSH params: the GEMM is the definition)
+    const int* idx;
+    const float* ca;
+    int m;
+    const float* X;
 };
+
+// A FastLSH hash sees only its sampled coordinates. The merged-coefficient GEMM
+// multiplies every coordinate, so a non-finite coordinate no hash i samples still turns 0 * inf into
+// NaN for hash i, and the fp32 rounding near |q| = 2^31 differs from a gather's. Elements the GEMM
+// flags (non-finite or out-of-int32 quotient; non-finite projections) are therefore re-evaluated here
+// as the gather itself — p = fma-chain over the m samples in the paper's order — before the flag is
+// final. Rare by construction; the flagged lane alone, global loads.
+__device__ __forceinline__ float gather_projection(const E2Args& a, long long row, int h) {
+    const float* x = a.X + row * a.n;
+    const int* id = a.idx + (long long)h * a.m;
+    const float* co = a.ca + (long long)h * a.m;
+    float p = __fmul_rn(x[id[0]], co[0]);
+    for (int j = 1; j < a.m; ++j) p = __fmaf_rn(x[id[j]], co[j], p);
+    return p;
+}
+
+// The flagged elements of one lane's 32-hash chunk (bit j: hash h0 + j of row `row`), after the
+// chunk's fast pass wrote INT32_MIN / the raw projection into tb: re-evaluate (FastLSH params), count
+// what stays flagged. Inlined in a cold branch after the unrolled loop (a real call costs the ABI's
+// register saves and doubled C1's epilogue time).
+__device__ __forceinline__ void fix_flagged(const E2Args& a, uint32_t* tb, uint32_t bits, int h0, long long row,
+                                        bool w_pow2, float inv_w) {
+    if (row >= a.N) return;  // rows past N are never stored
+    while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int h = h0 + j;
+        if (a.proj) {  // only FastLSH params flag projections (non-finite): the gather decides
+            tb[j] = __float_as_uint(gather_projection(a, row, h));
+            continue;
+        }
+        float qv = 0.0f, f = 0.0f;
+        bool ok = false;
+        if (a.idx) {
+            const float p = gather_projection(a, row, h);
+            qv = w_pow2 ? __fmul_rn(__fadd_rn(p, a.b[h]), inv_w) : __fdiv_rn(__fadd_rn(p, a.b[h]), a.w);
+            f = floorf(qv);
+            ok = f > -2147483648.0f && f < 2147483648.0f;
+        } else {
+            qv = __uint_as_float(tb[j]);  // E2LSH params: the GEMM's quotient, kept by the fast pass
+        }
+        if (ok) {
+            tb[j] = (uint32_t)(int)f;
+        } else {
+            atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+            tb[j] = 0x80000000u;
+        }
+    }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -259,24 +314,30 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
             uint32_t v[32];
             tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * BN + c0), v);
             if (h0 + c0 >= a.k) break;
+            uint32_t bad = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int h = h0 + c0 + j;
                 const float p = __uint_as_float(v[j]);
                 uint32_t out = v[j];
-                if (!a.proj && h < a.k) {
-                    const float num = __fadd_rn(p, a.b[h]);
-                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
-                    const float f = floorf(qv);
-                    int code = (int)f;
-                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
-                        code = INT_MIN;
-                        if (rbase + lane < a.N) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                if (h < a.k) {
+                    if (!a.proj) {
+                        const float num = __fadd_rn(p, a.b[h]);
+                        const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                        const float f = floorf(qv);
+                        if (f > -2147483648.0f && f < 2147483648.0f) {
+                            out = (uint32_t)(int)f;
+                        } else {
+                            bad |= 1u << j;
+                            out = __float_as_uint(qv);  // fix_flagged decides
+                        }
+                    } else if (a.idx && !isfinite(p)) {
+                        bad |= 1u << j;
                     }
-                    out = (uint32_t)code;
                 }
                 tb[lane * 33 + j] = out;
             }
+            if (bad) fix_flagged(a, tb + lane * 33, bad, h0 + c0, rbase + lane, w_pow2, inv_w);
             __syncwarp();
             const int h = h0 + c0 + lane;
 #pragma unroll 4
@@ -497,24 +558,30 @@ e2lsh_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
             uint32_t v[32];
             tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
             if (h0 + c0 >= a.k) break;
+            uint32_t bad = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int h = h0 + c0 + j;
                 const float p = __uint_as_float(v[j]);
                 uint32_t out = v[j];
-                if (!a.proj && h < a.k) {
-                    const float num = __fadd_rn(p, a.b[h]);
-                    const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
-                    const float f = floorf(qv);
-                    int code = (int)f;
-                    if (!(f > -2147483648.0f && f < 2147483648.0f)) {
-                        code = INT_MIN;
-                        if (rbase + lane < a.N) atomicAdd(a.flags + (isfinite(qv) ? 1 : 0), 1ull);
+                if (h < a.k) {
+                    if (!a.proj) {
+                        const float num = __fadd_rn(p, a.b[h]);
+                        const float qv = w_pow2 ? __fmul_rn(num, inv_w) : __fdiv_rn(num, w);
+                        const float f = floorf(qv);
+                        if (f > -2147483648.0f && f < 2147483648.0f) {
+                            out = (uint32_t)(int)f;
+                        } else {
+                            bad |= 1u << j;
+                            out = __float_as_uint(qv);  // fix_flagged decides
+                        }
+                    } else if (a.idx && !isfinite(p)) {
+                        bad |= 1u << j;
                     }
-                    out = (uint32_t)code;
                 }
                 tb[lane * 33 + j] = out;
             }
+            if (bad) fix_flagged(a, tb + lane * 33, bad, h0 + c0, rbase + lane, w_pow2, inv_w);
             __syncwarp();
             const int h = h0 + c0 + lane;
 #pragma unroll 4
@@ -568,6 +635,22 @@ static fastlsh_status ensure_dense(const fastlsh_params* p, DeviceCopy& d) {
         return set_cuda_error(e);
     }
     d.dense_kpad = kpad;
+    // FastLSH params: the canonical arrays for the exact re-evaluation of flagged elements
+    if (!p->is_e2lsh && !d.j_idx) {
+        int32_t* di = nullptr;
+        float* da = nullptr;
+        const size_t km = (size_t)p->k * p->m;
+        e = cudaMalloc(reinterpret_cast<void**>(&di), km * 4);
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&da), km * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(di, p->idx.data(), km * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(da, p->a.data(), km * 4, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(di); cudaFree(da);
+            return set_cuda_error(e);
+        }
+        d.j_idx = di;
+        d.j_a = da;
+    }
     return FASTLSH_OK;
 }
 
@@ -575,7 +658,7 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
                             float* proj, int precision, cudaStream_t stream) {
     if (p->n % 4 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
     {
-        std::lock_guard<std::mutex> g(const_cast<fastlsh_params*>(p)->mu);
+        std::lock_guard<std::mutex> g(const_cast<fastlsh_params*>(p)->dense_mu);
         fastlsh_status st = ensure_dense(p, d);
         if (st != FASTLSH_OK) return st;
     }
@@ -594,6 +677,10 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     a.codes = codes;
     a.proj = proj;
     a.flags = d.flags;
+    a.idx = p->is_e2lsh ? nullptr : d.j_idx;
+    a.ca = p->is_e2lsh ? nullptr : d.j_a;
+    a.m = p->m;
+    a.X = X;
     // The CTA pair wins at 3xTF32 (C1: 5.36 vs 5.49 ms; C3 chunk 8.2 vs 11.6 ms) and at 1xTF32 for short
     // K loops (C3: 7.35 vs 10.8 ms), but its converter relay costs more than it saves on long K loops
     // at 1xTF32 (C1: 4.54 vs 3.77 ms), where the single-CTA kernel stays.
@@ -604,13 +691,15 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
             !make_map(&pl, d.dense_lo, d.dense_kpad, p->n, 128))
             return FASTLSH_EUNSUPPORTED;
         const size_t psmem = (size_t)kPairStages * 4 * kHalfTile + 1024 + 512;  // = 12 x 16 KB at 1xTF32
-        static bool attr_done = false;
-        cudaError_t pe = cudaSuccess;
-        if (!attr_done) {
+        static bool attr_done[kMaxDevices] = {};  // the attribute is per device
+        int dev = 0;
+        cudaError_t pe = cudaGetDevice(&dev);
+        if (pe != cudaSuccess) return set_cuda_error(pe);
+        if (!attr_done[dev]) {
             pe = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_pair_kernel),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
             if (pe != cudaSuccess) return set_cuda_error(pe);
-            attr_done = true;
+            attr_done[dev] = true;
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(2 * ((N + 255) / 256)), (unsigned)(d.dense_kpad / BN));

@@ -69,6 +69,7 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
                              int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
                              const FusedKeys* fk) {
     const Packing& pk = p->pack;
+    if (!d.offp) return FASTLSH_EUNSUPPORTED;  // packing skipped at upload (dense-path shape)
     const int landing_row = ((4 * p->n + 15) / 16) * 16;
     int tma = (p->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     const int fused = (fk && fk->keys) ? 1 : 0;  // codes may be null: keys only

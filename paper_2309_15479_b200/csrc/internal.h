@@ -181,10 +181,13 @@ struct fastlsh_params {
     fastlsh::TPacking tpack;
     fastlsh::RPacking rpack;
     bool packed = false;
-    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 K1, 2 TMEM K1t, 3 row-major K1r, 4 K1j
+    bool pack_skipped = false; // auto mode on a dense-path shape: K1 / K1t / K1r packings built on demand
+    int32_t kernel = 0;        // fastlsh_params_set_kernel: 0 auto, 1 K1, 2 TMEM K1t, 3 row-major K1r, 4 K1j,
+                               // 5 dense K4 on merged coefficients
     int32_t table_align = 1;   // hash blocks hold whole tables of this many hashes (fused keys)
     fastlsh::DeviceCopy dev[fastlsh::kMaxDevices];
     std::mutex mu;
+    std::mutex dense_mu;       // guards DeviceCopy::dense_* (built on the first dense call; mu may be held)
     mutable fastlsh::jit::State jit;
 };
 
@@ -251,6 +254,8 @@ fastlsh_status launch_normalize(const float* X, long long N, int n, float* out, 
 fastlsh_status launch_max_norm(const float* X, long long N, int n, float* kappa, cudaStream_t s);
 fastlsh_status launch_mips(const float* X, long long N, int n, const float* kappa, int is_query, float* out,
                            cudaStream_t s);
+// api.cu: params the dense path (K4 on merged coefficients) serves in automatic mode
+bool dense_shape(const fastlsh_params* p);
 // e2lsh_tcgen05.cu
 fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N,
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);
