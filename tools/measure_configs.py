@@ -74,12 +74,18 @@ def main():
         rec = {"config": name, "m": m, "rows": N, "n": c.n, "k": c.k, "note": note,
                "t_roof_ms": t_roof * 1e3, "bound": "smem" if t_smem >= t_hbm else "hbm"}
         info = P.info()
+        if info["kernel"] == 5:
+            P.row_packing()  # builds the gather packings (reported below) without leaving auto mode
+            info = P.info()
         rec["packing"] = {kk: info[kk] for kk in ("parts", "slots", "warps_per_block", "hash_blocks",
                                                   "bank_efficiency")}
         rp = P.row_packing()
         if rp is not None:
             rec["row_packing"] = {kk: rp[kk] for kk in ("parts", "slots", "warps", "hash_blocks", "S", "n1")}
-        rec["auto_kernel"] = {1: "K1", 2: "K1t", 3: "K1r", 4: "K1j"}[info["kernel"]]
+        rec["auto_kernel"] = fl.Params.KERNELS[info["kernel"]]
+        ms = timed(lambda: fl.fastlsh_hash(P, X, out=codes), iters)  # the automatic choice (fastlsh_hash)
+        rec["auto"] = {"kernel": rec["auto_kernel"], "ms": ms, "hashes_per_s": N * c.k / (ms / 1e3),
+                       "roofline_frac": t_roof / (ms / 1e3)}
         for kern, key in (("jit", "K1j"), ("rows", "K1r"), ("smem", "K1"), ("tmem", "K1t")):
             try:
                 P.set_kernel(kern)
