@@ -45,9 +45,11 @@ def _peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
         return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "bf16_tflops": float(d.get("bf16_tflops", 2250.0)),
                 "source": "measured (MEASURED_PEAKS.json: copy bandwidth, burst)"}
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "bf16_tflops": 2250.0,
+                "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -206,6 +208,9 @@ def _config_dict(cfg, world, n_rank=None, n_total=None, chunks=1, strong=None):
 
 
 def _kernel_name(info, fused):
+    if info["kernel"] == 5:
+        return ("e2lsh_pair_kernel (kernel 5: 3xTF32 tcgen05 GEMM on the duplicates-merged coefficients)" +
+                (" + keys_kernel" if fused else ""))
     if info["kernel"] == 4:
         return ("k1j (K1j fastlsh_hash_keys: params-specialised lane = row kernel, codes + keys in one launch)"
                 if fused else "k1j (K1j fastlsh_hash: params-specialised lane = row kernel)")
@@ -219,6 +224,8 @@ def _launches_per_call(P, info, Kobj) -> int:
     launch; otherwise hash + the key kernel."""
     if Kobj is None or info["kernel"] == 4:
         return 1
+    if info["kernel"] == 5:
+        return 2  # the GEMM, then the key kernel on its codes
     rp = P.row_packing() if info["kernel"] == 3 else None
     if rp is not None and rp["hash_blocks"] == 1 and \
             Kobj.L * Kobj.K <= 0.75 * rp["hash_blocks"] * rp["warps"] * rp["slots"]:
@@ -228,6 +235,10 @@ def _launches_per_call(P, info, Kobj) -> int:
 
 def _packing_summary(P, info):
     """The GPU layout of the kernel that ran."""
+    if info["kernel"] == 5:
+        return {"kernel": "K4 dense (kernel 5)", "precision": "3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulate)",
+                "A": f"[{(P.k + 255) // 256 * 256} x {P.n}] merged coefficients, hi/lo split",
+                "tile": "CTA pair (cta_group::2), 256 rows x 256 hashes, TMEM accumulators"}
     if info["kernel"] == 4:
         return {"kernel": "K1j", "lane": "row (32 rows per warp, row in registers)",
                 "code": "S_i register operands, a_i / b_i / 1/w immediates (NVRTC, sm_100a)",
@@ -265,8 +276,18 @@ def _roofline(cfg, info, fused, N_launch, t_launch_s, step_ms, peaks, with_codes
     hbm_ns = 4.0 * N_launch * cfg.n + (4.0 * N_launch * cfg.k if with_codes else 0.0)
     t_roof = max(hbm_ns / (peaks["hbm_gbs"] * 1e9), gathers / g_peak)
     t_roof_nominal = max(hbm_ns / 8.0e12, gathers / g_peak)
-    kern = "K1j" if info["kernel"] == 4 else {1: "K1", 2: "K1t", 3: "K1r"}[info["kernel"]]
-    if info["kernel"] == 4:
+    kern = {1: "K1", 2: "K1t", 3: "K1r", 4: "K1j", 5: "K4dense"}[info["kernel"]]
+    if info["kernel"] == 5:
+        # the contraction X[N x n] . A[n x k]: algorithmic flops 2 N k n (the 3xTF32 emulation issues
+        # three TF32 MMAs per product: mma_work); peak = TF32 dense = the measured bf16 peak x 1/2 (the
+        # nominal tf32 : bf16 ratio, B200_PROFILING.md)
+        flops = 2.0 * N_launch * cfg.k * cfg.n
+        tf32_peak = peaks["bf16_tflops"] * 0.5 * 1e12
+        r = {"bound": "tensor", "achieved": flops / t_launch_s / 1e12, "peak": tf32_peak / 1e12, "unit": "TFLOP/s",
+             "frac": flops / t_launch_s / tf32_peak,
+             "mma_work_frac": 3 * flops / t_launch_s / tf32_peak,
+             "algorithmic_per_launch": {"flops": flops, "hbm_bytes": hbm_ns, "rows": N_launch, "gathers": gathers}}
+    elif info["kernel"] == 4:
         alg = hbm_ns + (8.0 * N_launch * cfg.L if (fused and cfg.L) else 0.0)
         r = {"bound": "hbm", "achieved": alg / t_launch_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
              "frac": alg / t_launch_s / (peaks["hbm_gbs"] * 1e9),
@@ -301,8 +322,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=4.0, help="reference arm: oracle seconds per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem"],
-                    help="pin the hashing kernel (auto: K1j for n <= 128, else K1r)")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem", "dense"],
+                    help="pin the hashing kernel (auto: dense for n >= 512 and m >= n/8, K1j for n <= 128, else K1r)")
+    ap.add_argument("--m", type=int, default=None, help="override the config's m (C2's m sweep: 32, 128, 512, 4096)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl", "alltoall"],
                     help="N > 1 key exchange: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
@@ -321,6 +343,9 @@ def main():
 
     from fastlsh_inputs import configs
     cfg = configs.get(args.config)
+    if args.m is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, m=args.m)
     if args.impl == "reference":
         run_reference(args, cfg)
         return
