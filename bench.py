@@ -104,7 +104,16 @@ def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("FASTLSH_BENCH_SHARE_GPU") == "1":  # functional smoke test of the N > 1 path on one GPU
+        local = 0
     return world, rank, local
+
+
+def _backend():
+    """NCCL (the product path). FASTLSH_BENCH_BACKEND=gloo only for the one-GPU functional smoke test of
+    the N > 1 orchestration (tools/gpu_multirank_smoke.sh): host-staged collectives, no rank's kernel
+    waits on another's; such a run's timings are not bench numbers."""
+    return os.environ.get("FASTLSH_BENCH_BACKEND", "nccl")
 
 
 def _cores():
@@ -324,7 +333,10 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
     ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem", "dense"],
                     help="pin the hashing kernel (auto: dense for n >= 512 and m >= n/8, K1j for n <= 128, else K1r)")
-    ap.add_argument("--m", type=int, default=None, help="override the config's m (C2's m sweep: 32, 128, 512, 4096)")
+    ap.add_argument("--sample-dims", type=int, default=None,
+                    help="override the config's m, the sampled dimensions per hash (C2's sweep: 32, 128, 512, 4096)")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="override the config's N (smoke tests; the JSON's config.workload states the rows used)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl", "alltoall"],
                     help="N > 1 key exchange: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
@@ -343,9 +355,9 @@ def main():
 
     from fastlsh_inputs import configs
     cfg = configs.get(args.config)
-    if args.m is not None:
+    if args.sample_dims is not None or args.rows is not None:
         import dataclasses
-        cfg = dataclasses.replace(cfg, m=args.m)
+        cfg = dataclasses.replace(cfg, m=args.sample_dims or cfg.m, N=args.rows or cfg.N)
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -363,7 +375,10 @@ def main():
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _backend() == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(_backend())
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
@@ -546,6 +561,22 @@ def main():
                                               "16-byte vector stream (fastlsh_bandwidth_probe)",
                                    "ms": pms}
         del scratch
+
+    # exchange check (N > 1, all-gather / NVLS): every rank re-hashes the first rows of the NEXT rank's
+    # shard itself (regenerated from the seed) and compares their keys with the columns the exchange
+    # delivered into its gathered table: bit-exact, since the kernels are deterministic
+    exchange_check = None
+    if world > 1 and gathered is not None:
+        nr = (rank + 1) % world
+        rlo, rhi = shard_rows(N_total, world, nr) if strong else (nr * cfg.N, (nr + 1) * cfg.N)
+        nck = min(rhi - rlo, 2048)
+        Xr = data.generate(cfg.data, cfg.n, rlo, rlo + nck, seed=cfg.seed, device=dev)
+        _, kref = fl.hash_keys(P, Kobj, Xr)
+        torch.cuda.synchronize()
+        okx = torch.tensor([1 if torch.equal(gathered[:, rlo:rlo + nck], kref) else 0], device=dev)
+        dist.all_reduce(okx, op=dist.ReduceOp.MIN)
+        exchange_check = {"rows_checked_per_rank": nck, "source_rank": "rank + 1", "ok": bool(okx.item())}
+        del Xr, kref
 
     # parity sample of the timed step's own output (the last chunk's codes, the keys of those rows),
     # copied out now, before any side measurement reuses the buffers; checked in the CPU leg below
@@ -793,7 +824,7 @@ def main():
                           f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
                 "key_exchange": ("nvls" if nvls else "alltoall" if a2a else "nccl") if world > 1 and Kobj else None,
-                "nvls_unavailable": nvls_why, "nvls_selfcheck": nvls_check,
+                "nvls_unavailable": nvls_why, "nvls_selfcheck": nvls_check, "exchange_check": exchange_check,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms),
                                  "hash_note": "sum over the step's chunk launches of the hashing kernel(s), CUDA events; "

@@ -31,8 +31,8 @@ def allgather_keys(keys_local, out=None, group=None, wait=True, n_total=None):
     staging buffer and compacted into `out` on the current stream after the collective.
     n_total defaults to world * N_local (equal shards). Returns `out`, or (wait=False) the list of
     pending works: the caller waits on them later (on NCCL that makes its current stream wait),
-    e.g. after overlapping the next step's hashing; with unequal shards the compaction then
-    happens inside wait=True calls only, so wait=False requires equal shards.
+    e.g. after overlapping the next step's hashing; with unequal shards the one pending object's
+    wait() also does the compaction (so the staging buffer lives until then).
     """
     import torch
     import torch.distributed as dist
@@ -57,19 +57,34 @@ def allgather_keys(keys_local, out=None, group=None, wait=True, n_total=None):
         for w in works:
             w.wait()
         return out
-    if not wait:
-        raise ValueError("unequal shards: the compaction after the all-gather needs wait=True")
     n_max = -(-n_total // world)
     pad = torch.zeros((L, n_max), dtype=keys_local.dtype, device=keys_local.device)
     pad[:, :n_local].copy_(keys_local)
     staged = torch.empty((L, world * n_max), dtype=keys_local.dtype, device=keys_local.device)
     works = [dist.all_gather_into_tensor(staged[l], pad[l], group=group, async_op=True) for l in range(L)]
-    for w in works:
-        w.wait()
-    for r in range(world):
-        a, b = shard_rows(n_total, world, r)
-        out[:, a:b].copy_(staged[:, r * n_max:r * n_max + (b - a)])
+    pending = _CompactingWait(works, staged, out, n_total, world, n_max)
+    if not wait:
+        return [pending]
+    pending.wait()
     return out
+
+
+class _CompactingWait:
+    """The pending all-gather of unequal shards: wait() waits for the collectives, then compacts the
+    padded blocks into `out` (on the caller's current stream, as an NCCL work's wait orders it)."""
+
+    def __init__(self, works, staged, out, n_total, world, n_max):
+        self.works, self.staged, self.out = works, staged, out
+        self.n_total, self.world, self.n_max = n_total, world, n_max
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for r in range(self.world):
+            a, b = shard_rows(self.n_total, self.world, r)
+            self.out[:, a:b].copy_(self.staged[:, r * self.n_max:r * self.n_max + (b - a)])
+        self.works = []
+        return True
 
 
 def table_owner(l: int, world: int) -> int:

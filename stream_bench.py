@@ -36,7 +36,10 @@ def main(args, cfg):
     world, rank, local = bench._dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if bench._backend() == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(bench._backend())
     dev = torch.device("cuda", local)
     batches = args.batches or cfg.batches
     B = cfg.N                     # rows per batch (whole job)

@@ -49,19 +49,13 @@ def _worker(rank, world, port, q, N):
         out = allgather_keys(torch.from_numpy(local.copy()), n_total=N)
         full = okeys.build_keys(codes, r, L, K).view(np.int64)
         ok_layout = np.array_equal(out.numpy(), full)
-        if N % world == 0:
-            # the bench's overlapped form: works returned unwaited, waited before the buffer is reused
-            out2 = torch.zeros_like(out)
-            works = allgather_keys(torch.from_numpy(local.copy()), out=out2, wait=False)
-            for w in works:
-                w.wait()
-            ok_layout = ok_layout and len(works) == L and np.array_equal(out2.numpy(), full)
-        else:
-            try:
-                allgather_keys(torch.from_numpy(local.copy()), wait=False, n_total=N)
-                ok_layout = False  # unequal shards must refuse the unwaited form
-            except ValueError:
-                pass
+        # the bench's overlapped form: works returned unwaited, waited before the buffer is reused
+        # (unequal shards: one pending object whose wait() also compacts the padded blocks)
+        out2 = torch.zeros_like(out)
+        works = allgather_keys(torch.from_numpy(local.copy()), out=out2, wait=False, n_total=N)
+        for w in works:
+            w.wait()
+        ok_layout = ok_layout and len(works) == (L if N % world == 0 else 1) and np.array_equal(out2.numpy(), full)
         # the table-sharded exchange: this rank receives its tables (l % world == rank) for all rows
         mine, tab = alltoall_keys_by_table(torch.from_numpy(local.copy()), N)
         ok_layout = ok_layout and mine == [l for l in range(L) if l % world == rank]
