@@ -338,12 +338,14 @@ def main():
     ap.add_argument("--rows", type=int, default=None,
                     help="override the config's N (smoke tests; the JSON's config.workload states the rows used)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "nccl", "alltoall"],
-                    help="N > 1 key exchange: nvls = multimem stores from the K1j epilogue into a symmetric-memory "
-                         "multicast table (fused all-gather), nccl = all_gather_into_tensor after hashing; auto tries "
-                         "nvls then nccl; alltoall = tables sharded by id (rank l %% G owns table l: G x less traffic)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "alltoall", "allgather", "nccl", "nvls"],
+                    help="N > 1 key exchange. alltoall (auto): the tables are sharded by id, rank l %% G gathers "
+                         "table l's keys of all rows (one NCCL all_to_all_single, (G-1)/G of the rank's own keys in "
+                         "and out); allgather (= nccl): every rank receives the whole [L][N] table "
+                         "(all_gather_into_tensor per table; measured beside alltoall as allgather_variant); nvls: "
+                         "multimem stores from the K1j epilogue into a symmetric-memory multicast table")
     ap.add_argument("--no-overlap", action="store_true",
-                    help="N > 1: wait for each step's key all-gather before the next step hashes")
+                    help="N > 1: wait for each step's key exchange before the next step hashes")
     ap.add_argument("--chunk-rows", type=int, default=8_388_608, help="C3: rows hashed per chunk (launch)")
     ap.add_argument("--no-tables", action="store_true", help="skip the bucket-table build and query measurements")
     ap.add_argument("--queries", type=int, default=10_000, help="queries answered in the query measurement")
@@ -412,22 +414,29 @@ def main():
     # all-gather is one group barrier. Otherwise (no multicast / not K1j): NCCL all-gather, where the
     # all-gather of step j runs on NCCL's stream while step j+1 hashes into the other keys buffer
     # (double-buffered); step j+1 waits for it before launching its own all-gather.
+    # Exchange (N > 1). Every GPU receiving the whole [L][N] key table (all-gather) costs each GPU's
+    # NVLink ingress (G-1)/G of 8 L N bytes per step whatever the transport (NCCL or NVLS multicast):
+    # 22.4 GB at C3, G = 8, >= 25 ms at 900 GB/s against ~8.4 ms of hashing. Sharding the tables by id
+    # (the builder of table l receives table l's keys of all rows) cuts that G-fold, so it is the
+    # default; the full all-gather is measured beside it (allgather_variant). Both overlap step j's
+    # exchange with step j+1's hashing (double-buffered keys) unless --no-overlap.
+    exchange = None
+    if Kobj and world > 1:
+        exchange = {"auto": "alltoall", "nccl": "allgather"}.get(args.exchange, args.exchange)
     ktable, nvls_why = None, None
-    if Kobj and world > 1 and jit and args.exchange != "nccl":
+    if exchange == "nvls":
         from paper_2309_15479_b200.distributed import KeyTable
-        try:
-            ktable = KeyTable(cfg.L, N_total, device=dev, mode="nvls")  # raises (allocating nothing) without multicast
-        except Exception as ex:  # noqa: BLE001 (fall back to NCCL; reported in the JSON)
-            if args.exchange == "nvls":
-                raise
-            ktable, nvls_why = None, f"{type(ex).__name__}: {ex}"
+        if not jit:
+            raise SystemExit("--exchange nvls needs the K1j kernel (n <= 128)")
+        ktable = KeyTable(cfg.L, N_total, device=dev, mode="nvls")  # raises (allocating nothing) without multicast
     nvls = ktable is not None
-    a2a = bool(Kobj) and world > 1 and args.exchange == "alltoall"
+    a2a = exchange == "alltoall"
     gathered = (ktable.table if nvls else torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev)) \
-        if (Kobj and world > 1 and not a2a) else None
-    overlap = gathered is not None and not nvls and not args.no_overlap
+        if exchange in ("allgather", "nvls") else None
+    overlap = (gathered is not None or a2a) and not nvls and not args.no_overlap
     keys_bufs = [keys, torch.empty_like(keys)] if overlap else [keys]
     pending = []
+    a2a_last = []  # (owned tables, their keys for all rows) of the last table-sharded exchange
     step_no = [0]
     fused = bool(Kobj)  # fastlsh_hash_keys: one launch where K1j / K1r-tile keys apply, else hash + keys
     ev = []
@@ -457,7 +466,11 @@ def main():
             ktable.handle.barrier()  # every rank's multicast key stores are complete and visible
         elif a2a:
             from paper_2309_15479_b200.distributed import alltoall_keys_by_table
-            alltoall_keys_by_table(kb, N_total)
+            if overlap:
+                drain()
+                pending[:] = alltoall_keys_by_table(kb, N_total, wait=False)
+            else:
+                a2a_last[:] = alltoall_keys_by_table(kb, N_total)
         elif gathered is not None:
             if overlap:
                 for w in pending:
@@ -471,7 +484,9 @@ def main():
 
     def drain():
         for w in pending:
-            w.wait()
+            r = w.wait()
+            if isinstance(r, tuple):  # the table-sharded exchange: (owned tables, their keys)
+                a2a_last[:] = r
         pending.clear()
 
     smi_index = local
@@ -566,14 +581,19 @@ def main():
     # shard itself (regenerated from the seed) and compares their keys with the columns the exchange
     # delivered into its gathered table: bit-exact, since the kernels are deterministic
     exchange_check = None
-    if world > 1 and gathered is not None:
+    if world > 1 and (gathered is not None or a2a_last):
         nr = (rank + 1) % world
         rlo, rhi = shard_rows(N_total, world, nr) if strong else (nr * cfg.N, (nr + 1) * cfg.N)
         nck = min(rhi - rlo, 2048)
         Xr = data.generate(cfg.data, cfg.n, rlo, rlo + nck, seed=cfg.seed, device=dev)
         _, kref = fl.hash_keys(P, Kobj, Xr)
         torch.cuda.synchronize()
-        okx = torch.tensor([1 if torch.equal(gathered[:, rlo:rlo + nck], kref) else 0], device=dev)
+        if gathered is not None:
+            got = gathered[:, rlo:rlo + nck]
+        else:  # table-sharded: this rank holds tables l % world == rank for all rows
+            mine, tab = a2a_last
+            got, kref = tab[:, rlo:rlo + nck], kref[mine]
+        okx = torch.tensor([1 if torch.equal(got, kref) else 0], device=dev)
         dist.all_reduce(okx, op=dist.ReduceOp.MIN)
         exchange_check = {"rows_checked_per_rank": nck, "source_rank": "rank + 1", "ok": bool(okx.item())}
         del Xr, kref
@@ -587,6 +607,41 @@ def main():
                "keys": ((gathered[:, lo + c0p + pri] if nvls else keys_bufs[(step_no[0] - 1) % len(keys_bufs)][:, c0p + pri])
                         .cpu().numpy().view(np.uint64) if Kobj is not None else None),
                "proj": fl.fastlsh_project(P, X[c0p:c1p][pri].contiguous()).cpu().numpy()}
+
+    # side measurement (N > 1, table-sharded default): the same step with the full key all-gather
+    # (every GPU receives the whole [L][N] table), overlapped the same way; max over ranks
+    allgather_variant = None
+    if a2a:
+        try:
+            a2a, gathered, overlap = False, torch.empty((cfg.L, N_total), dtype=torch.int64, device=dev), \
+                not args.no_overlap
+            keys_bufs[:] = [keys, torch.empty_like(keys)] if overlap else [keys]
+            for _ in range(2):
+                step(False)
+            drain()
+            torch.cuda.synchronize()
+            dist.barrier()
+            va = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            nvs = max(2, min(args.steps, 5))
+            va[0].record(stream)
+            for _ in range(nvs):
+                step(False)
+            drain()
+            va[1].record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            vt = torch.tensor([va[0].elapsed_time(va[1]) / nvs], dtype=torch.float64, device=dev)
+            dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+            allgather_variant = {"ms_per_step": float(vt[0]), "value": N_total * cfg.k / (float(vt[0]) / 1e3),
+                                 "steps": nvs, "exchange": "NCCL all_gather_into_tensor per table, every GPU "
+                                 "receives the whole [L][N] table; overlapped with the next step's hashing"
+                                 if overlap else "NCCL all_gather_into_tensor per table, serial"}
+        except Exception as ex:  # noqa: BLE001
+            allgather_variant = {"error": f"{type(ex).__name__}: {ex}"}
+        finally:
+            a2a, gathered = True, None
+            keys_bufs[:] = keys_bufs[:1]
+            torch.cuda.empty_cache()
 
     # side measurement: keys only (codes never leave the SM; K1j / K1r code tile), same chunks
     keys_only = None
@@ -820,10 +875,11 @@ def main():
                          else "per chunk fastlsh_hash_keys (kernel as in roofline.kernel)") +
                         ((f"; keys written by K1j with multimem.st into every GPU's copy of the [L][N] table "
                           f"(NVSwitch multicast, symmetric memory), then one group barrier" if nvls else
-                          "; then the table-sharded NCCL all-to-all (rank l % G receives table l for all rows)" if a2a else
+                          "; then the table-sharded NCCL all-to-all (rank l % G receives table l for all rows, "
+                          f"{'overlapped with the next step' if not args.no_overlap else 'serial'})" if a2a else
                           f"; then the NCCL key all-gather ({'overlapped with the next step' if overlap else 'serial'})")
                          if world > 1 else ""),
-                "key_exchange": ("nvls" if nvls else "alltoall" if a2a else "nccl") if world > 1 and Kobj else None,
+                "key_exchange": exchange, "allgather_variant": allgather_variant,
                 "nvls_unavailable": nvls_why, "nvls_selfcheck": nvls_check, "exchange_check": exchange_check,
                 "keys_only": keys_only,
                 "breakdown_ms": {"hash": statistics.mean(hash_ms),

@@ -92,7 +92,7 @@ def table_owner(l: int, world: int) -> int:
     return l % world
 
 
-def alltoall_keys_by_table(keys_local, n_total: int, group=None):
+def alltoall_keys_by_table(keys_local, n_total: int, group=None, wait=True):
     """The table-sharded alternative to the all-gather ("an all-to-all by table,
     G x less ingress"): table l goes to rank l % G, which receives every rank's rows of it.
 
@@ -101,7 +101,9 @@ def alltoall_keys_by_table(keys_local, n_total: int, group=None):
     holding them for ALL rows in global row order. Per rank the traffic is (G-1)/G of its own keys
     out and the same amount in, instead of (G-1)/G of the whole [L][N] table in (all-gather): at
     C3, G = 8, 2.8 GB vs 22.4 GB per rank and step. One all_to_all_single with split sizes (NCCL on
-    GPUs, gloo in the CPU tests), then a local reorder of the received blocks.
+    GPUs, gloo in the CPU tests), then a local reorder of the received blocks. wait=False returns
+    [pending] instead: pending.wait() finishes the collective, does the reorder (on the caller's
+    current stream) and returns (tables, keys) — the bench overlaps it with the next step's hashing.
     """
     import torch
     import torch.distributed as dist
@@ -120,15 +122,34 @@ def alltoall_keys_by_table(keys_local, n_total: int, group=None):
     mine = owned[rank]
     out_splits = [len(mine) * (b - a) for a, b in sizes]
     recv = torch.empty(sum(out_splits), dtype=keys_local.dtype, device=keys_local.device)
-    dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=out_splits, input_split_sizes=in_splits,
-                           group=group)
-    out = torch.empty((len(mine), n_total), dtype=keys_local.dtype, device=keys_local.device)
-    off = 0
-    for r, (a, b) in enumerate(sizes):
-        blk = recv[off:off + len(mine) * (b - a)].view(len(mine), b - a)
-        out[:, a:b].copy_(blk)
-        off += len(mine) * (b - a)
-    return mine, out
+    work = dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=out_splits,
+                                  input_split_sizes=in_splits, group=group, async_op=True)
+    pending = _ReorderWait(work, recv, send, mine, sizes, n_total)
+    return [pending] if not wait else pending.wait()
+
+
+class _ReorderWait:
+    """The pending table-sharded exchange: wait() waits for the all-to-all, then places each source
+    rank's block of the owned tables at its global rows; returns (tables, keys)."""
+
+    def __init__(self, work, recv, send, mine, sizes, n_total):
+        self.work, self.recv, self.send, self.mine, self.sizes, self.n_total = work, recv, send, mine, sizes, n_total
+        self.result = None
+
+    def wait(self):
+        import torch
+        if self.result is not None:
+            return self.result
+        self.work.wait()
+        mine, recv = self.mine, self.recv
+        out = torch.empty((len(mine), self.n_total), dtype=recv.dtype, device=recv.device)
+        off = 0
+        for a, b in self.sizes:
+            out[:, a:b].copy_(recv[off:off + len(mine) * (b - a)].view(len(mine), b - a))
+            off += len(mine) * (b - a)
+        self.result = (mine, out)
+        self.send = self.recv = None
+        return self.result
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:

@@ -60,6 +60,9 @@ def _worker(rank, world, port, q, N):
         mine, tab = alltoall_keys_by_table(torch.from_numpy(local.copy()), N)
         ok_layout = ok_layout and mine == [l for l in range(L) if l % world == rank]
         ok_layout = ok_layout and np.array_equal(tab.numpy(), full[mine])
+        (pend,) = alltoall_keys_by_table(torch.from_numpy(local.copy()), N, wait=False)  # the overlapped form
+        mine2, tab2 = pend.wait()
+        ok_layout = ok_layout and mine2 == mine and np.array_equal(tab2.numpy(), full[mine])
         m = max_over_ranks(1.0 + rank)
         q.put((rank, ok_layout, m))
     finally:
