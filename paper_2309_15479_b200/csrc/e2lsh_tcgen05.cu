@@ -57,6 +57,10 @@ struct E2Args {
     const float* ca;
     int m;
     const float* X;
+    // grid raster: 1 = hash tiles fastest (blockIdx.x), row tiles in blockIdx.y, so the CTAs resident
+    // together share their X tiles through L2 (X is read from HBM once instead of kpad/256 times);
+    // 0 = row tiles in blockIdx.x (more than 65535 row tiles)
+    int hash_fast;
 };
 
 // A FastLSH hash sees only its sampled coordinates. The merged-coefficient GEMM
@@ -194,8 +198,8 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStagesE + 1);
     constexpr int kConvThreads = kThreadsE - 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long m0 = (long long)blockIdx.x * BM;
-    const int h0 = blockIdx.y * BN;
+    const long long m0 = (long long)(a.hash_fast ? blockIdx.y : blockIdx.x) * BM;
+    const int h0 = (a.hash_fast ? blockIdx.x : blockIdx.y) * BN;
     const int KB = (a.n + BK - 1) / BK;
 
     const uint32_t sbase = smem_u32(smem);
@@ -448,8 +452,9 @@ e2lsh_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_consta
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const long long m0 = (long long)(blockIdx.x >> 1) * 256 + rank * 128;  // this CTA's 128 rows
-    const int h0 = blockIdx.y * BN;                                        // the pair's 256 hashes
+    // the cluster pairs blockIdx.x 2j, 2j+1: j is the hash tile (hash_fast) or the row-tile pair
+    const long long m0 = (long long)(a.hash_fast ? blockIdx.y : (blockIdx.x >> 1)) * 256 + rank * 128;  // this CTA's 128 rows
+    const int h0 = (int)(a.hash_fast ? (blockIdx.x >> 1) : blockIdx.y) * BN;  // the pair's 256 hashes
     const int hb = h0 + (int)rank * 128;                                   // this CTA's 128 of them
     const int KB = (a.n + BK - 1) / BK;
 
@@ -702,7 +707,10 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
             attr_done[dev] = true;
         }
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(2 * ((N + 255) / 256)), (unsigned)(d.dense_kpad / BN));
+        const long long pairs = (N + 255) / 256;
+        a.hash_fast = pairs <= 65535 ? 1 : 0;
+        cfg.gridDim = a.hash_fast ? dim3((unsigned)(2 * (d.dense_kpad / BN)), (unsigned)pairs)
+                                  : dim3((unsigned)(2 * pairs), (unsigned)(d.dense_kpad / BN));
         cfg.blockDim = dim3(kThreadsE);
         cfg.dynamicSmemBytes = psmem;
         cfg.stream = stream;
@@ -720,7 +728,10 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e);
-    dim3 grid((unsigned)((N + BM - 1) / BM), (unsigned)(d.dense_kpad / BN));
+    const long long tiles = (N + BM - 1) / BM;
+    a.hash_fast = tiles <= 65535 ? 1 : 0;
+    dim3 grid = a.hash_fast ? dim3((unsigned)(d.dense_kpad / BN), (unsigned)tiles)
+                            : dim3((unsigned)tiles, (unsigned)(d.dense_kpad / BN));
     e2lsh_tcgen05_kernel<<<grid, kThreadsE, smem, stream>>>(mx, mh, ml, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e);
