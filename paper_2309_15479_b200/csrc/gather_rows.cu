@@ -77,14 +77,17 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     for (int bl = 0; bl < pk.hash_blocks; ++bl)
         if ((pk.block_h0[bl] % 4) || (pk.block_kb[bl] % 4)) blocks_aligned = false;
     a.vec = (p->k % 4 == 0) && blocks_aligned && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
-    if (std::getenv("FASTLSH_NO_VEC_STORE")) a.vec = 0;  // experiment knob (and fallback test)
+    if (std::getenv("FASTLSH_NO_VEC_STORE")) a.vec = 0;  // fallback-path test knob: read per call (the test toggles it)
     a.kr = fk ? fk->r : nullptr;
     a.L = fk ? fk->L : 0;
     a.K = fk ? fk->K : 1;
     a.keys = fk ? fk->keys : nullptr;
     a.ldk = fk ? fk->ldk : 0;
-    a.debug = 0;
-    if (const char* e = std::getenv("FASTLSH_K1R_DEBUG")) a.debug = std::atoi(e);  // experiment knob
+    static const int debug = [] {  // experiment knob, read once
+        const char* e = std::getenv("FASTLSH_K1R_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.debug = debug;
 
     // resident CTAs per device: queried once per (params, device, shared-memory size) — at C0's
     // 10^4 rows the attribute + occupancy queries per call cost as much as the kernel

@@ -322,7 +322,7 @@ std::string k1j_source(const Spec& s) {
     // One hash as one inline-PTX block: p in the paper's slot order with immediate coefficients,
     // then (codes) p + b, * 1/w or / w, floor. NVVM does not re-optimise asm: with plain C++
     // expressions the front end took ~14 s for the C3 shape, as asm ~2 s.
-    auto hash_asm = [&](int i, int j) {
+    auto hash_asm = [&](int i, const std::string& cj) {
         const int32_t* id = s.idx + (size_t)i * s.m;
         const float* co = s.a + (size_t)i * s.m;
         std::vector<int> ops;  // distinct coordinates -> asm operand numbers %1 ...
@@ -336,7 +336,6 @@ std::string k1j_source(const Spec& s) {
         const char* P = s.mode == 0 ? "q" : "%0";
         const float scale = (s.mode == 0 && p2) ? 1.0f / s.w : 1.0f;
         char buf[112];
-        const std::string cj = "c" + std::to_string(j & 3);
         std::string h = s.mode == 0 ? "asm(\"{ .reg .f32 q; " : "{ float p; asm(\"";
         for (int t = 0; t < s.m; ++t) {
             const float c = co[t] * scale;  // exact: power-of-two scale
@@ -414,6 +413,13 @@ std::string k1j_source(const Spec& s) {
     // codes stored (codes / projections) or kept on chip (keys only): a compile-time choice of the variant
     const bool store = s.mode == 1 || s.codes;
     const bool pair = pair_stores(s.k);  // 256-byte row segments per store (see pair_end)
+    // quads of codes (4 per lane) computed before the wait for the pair box; FASTLSH_JIT_LATEWAIT
+    // overrides (experiment knob). C3 chunk, codes + keys (tools/mb_jit.py): D = 0 2.70-2.72 ms, 1 2.63,
+    // 2 2.59, 3 2.56, 4 2.58, 5 2.53, 6 2.51-2.52, 7 2.50, 8 (the whole group) 2.64 ms
+    static const int late_depth = [] {
+        const char* e = std::getenv("FASTLSH_JIT_LATEWAIT");
+        return e ? std::atoi(e) : 7;
+    }();
     if (keys) src += "        u64 s0, s1, s2;\n        const u32 live = row < a.N ? 1u : 0u;\n        u64* kp = a.keys + a.col0 + row;\n";
     char buf[160];
     for (int g = 0; g < groups; ++g) {
@@ -423,14 +429,27 @@ std::string k1j_source(const Spec& s) {
             src += "        {\n            group_begin(lane);\n"
                    "            unsigned char* box = cring + cbi * 4096 + lane * 128;\n";
         else
-            src += std::string("        {\n") + ((g & 1) ? "" : "            pair_begin(lane);\n") +
+            src += std::string("        {\n") + ((g & 1) || late_depth > 0 ? "" : "            pair_begin(lane);\n") +
                    "            unsigned char* box = cring + lane * 256 + " + std::to_string((g & 1) * 128) + ";\n"
                    "            const u32 swp = (u32)((2 * lane + " + std::to_string(g & 1) + ") & 7) << 4;\n";
-        for (int q = 0; q < 8 && 32 * g + 4 * q < s.k; ++q) {
-            src += "            { int c0, c1, c2, c3;\n";
+        // late wait (paired stores): the first D quads of a pair's first group are computed before the
+        // wait for the pair box, their codes held in registers (e<q>_<r>), then stored
+        const int nq = std::min(8, (s.k - 32 * g + 3) / 4);
+        const int D = (store && pair && !(g & 1)) ? std::min(late_depth, nq) : 0;
+        if (D) {
+            src += "            int";
+            for (int q = 0; q < D; ++q)
+                for (int r = 0; r < 4; ++r) src += std::string(q || r ? ", " : " ") + "e" + std::to_string(q) + "_" + std::to_string(r);
+            src += ";\n";
+        }
+        auto cname = [&](int q, int r) {
+            return q < D ? "e" + std::to_string(q) + "_" + std::to_string(r) : "c" + std::to_string(r);
+        };
+        for (int q = 0; q < nq; ++q) {
+            if (q >= D) src += "            { int c0, c1, c2, c3;\n";
             for (int j = 4 * q; j < 4 * q + 4; ++j) {
                 const int i = 32 * g + j;
-                src += "              " + hash_asm(i, j);
+                src += "              " + hash_asm(i, cname(q, j & 3));
                 if (keys && i < s.L * s.K) {
                     // key term (R9): the three 21-bit limbs of r[l][jj+1] (instruction
                     // immediates) times u32(code), exact 64-bit sums; S0 starts at r[l][0]
@@ -442,8 +461,8 @@ std::string k1j_source(const Spec& s) {
                         src += buf;
                     }
                     std::snprintf(buf, sizeof buf,
-                                  " { const u64 u = (u32)c%d; s0 += 0x%llxull * u; s1 += 0x%llxull * u; s2 += 0x%llxull * u; }",
-                                  j & 3, (unsigned long long)(r & 0x1fffff), (unsigned long long)((r >> 21) & 0x1fffff),
+                                  " { const u64 u = (u32)%s; s0 += 0x%llxull * u; s1 += 0x%llxull * u; s2 += 0x%llxull * u; }",
+                                  cname(q, j & 3).c_str(), (unsigned long long)(r & 0x1fffff), (unsigned long long)((r >> 21) & 0x1fffff),
                                   (unsigned long long)(r >> 42));
                     src += buf;
                     // key = (S0 + S1*2^21 + S2*2^42) mod 2^61-1 with S0 = r0 + ...: for K < 256, S1, S2 <
@@ -458,8 +477,17 @@ std::string k1j_source(const Spec& s) {
                 }
                 src += "\n";
             }
-            src += store ? "              put4(box, " + std::to_string(q) + (pair ? "u, swp" : "u, sw") + ", c0, c1, c2, c3); }\n"
-                         : "              (void)c0; (void)c1; (void)c2; (void)c3; }\n";
+            if (q < D) {
+                if (q == D - 1) {
+                    src += "              pair_begin(lane);\n";  // the box is needed only now
+                    for (int qq = 0; qq < D; ++qq)
+                        src += "              put4(box, " + std::to_string(qq) + "u, swp, " + cname(qq, 0) + ", " + cname(qq, 1) +
+                               ", " + cname(qq, 2) + ", " + cname(qq, 3) + ");\n";
+                }
+            } else {
+                src += store ? "              put4(box, " + std::to_string(q) + (pair ? "u, swp" : "u, sw") + ", c0, c1, c2, c3); }\n"
+                             : "              (void)c0; (void)c1; (void)c2; (void)c3; }\n";
+            }
         }
         if (!store)
             src += "        }\n";
@@ -756,13 +784,13 @@ fastlsh_status compile_check(const fastlsh_params* p, const fastlsh_keys* ks, in
     // generate and compile (no module load: works without a GPU) every variant selected by `what`:
     // bit 0 codes, 1 projections, 2 codes + keys, 3 keys only, 4 codes + keys with multicast stores
     if (!applicable(*p)) return FASTLSH_EUNSUPPORTED;
-    const int warps = warps_for(p->n);
     double total = 0;
     for (int bit = 0; bit < 5; ++bit) {
         if (!(what & (1 << bit))) continue;
         const bool with_keys = bit >= 2;
         if (with_keys && (!ks || !keys_fit(*p, ks))) return FASTLSH_EINVAL;
         const fastlsh_keys* kk = with_keys ? ks : nullptr;
+        const int warps = warps_for(p->n);
         Spec s{p->n, p->m, p->k, p->w, p->idx.data(), p->a.data(), p->b.data(), kk ? kk->L : 0, kk ? kk->K : 0,
                kk ? kk->r.data() : nullptr, warps, kNcb, bit == 1 ? 1 : 0, bit == 4 ? 1 : 0, bit == 3 ? 0 : 1};
         std::vector<char> cubin;
