@@ -392,7 +392,11 @@ RowKernelFn row_kernel_for(int cls) {
         case 3: return rows_kernel<MS, 3>;
         case 4: return rows_kernel<MS, 4>;
         case 5: return rows_kernel<MS, 5>;
-        default: return rows_kernel<MS, 6>;
+        case 6: return rows_kernel<MS, 6>;
+        default:
+            // class 7 serves 16-warp packings only (MS <= 64: the launch bounds' register cap)
+            if constexpr (MS <= 64) return rows_kernel<MS, 7>;
+            else return nullptr;
     }
 }
 

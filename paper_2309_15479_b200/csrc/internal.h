@@ -92,10 +92,12 @@ struct RClass { int S, R, NS, NC, D; };  // D: code-ring flush lag (gather_rows.
 // Classes 0-2 (n <= 128 / 256 / 512) stage a full second copy (n1 = n); classes 3-5 one copy.
 constexpr RClass kRClasses[] = {{320, 8, 3, 5, 3}, {576, 8, 4, 6, 5}, {1088, 8, 3, 5, 4}, {1056, 8, 3, 6, 5},
                                 {2080, 4, 4, 8, 7}, {4128, 4, 3, 3, 2},
-                                {2080, 8, 2, 4, 3}};
+                                {2080, 8, 2, 4, 3}, {4128, 6, 2, 2, 1}};
 constexpr int kRDualClasses = 3;
 constexpr int kRDualMaxN[kRDualClasses] = {128, 256, 512};
-constexpr int kNumRClasses = 7;  // class 6: 8-row dual stages for rows up to ~1000 words
+// class 6: 8-row dual stages for rows up to ~1000 words; class 7: 6-row stages of rows up to 4096
+// words for 16-warp packings (rpacker.cpp)
+constexpr int kNumRClasses = 8;
 struct RPacking {
     bool ok = false;
     int parts = 1, slots = 0, warps = 0, hash_blocks = 0, kb_max = 0, S = 0, cls = 0;

@@ -316,8 +316,19 @@ void try_rows(const fastlsh_params& p, int P, int Wmax, bool capped, RPacking& o
     // 16-warp packings 0.78-0.90 (C1, C4 P=2, C2 m=128 P=4), 8-warp ones 0.69-0.74 (C4 P=1, C2
     // m=128 P=1) -> 8 warps/SM cost a factor 0.8
     const int regs = MS <= 24 ? 85 : MS <= 40 ? 102 : MS <= 64 ? 128 : 255;
-    const RClass cl = kRClasses[pk.cls];
     const int kbp = (pk.kb_max + 3) & ~3;
+    // rows longer than 2048 words at 16 warps per CTA: 6-row stages (class 7, 2 x 99 KB) instead of
+    // 4-row ones (class 5, 3 x 66 KB): a third fewer per-group costs and 6 independent LDS per slot.
+    // C2 m = 32 (P = 1, MS = 36): 6.37 -> 5.47 ms. Measured no gain with parts (C2 m = 128, P = 2,
+    // MS = 64: 23.5 ms class 5, 23.2 class 7 — the model would credit it and pick it over the better
+    // P = 1 / 8-warp packing, 21.5 ms) and a loss at 8 warps (MS = 128: 22.9-23.8 ms with class 7's
+    // 2-deep ring): one-part 16-warp packings only.
+    if (pk.cls == 5 && W >= 16 && MS <= 64 && P == 1) {
+        const RClass c7 = kRClasses[7];
+        const double s7 = (double)c7.NS * c7.R * c7.S * 4 + (double)c7.NC * c7.R * kbp * 4 + 2048 + kbp * 4;
+        if (s7 <= 227.0 * 1024) pk.cls = 7;
+    }
+    const RClass cl = kRClasses[pk.cls];
     const double smem = (double)cl.NS * cl.R * cl.S * 4 + (double)cl.NC * cl.R * kbp * 4 + 1024;
     const int by_regs = 65536 / (W * 32 * regs), by_smem = (int)(227.0 * 1024 / smem);
     const int warps_sm = W * std::max(1, std::min(by_regs, by_smem));
