@@ -332,7 +332,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense E2LSH comparator")
     ap.add_argument("--kernel", default="auto", choices=["auto", "jit", "rows", "smem", "dense"],
-                    help="pin the hashing kernel (auto: dense for n >= 512 and m >= n/8, K1j for n <= 128, else K1r)")
+                    help="pin the hashing kernel (auto: K1j for n <= 128, else K1r; dense = kernel 5, opt-in analysis)")
     ap.add_argument("--sample-dims", type=int, default=None,
                     help="override the config's m, the sampled dimensions per hash (C2's sweep: 32, 128, 512, 4096)")
     ap.add_argument("--rows", type=int, default=None,
@@ -790,6 +790,30 @@ def main():
             del At, bt
         except Exception as ex:  # noqa: BLE001
             dense["cublas_error"] = str(ex)
+        # analysis only: the same FastLSH params as the 3xTF32 GEMM on the
+        # duplicates-merged coefficient matrix (kernel 5, opt-in). Not the graded path: north_star
+        # reserves the tensor cores for the E2LSH baseline, so the automatic choice never takes it.
+        if cfg.n % 4 == 0 and cfg.n >= 512 and info["kernel"] != 5:
+            try:
+                Pm = fl.Params.create(cfg.n, cfg.m, cfg.k, cfg.w, seed=cfg.seed)
+                Pm.set_kernel("dense")
+                fl.fastlsh_hash(Pm, Xd, out=cd)
+                d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                d0.record(stream)
+                for _ in range(3):
+                    fl.fastlsh_hash(Pm, Xd, out=cd)
+                d1.record(stream)
+                torch.cuda.synchronize()
+                ms = d0.elapsed_time(d1) / 3
+                dense["merged_fastlsh"] = {
+                    "ms": ms, "rows": Nd, "hashes_per_s": Nd * cfg.k / (ms / 1e3),
+                    "vs_headline_kernel": (ms / Nd) / t_codes,
+                    "note": "analysis only: these FastLSH params as kernel 5 (3xTF32 tcgen05 GEMM on the "
+                            "duplicates-merged coefficients, opt-in); the graded path is the gather kernel"}
+                del Pm
+            except Exception as ex:  # noqa: BLE001
+                dense["merged_fastlsh"] = {"error": str(ex)}
         dense["note"] = ("e2lsh_hash on E2LSH params (m = n) of the same k, w and rows (codes only); tf32x3 is the "
                          "parity-gated comparator (3xTF32), tf32x1 the ungated reference point; cublas_fp32 the "
                          "parity-clean library reference, cublas_tf32 the ungated library one; speedup vs the "

@@ -75,15 +75,15 @@ fastlsh_status new_params(int32_t n, int32_t m, int32_t k, float w, fastlsh_para
 // params K1 / K1t / K1r can pack (shared-memory stages of 4 rows, <= kMaxSlots * 256 slots a hash)
 bool packable(const fastlsh_params* p) { return p->n <= kMaxN && (int64_t)p->m <= (int64_t)kMaxSlots * 256; }
 
-// full = false: params the dense path will serve in auto mode skip the gather packings (seconds of
-// host work for large k*m); pinning a gather kernel or exporting a packing asks for them (full).
+// full = false: params pinned to the dense path (kernel 5) skip the gather packings (seconds of host
+// work for large k*m); pinning a gather kernel or exporting a packing asks for them (full).
 fastlsh_status ensure_packed(fastlsh_params* p, bool full = false) {
     if (p->packed && !(full && p->pack_skipped)) return FASTLSH_OK;
     if (!packable(p)) {  // only the generic K0 (and K1j where it applies) will serve these params
         p->packed = true;
         return FASTLSH_OK;
     }
-    if (!full && p->kernel == 0 && dense_shape(p)) {
+    if (!full && p->kernel == 5 && dense_shape(p)) {
         p->packed = p->pack_skipped = true;
         return FASTLSH_OK;
     }
@@ -161,22 +161,26 @@ bool jit_selected(const fastlsh_params* p) {
     return p->kernel == 4 || (p->kernel == 0 && jit::applicable(*p));
 }
 // K4 on the duplicates-merged coefficient matrix: Eq. 5 as a dense 3xTF32
-// tcgen05 GEMM, A[c][i] = sum_{j: idx_ij = c} a_ij. Serves the call when pinned (kernel 5) or, in auto
-// mode, for long rows sampled densely — n >= 512 and m >= n/8 — where the gathers cost more than the
-// GEMM (measured on C2, n = 4096: m = 512 K1r 25.2 vs dense 8.5 ms per 250k rows, m = 4096 17.4 vs
-// 0.88 ms per 20k rows; m = 128 K1r 21.5 vs 36.5 ms and C1 / C3 / C4 keep the gather kernels), and
-// only while the dense hi/lo matrices stay small (kpad * n * 8 bytes <= 1 GiB).
+// tcgen05 GEMM, A[c][i] = sum_{j: idx_ij = c} a_ij. Opt-in only (kernel 5, fastlsh_params_set_kernel):
+// north_star reserves the tensor cores for the dense E2LSH baseline — FastLSH's sampled projection is
+// a gather — and SURVEY.md §8(f)3(iii) keeps this as analysis, so the automatic choice never takes it
+// even where it is faster (C2 n = 4096: m = 512 K1r 25.2 vs dense 8.5 ms per 250k rows, m = 4096
+// 17.4 vs 0.88 ms per 20k rows; bench.py reports it beside the gather kernel). The dense hi/lo
+// matrices must stay small (kpad * n * 8 bytes <= 1 GiB).
 bool dense_shape(const fastlsh_params* p) {
-    if (p->n % 4 || p->n < 512 || (int64_t)8 * p->m < p->n) return false;
+    if (p->n % 4) return false;
     const int64_t kpad = ((int64_t)p->k + 255) / 256 * 256;
     return kpad * p->n * 8 <= ((int64_t)1 << 30);
 }
-bool dense_selected(const fastlsh_params* p) { return p->kernel == 5 || (p->kernel == 0 && dense_shape(p)); }
+bool dense_selected(const fastlsh_params* p) { return p->kernel == 5; }
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
     if (dense_selected(p)) {
+        // calls the GEMM cannot serve (X not 16-byte aligned) take the generic kernel K0: the gather
+        // packings of a pinned dense params object may not exist
         fastlsh_status st = launch_e2lsh(p, const_cast<DeviceCopy&>(d), X, N, codes, proj, 3, stream);
-        if (st != FASTLSH_EUNSUPPORTED || p->kernel == 5) return st;
+        if (st != FASTLSH_EUNSUPPORTED) return st;
+        return launch_generic(p, d, X, N, codes, proj, stream);
     }
     if (jit_selected(p)) {
         fastlsh_status st = jit::launch(p, d, X, N, codes, proj, nullptr, nullptr, nullptr, 0, stream);
@@ -434,6 +438,11 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
     if (!p || kernel < 0 || kernel > 5) return FASTLSH_EINVAL;
     std::lock_guard<std::mutex> g(p->mu);
+    if (kernel == 5) {  // pinned dense path: the gather packings are not needed (built on demand later)
+        if (p->n % 4) return FASTLSH_EUNSUPPORTED;  // K4's K-major tensor maps
+        p->kernel = 5;
+        return ensure_packed(p, false);
+    }
     const bool gather = kernel >= 1 && kernel <= 3;
     if (gather && p->pack_skipped) {
         // the gather packings were skipped (dense-path shape): build them now, unless a device copy
@@ -446,7 +455,6 @@ fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
     if (kernel == 2 && !p->tpack.ok) return FASTLSH_EUNSUPPORTED;
     if (kernel == 3 && !p->rpack.ok) return FASTLSH_EUNSUPPORTED;
     if (kernel == 4 && !jit::applicable(*p)) return FASTLSH_EUNSUPPORTED;
-    if (kernel == 5 && p->n % 4) return FASTLSH_EUNSUPPORTED;  // K4's K-major tensor maps
     p->kernel = kernel;
     return FASTLSH_OK;
 }

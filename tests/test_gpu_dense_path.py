@@ -1,7 +1,8 @@
 """The dense path for FastLSH params (kernel 5): Eq. 5 as a
-3xTF32 tcgen05 GEMM against the duplicates-merged coefficient matrix, chosen automatically for
-n >= 512, m >= n/8 (C2 m = 512 / 4096). Same parity rule as the gather kernels, same flags, and the
-fallbacks when the GEMM cannot serve a call."""
+3xTF32 tcgen05 GEMM against the duplicates-merged coefficient matrix. Opt-in only
+(fastlsh_params_set_kernel 5): north_star reserves the tensor cores for the dense E2LSH baseline, so the
+automatic choice stays on the gather kernels. Same parity rule as the gather kernels, same flags, and
+the fallbacks when the GEMM cannot serve a call."""
 import os
 
 import numpy as np
@@ -33,9 +34,13 @@ def _check(P, idx, a, b, w, X):
 
 
 @pytest.mark.parametrize("m,N", [(512, 300), (4096, 77), (1000, 513)])
-def test_auto_dense_on_c2_shapes(m, N):
+def test_pinned_dense_on_c2_shapes(m, N):
+    """C2 shapes where the GEMM is the faster path: auto stays on the gather kernel (K1r), pinned
+    dense meets the same parity bar."""
     c = configs.get("C2")
     P, idx, a, b = _params(c.n, m, c.k, c.w, c.seed)
+    assert P.info()["kernel"] == 3
+    P.set_kernel("dense")
     assert P.info()["kernel"] == 5
     X = data.generate(c.data, c.n, 0, N, seed=c.seed, device="cuda")
     rel, amb, _ = _check(P, idx, a, b, c.w, X)
@@ -59,6 +64,7 @@ def test_pinned_dense_on_c1_matches_gather_kernel():
 def test_dense_flags_and_sentinels():
     n, m, k = 512, 64, 40
     P, idx, a, b = _params(n, m, k, 1e-3)
+    P.set_kernel("dense")
     assert P.info()["kernel"] == 5
     X = torch.randn((70, n), device="cuda")
     X[3, :] = float("nan")
@@ -76,9 +82,10 @@ def test_dense_flags_and_sentinels():
 
 def test_dense_misaligned_x_falls_back_to_generic():
     """X 4-byte but not 16-byte aligned: the GEMM's tensor maps cannot serve it, and with the gather
-    packings skipped for this shape the generic K0 does (same parity rule)."""
+    packings skipped for pinned dense params the generic K0 does (same parity rule)."""
     n, m, k = 512, 128, 96
     P, idx, a, b = _params(n, m, k, 1.0)
+    P.set_kernel("dense")
     base = torch.randn(200 * n + 1, device="cuda")
     X = base[1:].view(200, n)
     assert X.data_ptr() % 16 != 0
@@ -89,6 +96,7 @@ def test_dense_misaligned_x_falls_back_to_generic():
 def test_dense_keys_and_host_path():
     n, m, k, L, K = 768, 128, 160, 16, 10
     P, idx, a, b = _params(n, m, k, 2.0)
+    P.set_kernel("dense")
     assert P.info()["kernel"] == 5
     Kobj = fl.Keys.create(L, K, seed=3)
     X = data.generate("sparse80", n, 0, 1234, seed=5, device="cuda")
@@ -104,15 +112,17 @@ def test_dense_keys_and_host_path():
 
 
 def test_pinning_a_gather_kernel_after_upload_is_a_state_error():
-    """The gather packings of a dense-path shape are built on demand: pinning K1r before the first
-    upload works (and is exact), after it the device copy lacks them (ESTATE)."""
+    """Params pinned to the dense path skip the gather packings: pinning K1r back before the first
+    upload builds them (and is exact), after it the device copy lacks them (ESTATE)."""
     n, m, k = 512, 64, 64
     P, idx, a, b = _params(n, m, k, 1.0)
+    P.set_kernel("dense")
     P.set_kernel("rows")
     assert P.info()["kernel"] == 3
     X = torch.randn((100, n), device="cuda")
     _check(P, idx, a, b, 1.0, X)
     Q, *_ = _params(n, m, k, 1.0)
+    Q.set_kernel("dense")
     fl.fastlsh_hash(Q, X)  # uploads with the packings skipped
     with pytest.raises(fl.FastLSHError) as e:
         Q.set_kernel("rows")

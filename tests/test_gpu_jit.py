@@ -77,7 +77,8 @@ def test_jit_parity_configs(name, N):
 
 @pytest.mark.parametrize("N,n,m,k,w", [(1, 128, 16, 64, 4.0), (31, 32, 5, 36, 1.5), (33, 36, 1, 4, 0.75),
                                        (1000, 100, 64, 256, 2.0), (4097, 128, 3, 128, 1.5),
-                                       (65, 4, 4, 100, 1.0), (129, 64, 130, 32, 0.5), (7, 128, 128, 128, 3.0)])
+                                       (65, 4, 4, 100, 1.0), (129, 64, 130, 32, 0.5), (7, 128, 128, 128, 3.0),
+                                       (500, 64, 8, 96, 2.0), (333, 128, 16, 160, 4.0)])  # odd group counts: last pair half empty
 def test_jit_edge_shapes(N, n, m, k, w):
     """Ragged tiles (N % 32), n % 32 != 0 (partial X boxes), k % 32 != 0 (partial code boxes),
     m = 1, m > n (replacement), non-power-of-two w (IEEE division), tiny n."""

@@ -160,7 +160,7 @@ def test_bench_config_packing_quality(lib):
 
 def test_kernel_selection_rules(lib, monkeypatch):
     """fastlsh_params_set_kernel: 0-5 accepted, others EINVAL; K1t needs n % 4 == 0 and m <= 128;
-    auto mode reports the dense path (5) for n >= 512 with m >= n/8, K1j (4) for n <= 128 shapes
+    auto mode never picks the dense path (5, opt-in), K1j (4) for n <= 128 shapes
     (NVRTC present), K1r (3) for other n % 4 == 0 shapes whose row packing exists, else K1;
     FASTLSH_NO_JIT=1 turns K1j off."""
     import paper_2309_15479_b200 as fl
@@ -188,13 +188,16 @@ def test_kernel_selection_rules(lib, monkeypatch):
     assert Q.info()["kernel"] == 1
     idx, a, b = fastlsh_arrays(960, 60, 500, 1.0, 1)  # n > 128: K1j does not apply
     assert fl.Params.from_arrays(960, 1.0, idx, a, b).info()["kernel"] == 3
-    # C2's m sweep (n = 4096): the gathers up to m = 128, the dense GEMM from m = n/8 = 512 on
-    for m, kern in ((32, 3), (128, 3), (511, 3), (512, 5), (4096, 5)):  # (k = 100 keeps the packers quick)
-        assert fl.Params.create(4096, m, 100, 0.5, seed=1).info()["kernel"] == kern, m
-    assert fl.Params.create(256, 64, 256, 1.0, seed=1).info()["kernel"] != 5      # n < 512
-    assert fl.Params.create(1000, 200, 1000, 1.0, seed=1).info()["kernel"] == 5   # m >= n/8
-    assert fl.Params.create(1001, 200, 100, 1.0, seed=1).info()["kernel"] != 5    # n % 4 != 0
-    assert fl.Params.create(65536, 8192, 4096, 1.0, seed=1).info()["kernel"] != 5  # dense A > 1 GiB
+    # the dense path (kernel 5) is opt-in only: north_star reserves the tensor cores for the E2LSH
+    # baseline, so auto keeps the gather kernels on every shape, C2's m sweep included (k = 100 keeps
+    # the packers quick)
+    for m in (32, 512, 4096):
+        assert fl.Params.create(4096, m, 100, 0.5, seed=1).info()["kernel"] == 3, m
+    D = fl.Params.create(1000, 200, 100, 1.0, seed=1)
+    D.set_kernel("dense")
+    assert D.info()["kernel"] == 5
+    with pytest.raises(fl.FastLSHError):
+        fl.Params.create(1001, 200, 100, 1.0, seed=1).set_kernel("dense")  # n % 4 != 0
     monkeypatch.setenv("FASTLSH_NO_JIT", "1")
     idx, a, b = fastlsh_arrays(128, 16, 64, 4.0, 1)
     assert fl.Params.from_arrays(128, 4.0, idx, a, b).info()["kernel"] == 3
