@@ -133,8 +133,7 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
 
 /* Choose the hashing kernel of these params (all compute Eq. 5, with the same
  * epilogue; only the summation order of the fp32 projection differs, within the same bound):
- *   0 = automatic (default), first applicable of: the dense path (5) for n >= 512 and m >= n/8;
- *       K1j (4); the row-major gather K1r when its packing exists and its cost model beats K1's,
+ *   0 = automatic (default), first applicable of: K1j (4); the row-major gather K1r when its packing exists and its cost model beats K1's,
  *       for calls with n % 4 == 0 and X 16-byte aligned; K0 for params nothing else packs; else K1;
  *   1 = always the shared-memory gather K1 (column-interleaved stages, LDS.128);
  *   2 = always K1t (calls on shapes or pointers it cannot serve return EUNSUPPORTED);
@@ -149,9 +148,12 @@ fastlsh_status fastlsh_params_upload(fastlsh_params* p, int32_t device, fastlsh_
  *   5 = always the dense path: Eq. 5 as one tcgen05 3xTF32 GEMM against the
  *       coefficient matrix A[c][i] = sum of a_ij over the samples j of hash i with idx_ij = c
  *       (duplicates merged in double, rounded once to f32; built on the first call per device,
- *       kpad x n x 8 bytes), then the same epilogue (e2lsh_hash's kernel). In automatic mode it
- *       serves n >= 512, m >= n/8 while that matrix is <= 1 GiB: there the gathers (N k m) cost
- *       more than the GEMM (N k n MMA work on tensor cores). Needs n % 4 == 0, X 16-byte aligned.
+ *       kpad x n x 8 bytes), then the same epilogue (e2lsh_hash's kernel). Opt-in only (analysis):
+ *       north_star reserves the tensor cores for the dense E2LSH baseline, so automatic mode never
+ *       takes it, although for long densely-sampled rows (C2: n = 4096, m >= 512) it is faster than
+ *       the gathers. Needs n % 4 == 0; calls with X not 16-byte aligned take the generic kernel K0.
+ *       Pinning 5 before the first upload skips the gather packings; pinning 0-3 afterwards then
+ *       returns ESTATE once a device copy exists (before it, the packings are built).
  * EINVAL for other values; EUNSUPPORTED for 2, 3, 4 or 5 when that kernel cannot serve the params. */
 fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel);
 

@@ -176,11 +176,10 @@ bool dense_selected(const fastlsh_params* p) { return p->kernel == 5; }
 fastlsh_status launch_hash(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                            int32_t* codes, float* proj, cudaStream_t stream) {
     if (dense_selected(p)) {
-        // calls the GEMM cannot serve (X not 16-byte aligned) take the generic kernel K0: the gather
-        // packings of a pinned dense params object may not exist
+        // calls the GEMM cannot serve (X not 16-byte aligned) fall through to K1 (K0 when the gather
+        // packings were skipped: dense pinned before the first info / upload)
         fastlsh_status st = launch_e2lsh(p, const_cast<DeviceCopy&>(d), X, N, codes, proj, 3, stream);
         if (st != FASTLSH_EUNSUPPORTED) return st;
-        return launch_generic(p, d, X, N, codes, proj, stream);
     }
     if (jit_selected(p)) {
         fastlsh_status st = jit::launch(p, d, X, N, codes, proj, nullptr, nullptr, nullptr, 0, stream);
@@ -443,7 +442,8 @@ fastlsh_status fastlsh_params_set_kernel(fastlsh_params* p, int32_t kernel) {
         p->kernel = 5;
         return ensure_packed(p, false);
     }
-    const bool gather = kernel >= 1 && kernel <= 3;
+    // auto (0) and the gather kernels need the packings a pinned-dense params object skipped
+    const bool gather = kernel <= 3;
     if (gather && p->pack_skipped) {
         // the gather packings were skipped (dense-path shape): build them now, unless a device copy
         // without them exists already

@@ -25,8 +25,8 @@ RowKernelFn select_row_kernel(int MS, int cls) {
 size_t row_smem_bytes(const RPacking& pk, int key_words = 0) {
     const RClass c = kRClasses[pk.cls];
     const int kbp = (pk.kb_max + 3) & ~3;
-    return (size_t)c.NS * c.R * c.S * 4 + (size_t)c.NC * c.R * kbp * 4 + (size_t)(c.NS + 2 * c.NC) * 8 +
-           (size_t)key_words * 8 + c.NS * 4 + (size_t)kbp * 4;
+    return (size_t)c.NS * c.R * c.S * 4 + (size_t)c.NC * c.R * kbp * 4 + (size_t)((c.NS + 2 * c.NC + 1) & ~1) * 8 +
+           (size_t)key_words * 16 + c.NS * 4 + (size_t)kbp * 4;  // key multipliers as uint4 limbs
 }
 
 }  // namespace k1r
@@ -38,7 +38,8 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     const RPacking& pk = p->rpack;
     if (!pk.ok || !d.r_offp) return FASTLSH_EUNSUPPORTED;
     // keys from the code tile need every table's codes in the one block
-    if (fk && (pk.hash_blocks != 1 || (int64_t)fk->L * fk->K > p->k)) return FASTLSH_EUNSUPPORTED;
+    // (and K <= 1024: the limb sums of the flush are exact while K * 2^53 < 2^63)
+    if (fk && (pk.hash_blocks != 1 || (int64_t)fk->L * fk->K > p->k || fk->K > 1024)) return FASTLSH_EUNSUPPORTED;
     const int key_words = fk ? fk->L * (fk->K + 1) : 0;
     // TMA bulk row copies need 16-byte aligned rows
     if ((p->n % 4) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;

@@ -141,8 +141,9 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     int32_t* cbuf = reinterpret_cast<int32_t*>(smem + (size_t)NS * stage_bytes);
     const int cwords = R * a.kbp;  // one code buffer
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(cbuf + NC * cwords);
-    uint64_t* s_kr = reinterpret_cast<uint64_t*>(bars + NS + 2 * NC);  // [L][K+1] key multipliers (a.kr)
-    int* cnt = reinterpret_cast<int*>(s_kr + (a.kr ? a.L * (a.K + 1) : 0));  // [NS] stage readers (monotone)
+    // [L][K+1] key multipliers (a.kr) as three 21-bit limbs {r & (2^21-1), (r >> 21) & (2^21-1), r >> 42, 0}
+    uint4* s_kl = reinterpret_cast<uint4*>(bars + ((NS + 2 * NC + 1) & ~1));  // 16-byte aligned
+    int* cnt = reinterpret_cast<int*>(s_kl + (a.kr ? a.L * (a.K + 1) : 0));  // [NS] stage readers (monotone)
     float* s_b = reinterpret_cast<float*>(cnt + NS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -175,7 +176,10 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + a.S0 - 32 + (i & 31)] = 0.f;
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
     if (a.kr)
-        for (int i = tid; i < a.L * (a.K + 1); i += nthreads) s_kr[i] = a.kr[i];
+        for (int i = tid; i < a.L * (a.K + 1); i += nthreads) {
+            const uint64_t r = a.kr[i];
+            s_kl[i] = make_uint4((uint32_t)r & 0x1fffffu, (uint32_t)(r >> 21) & 0x1fffffu, (uint32_t)(r >> 42), 0u);
+        }
 
     uint32_t opk[MS / 2];
     float cf[MS];
@@ -246,25 +250,31 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
         }
         if (a.kr) {
             // items (table t, row r), rows fastest: 8 lanes write one 64-byte run of a table.
-            // Exact 128-bit accumulation of the K products (each < 2^93), one Mersenne reduction.
+            // Limb form (as K1j): S_q = sum_j limb_q(r_{j+1}) * u32(c_j), three IMAD.WIDE.U32 per code,
+            // exact while K * 2^53 < 2^63 (K <= 1024, checked by the launcher); key = (r0 + S0 +
+            // S1 2^21 + S2 2^42) mod 2^61-1 with 61-bit rotations.
             const int K = a.K;
+            constexpr uint64_t P61 = (1ull << 61) - 1;
+            auto mod61 = [](uint64_t x) {
+                x = (x & P61) + (x >> 61);
+                return x >= P61 ? x - P61 : x;
+            };
+            auto rotl61 = [](uint64_t x, int j) { return ((x << j) & P61) | (x >> (61 - j)); };
             for (int u = tid; u < a.L * R; u += nthreads) {
                 const int r = u % R, t = u / R;
                 if (r >= rows) continue;
-                const uint64_t* rl = s_kr + t * (K + 1);
+                const uint4* rl = s_kl + t * (K + 1);
                 const int32_t* cc = src + r * a.kbp + t * K;
-                uint64_t lo = rl[0], hi = 0;
+                const uint4 q0 = rl[0];
+                uint64_t s0 = (uint64_t)q0.x | ((uint64_t)q0.y << 21) | ((uint64_t)q0.z << 42), s1 = 0, s2 = 0;
                 for (int jj = 0; jj < K; ++jj) {
-                    const uint64_t rv = rl[jj + 1];
-                    const uint64_t u32c = (uint32_t)cc[jj];
-                    const uint64_t plo = rv * u32c;
-                    lo += plo;
-                    hi += __umul64hi(rv, u32c) + (lo < plo ? 1 : 0);
+                    const uint4 q = rl[jj + 1];
+                    const uint32_t c = (uint32_t)cc[jj];
+                    s0 += (uint64_t)q.x * c;
+                    s1 += (uint64_t)q.y * c;
+                    s2 += (uint64_t)q.z * c;
                 }
-                constexpr uint64_t P61 = (1ull << 61) - 1;
-                uint64_t x = (lo & P61) + (lo >> 61) + (hi << 3);  // 2^64 = 8 (mod 2^61 - 1)
-                x = (x & P61) + (x >> 61);
-                a.keys[(long long)t * a.ldk + row0 + r] = x >= P61 ? x - P61 : x;
+                a.keys[(long long)t * a.ldk + row0 + r] = mod61(mod61(s0) + rotl61(mod61(s1), 21) + rotl61(mod61(s2), 42));
             }
         }
         __syncwarp();

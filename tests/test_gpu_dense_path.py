@@ -80,9 +80,9 @@ def test_dense_flags_and_sentinels():
     assert nf == k + int(uses0.sum()) and sat == k
 
 
-def test_dense_misaligned_x_falls_back_to_generic():
-    """X 4-byte but not 16-byte aligned: the GEMM's tensor maps cannot serve it, and with the gather
-    packings skipped for pinned dense params the generic K0 does (same parity rule)."""
+def test_dense_misaligned_x_falls_back_to_a_gather_kernel():
+    """X 4-byte but not 16-byte aligned: the GEMM's tensor maps cannot serve it, so the call falls
+    through to the gather chain (K1 here; K0 when the packings were skipped), same parity rule."""
     n, m, k = 512, 128, 96
     P, idx, a, b = _params(n, m, k, 1.0)
     P.set_kernel("dense")
@@ -111,20 +111,19 @@ def test_dense_keys_and_host_path():
     assert np.array_equal(kh.numpy().view(np.uint64), kr)
 
 
-def test_pinning_a_gather_kernel_after_upload_is_a_state_error():
-    """Params pinned to the dense path skip the gather packings: pinning K1r back before the first
-    upload builds them (and is exact), after it the device copy lacks them (ESTATE)."""
+def test_switching_between_dense_and_gather_kernels():
+    """Python params are packed at creation (info), so pinning the dense path and back to a gather
+    kernel works before and after the upload; every switch meets the parity rule."""
     n, m, k = 512, 64, 64
     P, idx, a, b = _params(n, m, k, 1.0)
+    X = torch.randn((100, n), device="cuda")
     P.set_kernel("dense")
+    _check(P, idx, a, b, 1.0, X)
     P.set_kernel("rows")
     assert P.info()["kernel"] == 3
-    X = torch.randn((100, n), device="cuda")
     _check(P, idx, a, b, 1.0, X)
-    Q, *_ = _params(n, m, k, 1.0)
-    Q.set_kernel("dense")
-    fl.fastlsh_hash(Q, X)  # uploads with the packings skipped
-    with pytest.raises(fl.FastLSHError) as e:
-        Q.set_kernel("rows")
-    assert e.value.status == fl.ESTATE
-    Q.set_kernel("dense")
+    P.set_kernel("auto")
+    assert P.info()["kernel"] == 3
+    P.set_kernel("dense")
+    assert P.info()["kernel"] == 5
+    _check(P, idx, a, b, 1.0, X)
