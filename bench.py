@@ -687,8 +687,13 @@ def main():
             entries = cfg.L * N
             tables = {"ms": tms, "entries": entries, "entries_per_s": entries / (tms / 1e3),
                       "buckets_table0": int(out_t[3][0].item()),
-                      "hbm_bytes_algorithmic": entries * (8 * 8 + 8 * 24 + 8 + 4),
-                      "note": "8 LSD radix passes (hist 8 B + scatter 12 B in / 12 B out per entry) + bucket starts"}
+                      "hbm_bytes_algorithmic": entries * ((8 + 8 + 12 + 12 + 12 + 8 + 8 + 4) if N <= (1 << 22)
+                                                          else (8 * 8 + 8 * 24 + 8 + 4)),
+                      "note": ("MSD form (N <= 2^22): one global top-digit pass (hist 8 B + scatter 8 B in / 12 B out per "
+                               "entry), per-segment LSD sorts in L2 (12 B in / 12 B out), bucket starts (8 + 8 B in, 4 B "
+                               "out); bound by the shared-memory ranking of the seven in-segment passes, not HBM"
+                               if N <= (1 << 22) else
+                               "8 LSD radix passes (hist 8 B + scatter 12 B in / 12 B out per entry) + bucket starts")}
             tables["hbm_frac"] = tables["hbm_bytes_algorithmic"] / (tms / 1e3) / (peaks["hbm_gbs"] * 1e9)
             del out_t
         except Exception as ex:  # noqa: BLE001 (report, never hide a failure)

@@ -19,6 +19,28 @@ fastlsh_status set_cuda_error(cudaError_t e) {
     return FASTLSH_ECUDA;
 }
 
+fastlsh_status smem_optin_once(const void* fn) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& d : done)
+        if (d.first == fn && d.second == dev) return FASTLSH_OK;
+    // the opt-in covers dynamic memory only: the kernel's static shared memory counts against 227 KB
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, fn);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // not sticky: keep it out of later launches' cudaGetLastError checks
+        return set_cuda_error(e);
+    }
+    done.push_back({fn, dev});
+    return FASTLSH_OK;
+}
+
 namespace {
 
 #define FL_CUDA(call)                                  \

@@ -725,9 +725,9 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
         return pe == cudaSuccess ? FASTLSH_OK : set_cuda_error(pe);
     }
     const size_t smem = 3 * kStageBytesE + 1024 + 256;  // 3 x 64 KB (3xTF32) or 6 x 32 KB (1xTF32)
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
+    if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel)); so != FASTLSH_OK)
+        return so;
+    cudaError_t e;
     const long long tiles = (N + BM - 1) / BM;
     a.hash_fast = tiles <= 65535 ? 1 : 0;
     dim3 grid = a.hash_fast ? dim3((unsigned)(d.dense_kpad / BN), (unsigned)tiles)

@@ -151,9 +151,8 @@ fastlsh_status launch_gather(const fastlsh_params* p, const DeviceCopy& d, const
     a.ldk = fused ? fk->ldk : 0;
 
     const size_t smem = smem_bytes(pk, shape, tma, landing_row, keys_words);
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
+    if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(fn)); so != FASTLSH_OK) return so;
+    cudaError_t e = cudaSuccess;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

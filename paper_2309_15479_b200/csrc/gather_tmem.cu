@@ -685,9 +685,9 @@ fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, 
     a.cta_first[0] = 0;
     for (int hb = 0; hb < tp.HB; ++hb) a.cta_first[hb + 1] = a.cta_first[hb] + (int)R[hb];
     const int grid = a.cta_first[tp.HB];
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(tmem_gather_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
+    if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(tmem_gather_kernel)); so != FASTLSH_OK)
+        return so;
+    cudaError_t e;
     tmem_gather_kernel<<<grid, 512, tp.smem, stream>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e);

@@ -263,6 +263,11 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
                             int32_t* codes, float* proj, int precision, cudaStream_t stream);
 
 fastlsh_status set_cuda_error(cudaError_t e);
+// cudaFuncAttributeMaxDynamicSharedMemorySize = 227 KB minus the kernel's static shared memory for
+// kernel `fn` on the current device, once per (kernel, device) for the process (launchers call it
+// before every launch; only the first call reaches the driver). Launches then pass their own
+// dynamic size, which must fit that bound.
+fastlsh_status smem_optin_once(const void* fn);
 
 // jit.cpp — K1j, the params-specialised lane = row kernel
 namespace jit {

@@ -408,17 +408,7 @@ fastlsh_status launch_build_keys(const fastlsh_keys* keys, const uint64_t* dev_r
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess || dev < 0 || dev >= kMaxDevices) return e != cudaSuccess ? set_cuda_error(e) : FASTLSH_EUNSUPPORTED;
-    {   // the dynamic shared-memory opt-in once per device, at the device maximum (not per launch)
-        static bool attr_set[kMaxDevices] = {};
-        static std::mutex mu;
-        std::lock_guard<std::mutex> g(mu);
-        if (!attr_set[dev]) {
-            e = cudaFuncSetAttribute(reinterpret_cast<const void*>(keys_kernel),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            if (e != cudaSuccess) return set_cuda_error(e);
-            attr_set[dev] = true;
-        }
-    }
+    if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(keys_kernel)); so != FASTLSH_OK) return so;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(keys_kernel),
                                                       kKeyThreads, smem);

@@ -179,9 +179,8 @@ fastlsh_status launch_query(const float* X, long long N, int n, const uint64_t* 
     cudaError_t e = cudaMemsetAsync(ws, 0, query_workspace_bytes(N, grid), stream);
     if (e != cudaSuccess) return set_cuda_error(e);
     const size_t smem = (size_t)((n + 3) & ~3) * 4 + (size_t)L * 16;
-    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(query_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e);
+    if (smem > 227 * 1024) return FASTLSH_EUNSUPPORTED;
+    if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(query_kernel)); so != FASTLSH_OK) return so;
     query_kernel<<<grid, kQWarps * 32, smem, stream>>>(X, N, n, sk, ids, L, Q, qkeys, nq, ldq, topk, out_ids, out_dist,
                                                       out_ncand, static_cast<uint32_t*>(ws), words);
     e = cudaGetLastError();

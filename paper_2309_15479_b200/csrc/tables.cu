@@ -14,9 +14,16 @@
 // Then bucket starts (key differs from its predecessor): per-tile flag counts, a per-table scan
 // over tiles, and per-tile block-scanned writes. Bound: HBM (per pass each element is read twice
 // and written once: 8 B key + 4 B id).
+// Tables of N <= kMsdMaxN rows take the MSD form instead: ONE global pass of the same machinery on
+// the top digit (bits 53-60) splits each table into 256 segments (~N/256 entries), then one CTA
+// per segment finishes it with the 7 remaining stable LSD passes over bits 0-55 (segment_sort),
+// ping-ponging between the workspace and the output inside its segment — a few tens of KB per
+// CTA, so the intermediate passes stay in L2 and HBM sees about one read and one write per pass
+// of the whole table instead of eight.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "internal.h"
 
@@ -191,6 +198,118 @@ __global__ void __launch_bounds__(kSortWarps * 32, 3) radix_scatter(const uint64
     }
 }
 
+// MSD form, second level: table l's top-digit segment d = [hist[l][d][0], hist[l][d+1][0]) (the
+// scanned level-1 histogram) is sorted by the CTA (d, l) with 7 stable LSD passes over bits 0-55
+// (bits 53-55 are equal inside a segment: harmless). Pass p reads ping (p even: the workspace
+// alt_*, else the output) and writes pong; each pass walks the segment in tiles of kTile elements
+// in order, ranks a tile like radix_scatter (warps take consecutive runs, __match_any_sync, warp
+// counts prefixed in shared memory) and carries per-digit running offsets across tiles, so equal
+// digits keep their order (stability: the row id stays the tie-break). The next pass's histogram
+// is counted while scattering. Plain (not read-only-path) loads: the CTA rereads what it wrote,
+// ordered by __syncthreads.
+constexpr long long kMsdMaxN = 1ll << 22;
+constexpr int kMsdShift = 53;      // level 1: bits 53-60 of the 61-bit keys
+constexpr int kSegPasses = 7;      // level 2: bits 0-55
+__global__ void __launch_bounds__(kSortWarps * 32, 3) segment_sort(uint64_t* __restrict__ alt_k, uint32_t* __restrict__ alt_i,
+                                                              uint64_t* __restrict__ out_k, uint32_t* __restrict__ out_i,
+                                                              long long N, int T, const uint32_t* __restrict__ hist) {
+    __shared__ uint32_t hcnt[kBins];  // histogram of the current pass's digit (next pass's while scattering)
+    __shared__ uint32_t base[kBins];  // running output offset of each digit
+    __shared__ uint32_t wcnt[kSortWarps][kBins];
+    __shared__ uint32_t wsum[kSortWarps];
+    const int d0 = blockIdx.x, l = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* hl = hist + (size_t)l * kBins * T;
+    const long long s0 = hl[(size_t)d0 * T];
+    const long long s1 = d0 + 1 < kBins ? (long long)hl[(size_t)(d0 + 1) * T] : N;
+    const int len = (int)(s1 - s0);
+    if (len <= 0) return;
+    uint64_t* ak = alt_k + (long long)l * N + s0;
+    uint32_t* ai = alt_i + (long long)l * N + s0;
+    uint64_t* ok = out_k + (long long)l * N + s0;
+    uint32_t* oi = out_i + (long long)l * N + s0;
+    if (len == 1) {
+        if (tid == 0) {
+            ok[0] = ak[0];
+            oi[0] = ai[0];
+        }
+        return;
+    }
+    hcnt[tid] = 0;  // blockDim.x == kBins
+    __syncthreads();
+    for (int e = tid; e < len; e += blockDim.x) atomicAdd(&hcnt[digit_of(ak[e], 0)], 1u);
+    __syncthreads();
+    for (int p = 0; p < kSegPasses; ++p) {
+        const int shift = p * kRadixBits;
+        const uint64_t* sk = (p & 1) ? ok : ak;
+        const uint32_t* si = (p & 1) ? oi : ai;
+        uint64_t* dk = (p & 1) ? ak : ok;
+        uint32_t* di = (p & 1) ? ai : oi;
+        {   // base = exclusive scan of hcnt; hcnt restarts for the next pass
+            const uint32_t v = hcnt[tid];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            uint32_t b = 0;
+            for (int w = 0; w < warp; ++w) b += wsum[w];
+            base[tid] = b + x - v;
+            hcnt[tid] = 0;
+        }
+        for (int t0 = 0; t0 < len; t0 += kTile) {
+            for (int w = 0; w < kSortWarps; ++w) wcnt[w][tid] = 0;
+            __syncthreads();
+            const int w0 = t0 + warp * kItems * 32;
+            uint64_t k[kItems];
+            uint32_t id[kItems], loc[kItems];
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const int e = w0 + r * 32 + lane;
+                const bool live = e < len;
+                k[r] = live ? sk[e] : 0ull;
+                id[r] = live ? si[e] : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const bool live = w0 + r * 32 + lane < len;
+                const uint32_t d = digit_of(k[r], shift);
+                const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+                const unsigned peers = __match_any_sync(0xffffffffu, live ? d : 0xffffffffu) & live_mask;
+                const uint32_t before = wcnt[warp][d];
+                __syncwarp();
+                loc[r] = before + __popc(peers & ((1u << lane) - 1u));
+                if (live && (peers & ((1u << lane) - 1u)) == 0) wcnt[warp][d] = before + __popc(peers);
+                __syncwarp();
+            }
+            __syncthreads();
+            uint32_t tot = 0;  // this thread's digit (tid): exclusive prefix over warps, tile total
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t c = wcnt[w][tid];
+                wcnt[w][tid] = tot;
+                tot += c;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                if (w0 + r * 32 + lane >= len) continue;
+                const uint32_t d = digit_of(k[r], shift);
+                const uint32_t pos = base[d] + wcnt[warp][d] + loc[r];
+                dk[pos] = k[r];
+                di[pos] = id[r];
+                if (p + 1 < kSegPasses) atomicAdd(&hcnt[digit_of(k[r], shift + kRadixBits)], 1u);
+            }
+            __syncthreads();
+            base[tid] += tot;
+        }
+        __syncthreads();  // this pass's global writes are visible to the CTA before the next pass reads
+    }
+}
+
 // bucket starts of every table: positions j with j == 0 or key[j] != key[j-1], then N.
 // (1) per-tile flag counts, (2) per-table exclusive scan over tiles (radix_scan with one "bin"),
 // (3) per tile: block scan of the flags, positions written at the tile's offset.
@@ -302,10 +421,33 @@ fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, lon
     hp = (hp + 255) & ~(uintptr_t)255;
     uint32_t* hist = reinterpret_cast<uint32_t*>(hp);
     const dim3 grid(T, L);
-    cudaError_t ae = cudaFuncSetAttribute(reinterpret_cast<const void*>(radix_scatter),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * 12);
-    if (ae != cudaSuccess) return set_cuda_error(ae);
-    for (int p = 0; p < kPasses; ++p) {
+    constexpr int kSegSmemPad = 36 * 1024;  // + ~11 KB static: under the 48 KB no-opt-in limit
+    {   // the dynamic shared-memory opt-in once per device (not per call)
+        int dev = 0;
+        cudaError_t ae = cudaGetDevice(&dev);
+        if (ae != cudaSuccess) return set_cuda_error(ae);
+        if (dev < 0 || dev >= kMaxDevices) return FASTLSH_EUNSUPPORTED;
+        static bool attr_set[kMaxDevices] = {};
+        static std::mutex mu;
+        std::lock_guard<std::mutex> g(mu);
+        if (!attr_set[dev]) {
+            ae = cudaFuncSetAttribute(reinterpret_cast<const void*>(radix_scatter),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * 12);
+            if (ae != cudaSuccess) return set_cuda_error(ae);
+            attr_set[dev] = true;
+        }
+    }
+    if (N <= kMsdMaxN) {
+        // MSD form: one global pass on the top digit into the workspace, then per-segment sorts
+        radix_hist<<<grid, 256, 0, stream>>>(keys, ldk, N, T, kMsdShift, hist);
+        radix_scan<<<L, 1024, 0, stream>>>(hist, T);
+        radix_scatter<<<grid, kSortWarps * 32, kTile * 12, stream>>>(keys, ldk, nullptr, alt_k, alt_i, N, T, kMsdShift,
+                                                                     hist);
+        // 36 KB of (unused) dynamic shared memory caps residency at 4 CTAs per SM, so the segments in
+        // flight (~N/256 x 12 B x 2 each) stay in L2 through their seven passes
+        segment_sort<<<dim3(kBins, L), kSortWarps * 32, kSegSmemPad, stream>>>(alt_k, alt_i, sorted_keys, ids, N, T, hist);
+    }
+    for (int p = 0; p < kPasses && N > kMsdMaxN; ++p) {
         const int shift = p * kRadixBits;
         // pass 0 reads the caller's keys (ids = row indices); then ping-pong so the last pass
         // (odd) lands in the output arrays
