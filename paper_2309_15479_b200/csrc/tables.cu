@@ -235,6 +235,79 @@ __global__ void __launch_bounds__(kSortWarps * 32, 3) segment_sort(uint64_t* __r
         }
         return;
     }
+    if (len <= kTile) {
+        // the common case (segments average N/256 entries): the whole segment is one tile, kept in
+        // shared memory; each pass loads it into registers, ranks it (the tile's digit totals are the
+        // segment's histogram: no separate count) and scatters it back in place
+        extern __shared__ __align__(16) unsigned char seg_smem[];
+        uint64_t* bk = reinterpret_cast<uint64_t*>(seg_smem);
+        uint32_t* bi = reinterpret_cast<uint32_t*>(bk + kTile);
+        for (int e = tid; e < len; e += blockDim.x) {
+            bk[e] = ak[e];
+            bi[e] = ai[e];
+        }
+        const int w0 = warp * kItems * 32;
+        for (int p = 0; p < kSegPasses; ++p) {
+            const int shift = p * kRadixBits;
+            for (int w = 0; w < kSortWarps; ++w) wcnt[w][tid] = 0;
+            __syncthreads();
+            uint64_t k[kItems];
+            uint32_t id[kItems], loc[kItems];
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const int e = w0 + r * 32 + lane;
+                const bool live = e < len;
+                k[r] = live ? bk[e] : 0ull;
+                id[r] = live ? bi[e] : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                const bool live = w0 + r * 32 + lane < len;
+                const uint32_t d = digit_of(k[r], shift);
+                const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+                const unsigned peers = __match_any_sync(0xffffffffu, live ? d : 0xffffffffu) & live_mask;
+                const uint32_t before = wcnt[warp][d];
+                __syncwarp();
+                loc[r] = before + __popc(peers & ((1u << lane) - 1u));
+                if (live && (peers & ((1u << lane) - 1u)) == 0) wcnt[warp][d] = before + __popc(peers);
+                __syncwarp();
+            }
+            __syncthreads();
+            uint32_t tot = 0;  // digit tid: exclusive prefix over warps, segment total
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t c = wcnt[w][tid];
+                wcnt[w][tid] = tot;
+                tot += c;
+            }
+            uint32_t x = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            uint32_t b = 0;
+            for (int w = 0; w < warp; ++w) b += wsum[w];
+            base[tid] = b + x - tot;
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < kItems; ++r) {
+                if (w0 + r * 32 + lane >= len) continue;
+                const uint32_t d = digit_of(k[r], shift);
+                const uint32_t pos = base[d] + wcnt[warp][d] + loc[r];
+                bk[pos] = k[r];
+                bi[pos] = id[r];
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < len; e += blockDim.x) {
+            ok[e] = bk[e];
+            oi[e] = bi[e];
+        }
+        return;
+    }
     hcnt[tid] = 0;  // blockDim.x == kBins
     __syncthreads();
     for (int e = tid; e < len; e += blockDim.x) atomicAdd(&hcnt[digit_of(ak[e], 0)], 1u);
@@ -421,7 +494,6 @@ fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, lon
     hp = (hp + 255) & ~(uintptr_t)255;
     uint32_t* hist = reinterpret_cast<uint32_t*>(hp);
     const dim3 grid(T, L);
-    constexpr int kSegSmemPad = 36 * 1024;  // + ~11 KB static: under the 48 KB no-opt-in limit
     {   // the dynamic shared-memory opt-in once per device (not per call)
         int dev = 0;
         cudaError_t ae = cudaGetDevice(&dev);
@@ -443,9 +515,10 @@ fastlsh_status launch_build_tables(const uint64_t* keys, int L, long long N, lon
         radix_scan<<<L, 1024, 0, stream>>>(hist, T);
         radix_scatter<<<grid, kSortWarps * 32, kTile * 12, stream>>>(keys, ldk, nullptr, alt_k, alt_i, N, T, kMsdShift,
                                                                      hist);
-        // 36 KB of (unused) dynamic shared memory caps residency at 4 CTAs per SM, so the segments in
-        // flight (~N/256 x 12 B x 2 each) stay in L2 through their seven passes
-        segment_sort<<<dim3(kBins, L), kSortWarps * 32, kSegSmemPad, stream>>>(alt_k, alt_i, sorted_keys, ids, N, T, hist);
+        // one tile of (key, id) in dynamic shared memory (segments <= kTile are sorted there; larger
+        // ones ping-pong through L2, where the 3 CTAs per SM this size allows keep them resident)
+        if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(segment_sort)); so != FASTLSH_OK) return so;
+        segment_sort<<<dim3(kBins, L), kSortWarps * 32, kTile * 12, stream>>>(alt_k, alt_i, sorted_keys, ids, N, T, hist);
     }
     for (int p = 0; p < kPasses && N > kMsdMaxN; ++p) {
         const int shift = p * kRadixBits;
