@@ -237,8 +237,10 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ke
  *   bucket_start[l*(N+1) + b]  first entry of bucket b for b < nbuckets[l], then N for the rest
  *                              of the row ([L][N+1] u32),
  *   nbuckets[l]           number of distinct keys of table l (device i64 [L]).
- * keys: device u64 [L][ldk] (e.g. fastlsh_build_keys output), ldk >= N. A stable LSD radix sort
- * (8 passes of 8 bits over the 61-bit keys) per table, then bucket starts. `workspace` is a device
+ * keys: device u64 [L][ldk] (e.g. fastlsh_build_keys output), ldk >= N. A stable radix sort per
+ * table: for N <= 2^22 one global pass on the top 8 bits into 256 segments, each then sorted by one
+ * CTA with 7 stable passes over bits 0-55 (in shared memory when it fits one 4096-entry tile);
+ * larger N, 8 global LSD passes of 8 bits. Then bucket starts. `workspace` is a device
  * buffer of >= fastlsh_tables_workspace(L, N) bytes (16-byte aligned), owned by the caller.
  * EINVAL on bad sizes/pointers (N must be < 2^32 - 1); asynchronous on `stream`. */
 fastlsh_status fastlsh_tables_workspace(int32_t L, int64_t N, size_t* bytes);
