@@ -228,18 +228,21 @@ def _kernel_name(info, fused):
 
 
 def _launches_per_call(P, info, Kobj) -> int:
-    """Kernel launches of one fastlsh_hash_keys call (api.cu's dispatch rules): K1j and K1r with the
-    keys built from its code tile (one CTA hash block, key work small next to the gathers) are one
-    launch; otherwise hash + the key kernel."""
+    """Kernel launches of one fastlsh_hash_keys call (api.cu's dispatch rules, rows_keys_pay): K1j,
+    and K1r with the keys built from its code tile (every CTA hash block holds whole tables, a
+    block's key work small next to its gathers), are one launch; otherwise hash + the key kernel."""
     if Kobj is None or info["kernel"] == 4:
         return 1
     if info["kernel"] == 5:
         return 2  # the GEMM, then the key kernel on its codes
     rp = P.row_packing() if info["kernel"] == 3 else None
-    if rp is not None and rp["hash_blocks"] == 1 and \
-            Kobj.L * Kobj.K <= 0.75 * rp["hash_blocks"] * rp["warps"] * rp["slots"]:
-        return 1
-    return 2
+    if rp is None:
+        return 2
+    L, K = Kobj.L, Kobj.K
+    h0s, ends = [int(h) for h in rp["block_h0"]], [int(h + b) for h, b in zip(rp["block_h0"], rp["block_kb"])]
+    whole = all(h % K == 0 for h in h0s) and all(e % K == 0 or e >= L * K for e in ends)
+    tables = max(min(L, e // K) - h // K for h, e in zip(h0s, ends))
+    return 1 if whole and tables * K <= 0.75 * rp["warps"] * rp["slots"] else 2
 
 
 def _packing_summary(P, info):

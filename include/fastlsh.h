@@ -222,7 +222,8 @@ fastlsh_status fastlsh_build_keys(const fastlsh_keys* keys, const int32_t* codes
 
 /* Codes (as fastlsh_hash) and keys (as fastlsh_build_keys) for the same rows on `stream`; keys may
  * be NULL (codes only). When the params were packed with fastlsh_params_set_table_size(p, K) so that
- * every CTA hash block holds whole tables, the keys are built in the hashing kernel's epilogue
+ * every CTA hash block holds whole tables (K1j always; K1r when its hash blocks start on multiples
+ * of K, e.g. C4's 4 blocks of 500 hashes with K = 10), the keys are built in the hashing kernel's epilogue
  * (codes never re-read); then `codes` may be NULL too — keys only, codes never written to HBM
  * (SURVEY.md §8(f)1). Otherwise codes == NULL is EINVAL. */
 fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* keys,

@@ -169,12 +169,14 @@ bool rows_selected(const fastlsh_params* p) {
     if (p->n % 4) return false;  // rows are not 16-byte multiples: no bulk row copies
     return p->kernel == 0 && p->rpack.cost <= p->pack.cost * kK1Derate;
 }
-// Keys from K1r's code tile pay off when the key work (L*K products per row, spread over the CTA)
-// is small next to the gather work (HB*W*MS LDS.32 wavefronts per row): measured C1 (500 vs 1024)
-// 4.49 vs 4.59 ms for hash + keys, C3 (256 vs 144) 10.9 vs 9.8 ms per 8M rows.
+// Keys from K1r's code tile (every hash block builds the tables it holds) pay off when a block's key
+// work (tables x K products per row, spread over the CTA) is small next to its gather work (W*MS
+// LDS.32 wavefronts per row): measured C1 (500 vs 1024) 4.49 vs 4.59 ms for hash + keys, C3 (256
+// vs 144) 10.9 vs 9.8 ms per 8M rows.
 bool rows_keys_pay(const fastlsh_params* p, const fastlsh_keys* ks) {
     const RPacking& r = p->rpack;
-    return (double)ks->L * ks->K <= 0.75 * (double)r.hash_blocks * r.warps * r.slots;
+    if (!rows_keys_fusable(r, ks->L, ks->K)) return false;
+    return (double)rows_key_tables_max(r, ks->L, ks->K) * ks->K <= 0.75 * (double)r.warps * r.slots;
 }
 // K1j (params-specialised lane = row kernel, jit.cpp) serves the call when pinned (kernel 4) or, in
 // auto mode, whenever it applies (n <= 128: the gathers become register operands, no shared-memory
@@ -735,10 +737,10 @@ fastlsh_status fastlsh_hash_keys(const fastlsh_params* p, const fastlsh_keys* ks
         st = jit::launch(p, p->dev[dev], X, N, codes, nullptr, ks, dr, keys_out, ldk, reinterpret_cast<cudaStream_t>(stream));
         if (st != FASTLSH_EUNSUPPORTED || p->kernel == 4) return st;
     }
-    // K1r (one hash block): keys built from the code tile in shared memory; codes not written
+    // K1r (hash blocks on table boundaries): keys built from the code tile in shared memory; codes not written
     // when codes == NULL. Falls through when K1r cannot serve the call.
-    if (rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
-        (!codes || rows_keys_pay(p, ks))) {
+    if (rows_selected(p) && (p->table_align <= 1 || p->table_align == ks->K) &&
+        rows_keys_fusable(p->rpack, ks->L, ks->K) && (!codes || rows_keys_pay(p, ks))) {
         const uint64_t* dr = nullptr;
         st = keys_device(ks, dev, &dr);
         if (st != FASTLSH_OK) return st;
@@ -883,10 +885,10 @@ fastlsh_status fastlsh_hash_host(fastlsh_params* p, const fastlsh_keys* ks, cons
             fused_here = st == FASTLSH_OK;
             if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
         }
-        if (!fused_here && want_keys && !dense && rows_selected(p) && p->rpack.hash_blocks == 1 && p->table_align <= 1 &&
-            rows_keys_pay(p, ks)) {
+        if (!fused_here && want_keys && !dense && rows_selected(p) &&
+            (p->table_align <= 1 || p->table_align == ks->K) && rows_keys_pay(p, ks)) {
             FusedKeys fk{dr, ks->L, ks->K, d.ws_keys[b], rows};
-            st = launch_gather_rows(p, d, d.ws_x[b], rows, d.ws_codes[b], nullptr, s, &fk);
+            st = launch_gather_rows(p, d, d.ws_x[b], rows, codes_host ? d.ws_codes[b] : nullptr, nullptr, s, &fk);
             fused_here = st == FASTLSH_OK;
             if (st != FASTLSH_OK && st != FASTLSH_EUNSUPPORTED) return st;
         }

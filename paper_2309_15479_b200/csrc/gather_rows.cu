@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "internal.h"
@@ -33,14 +34,38 @@ size_t row_smem_bytes(const RPacking& pk, int key_words = 0) {
 
 using namespace k1r;
 
+// A block [h0, h0 + kb) holds whole tables when h0 is a multiple of K and its end is too (or lies
+// past the last table's codes, L*K <= k).
+bool rows_keys_fusable(const RPacking& pk, int L, int K) {
+    if (!pk.ok || K < 1) return false;
+    for (int bl = 0; bl < pk.hash_blocks; ++bl) {
+        if (pk.block_h0[bl] % K) return false;
+        const int end = pk.block_h0[bl] + pk.block_kb[bl];
+        if (end % K && end < L * K) return false;
+    }
+    return true;
+}
+int rows_key_tables_max(const RPacking& pk, int L, int K) {
+    int t = 0;
+    for (int bl = 0; bl < pk.hash_blocks; ++bl) {
+        const int t0 = pk.block_h0[bl] / K, t1 = std::min(L, (pk.block_h0[bl] + pk.block_kb[bl]) / K);
+        t = std::max(t, t1 - t0);
+    }
+    return t;
+}
+
 fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X, int64_t N,
                                   int32_t* codes, float* proj, cudaStream_t stream, const FusedKeys* fk) {
     const RPacking& pk = p->rpack;
     if (!pk.ok || !d.r_offp) return FASTLSH_EUNSUPPORTED;
-    // keys from the code tile need every table's codes in the one block
-    // (and K <= 1024: the limb sums of the flush are exact while K * 2^53 < 2^63)
-    if (fk && (pk.hash_blocks != 1 || (int64_t)fk->L * fk->K > p->k || fk->K > 1024)) return FASTLSH_EUNSUPPORTED;
-    const int key_words = fk ? fk->L * (fk->K + 1) : 0;
+    // keys from the code tile need every table's codes in one block: blocks start on table
+    // boundaries (K <= 1024: the limb sums of the flush are exact while K * 2^53 < 2^63)
+    int key_words = 0;
+    if (fk) {
+        if (!rows_keys_fusable(pk, fk->L, fk->K) || (int64_t)fk->L * fk->K > p->k || fk->K > 1024)
+            return FASTLSH_EUNSUPPORTED;
+        key_words = rows_key_tables_max(pk, fk->L, fk->K) * (fk->K + 1);
+    }
     // TMA bulk row copies need 16-byte aligned rows
     if ((p->n % 4) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
     constexpr size_t kSmemMax = 227 * 1024;
@@ -82,6 +107,7 @@ fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, 
     a.kr = fk ? fk->r : nullptr;
     a.L = fk ? fk->L : 0;
     a.K = fk ? fk->K : 1;
+    a.kw = key_words;
     a.keys = fk ? fk->keys : nullptr;
     a.ldk = fk ? fk->ldk : 0;
     static const int debug = [] {  // experiment knob, read once

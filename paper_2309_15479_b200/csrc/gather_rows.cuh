@@ -53,10 +53,12 @@ struct RowArgs {
     unsigned long long* flags;
     int vec;                   // 1: the block's code runs are 16-byte aligned (16-byte copy-out)
     int debug;                 // experiment knob (FASTLSH_K1R_DEBUG): 1 no code output, 2 no refills
-    // compound keys built from the code tile in the flush (R9), when one
-    // block covers all hashes: key_l(v) = (r0 + sum_j r_{j+1} u32(c_{lK+j})) mod 2^61-1
+    // compound keys built from the code tile in the flush (R9): each hash
+    // block builds the tables whose K codes it holds (blocks start on table boundaries, checked by
+    // the launcher): key_l(v) = (r0 + sum_j r_{j+1} u32(c_{lK+j})) mod 2^61-1
     const uint64_t* kr;        // multipliers [L][K+1] (nullptr: no keys)
     int L, K;
+    int kw;                    // shared-memory key multipliers per CTA: max tables of a block * (K+1)
     uint64_t* keys;            // [L][ldk], column = row index
     long long ldk;
 };
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(cbuf + NC * cwords);
     // [L][K+1] key multipliers (a.kr) as three 21-bit limbs {r & (2^21-1), (r >> 21) & (2^21-1), r >> 42, 0}
     uint4* s_kl = reinterpret_cast<uint4*>(bars + ((NS + 2 * NC + 1) & ~1));  // 16-byte aligned
-    int* cnt = reinterpret_cast<int*>(s_kl + (a.kr ? a.L * (a.K + 1) : 0));  // [NS] stage readers (monotone)
+    int* cnt = reinterpret_cast<int*>(s_kl + (a.kr ? a.kw : 0));  // [NS] stage readers (monotone)
     float* s_b = reinterpret_cast<float*>(cnt + NS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -155,6 +157,9 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     const int kb = a.block_kb[hb];
     const int h0 = a.block_h0[hb];
     const int hpw = 32 / a.P;
+    // tables [t0, t1) of this block (keys only): h0 is a multiple of K
+    const int t0 = a.kr ? h0 / a.K : 0;
+    const int t1 = a.kr ? min(a.L, (h0 + kb) / a.K) : 0;
 
     const uint32_t stage0 = smem_u32(stages);
     const uint32_t cbuf0 = smem_u32(cbuf);
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
     for (int i = tid; i < NS * R * 32; i += nthreads) stages[(size_t)(i >> 5) * S + a.S0 - 32 + (i & 31)] = 0.f;
     for (int i = tid; i < kb; i += nthreads) s_b[i] = a.b[h0 + i];
     if (a.kr)
-        for (int i = tid; i < a.L * (a.K + 1); i += nthreads) {
-            const uint64_t r = a.kr[i];
+        for (int i = tid; i < (t1 - t0) * (a.K + 1); i += nthreads) {
+            const uint64_t r = a.kr[(size_t)t0 * (a.K + 1) + i];
             s_kl[i] = make_uint4((uint32_t)r & 0x1fffffu, (uint32_t)(r >> 21) & 0x1fffffu, (uint32_t)(r >> 42), 0u);
         }
 
@@ -260,11 +265,11 @@ __global__ void __launch_bounds__((MS <= 24 ? 768 : MS <= 40 ? 640 : MS <= 64 ? 
                 return x >= P61 ? x - P61 : x;
             };
             auto rotl61 = [](uint64_t x, int j) { return ((x << j) & P61) | (x >> (61 - j)); };
-            for (int u = tid; u < a.L * R; u += nthreads) {
-                const int r = u % R, t = u / R;
+            for (int u = tid; u < (t1 - t0) * R; u += nthreads) {
+                const int r = u % R, tl = u / R, t = t0 + tl;
                 if (r >= rows) continue;
-                const uint4* rl = s_kl + t * (K + 1);
-                const int32_t* cc = src + r * a.kbp + t * K;
+                const uint4* rl = s_kl + tl * (K + 1);
+                const int32_t* cc = src + r * a.kbp + tl * K;
                 const uint4 q0 = rl[0];
                 uint64_t s0 = (uint64_t)q0.x | ((uint64_t)q0.y << 21) | ((uint64_t)q0.z << 42), s1 = 0, s2 = 0;
                 for (int jj = 0; jj < K; ++jj) {

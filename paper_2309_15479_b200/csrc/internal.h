@@ -227,6 +227,9 @@ fastlsh_status launch_gather_tmem(const fastlsh_params* p, const DeviceCopy& d, 
                                   int64_t N, int32_t* codes, float* proj, cudaStream_t stream);
 // gather_rows.cu (fk: compound keys built in the flush of the code tile; needs one hash block)
 struct FusedKeys;
+// K1r keys from the code tile: every hash block holds whole tables; the most tables one block holds
+bool rows_keys_fusable(const RPacking& pk, int L, int K);
+int rows_key_tables_max(const RPacking& pk, int L, int K);
 fastlsh_status launch_gather_rows(const fastlsh_params* p, const DeviceCopy& d, const float* X,
                                   int64_t N, int32_t* codes, float* proj, cudaStream_t stream,
                                   const FusedKeys* fk = nullptr);

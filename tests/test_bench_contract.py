@@ -34,3 +34,20 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_other_ranks_exit_quietly():
     assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--config", "C0") == []
+
+
+def test_launch_count_mirrors_the_fused_key_rule():
+    """bench.py's gpu_launches claim: one launch per fastlsh_hash_keys call when K1r's hash blocks
+    hold whole tables (C1: one block; C4: 4 blocks of 500 hashes, K = 10), two (hash + key kernel)
+    when a table straddles a block boundary (C4 with K = 7). Host-side packing only: no GPU."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2309_15479_b200 as fl
+    from fastlsh_inputs import configs
+
+    for name, L, K, want in (("C1", 50, 10, 1), ("C4", 200, 10, 1), ("C4", 200, 7, 2)):
+        c = configs.get(name)
+        P = fl.Params.create(c.n, c.m, c.k, c.w, seed=c.seed)
+        info = P.info()
+        assert info["kernel"] == 3, (name, info["kernel"])
+        assert bench._launches_per_call(P, info, fl.Keys.create(L, K, seed=1)) == want, (name, L, K)

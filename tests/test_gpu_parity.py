@@ -398,11 +398,13 @@ def test_rows_kernel_determinism_and_flags():
 
 
 @pytest.mark.parametrize("name,L,K,N", [("C1", 50, 10, 3001), ("C3", 16, 16, 4099), ("C0", 5, 12, 999),
-                                         ("C4", 200, 10, 1203)])
+                                         ("C4", 200, 10, 1203), ("C4", 60, 10, 1203), ("C4", 200, 7, 1203)])
 def test_rows_kernel_keys_from_code_tile(name, L, K, N):
-    """K1r builds the compound keys from its shared-memory code tile when one CTA block covers all
-    hashes (C0/C1/C3); bit-exact vs codes + the standalone key kernel, also keys-only and into
-    columns [col0, col0 + N) of a wider table. C4 (8 blocks) takes the separate kernel, same result."""
+    """K1r builds the compound keys from its shared-memory code tile when every CTA hash block holds
+    whole tables (C0/C1/C3: one block; C4: 4 blocks of 500 hashes, K = 10 — each block builds its 50
+    tables; L = 60: the last two blocks build none); bit-exact vs codes + the standalone key kernel,
+    also keys-only (which only the fused path serves) into columns [col0, col0 + N) of a wider table.
+    C4 with K = 7 (tables straddle the block boundaries) takes the separate kernel, same result."""
     c = configs.get(name)
     idx, a, b = fastlsh_arrays(c.n, c.m, c.k, c.w, 3)
     P = fl.Params.from_arrays(c.n, c.w, idx, a, b).set_kernel("rows")  # (C0/C3 default to K1j)
@@ -414,7 +416,11 @@ def test_rows_kernel_keys_from_code_tile(name, L, K, N):
     keys_p = fl.build_keys(Kobj, codes_p)
     assert torch.equal(codes_f, codes_p)
     assert torch.equal(keys_f, keys_p)
-    if P.row_packing()["hash_blocks"] == 1:
+    rp = P.row_packing()
+    ends = rp["block_h0"] + rp["block_kb"]
+    whole_tables = all(h % K == 0 for h in rp["block_h0"]) and all(e % K == 0 or e >= L * K for e in ends)
+    assert whole_tables == (K != 7)
+    if whole_tables:
         wide = torch.zeros((L, N + 77), dtype=torch.int64, device="cuda")
         _, w2 = fl.hash_keys(P, Kobj, X, keys_out=wide, with_codes=False, col0=77)
         assert torch.equal(w2[:, 77:], keys_p) and (w2[:, :77] == 0).all()
