@@ -398,7 +398,8 @@ def test_rows_kernel_determinism_and_flags():
 
 
 @pytest.mark.parametrize("name,L,K,N", [("C1", 50, 10, 3001), ("C3", 16, 16, 4099), ("C0", 5, 12, 999),
-                                         ("C4", 200, 10, 1203), ("C4", 60, 10, 1203), ("C4", 200, 7, 1203)])
+                                         ("C4", 200, 10, 1203), ("C4", 60, 10, 1203), ("C4", 200, 7, 1203),
+                                         ("C4", 200, 10, 1), ("C4", 200, 10, 7), ("C1", 50, 10, 5)])
 def test_rows_kernel_keys_from_code_tile(name, L, K, N):
     """K1r builds the compound keys from its shared-memory code tile when every CTA hash block holds
     whole tables (C0/C1/C3: one block; C4: 4 blocks of 500 hashes, K = 10 — each block builds its 50
