@@ -195,8 +195,12 @@ fastlsh_status fastlsh_project(const fastlsh_params* p, const float* X, int64_t 
 /* codes = floor((X . A^T + b) / w) with A[k][n] the dense coefficient matrix of the params
  * (for E2LSH params, a_i itself; for FastLSH params, the duplicates-merged sampled matrix).
  * tcgen05 kind::tf32 MMAs with a 3xTF32 split (hi*hi + hi*lo + lo*hi), fp32 accumulation in TMEM,
- * fused +b, /w, floor epilogue. precision: 3 = 3xTF32 (parity-gated), 1 = plain TF32.
- * Requires n % 32 == 0 and k % 16 == 0 (else EUNSUPPORTED). */
+ * fused +b, /w, floor epilogue. precision: 3 = 3xTF32 (parity-gated), 1 = plain TF32 (ungated),
+ * 2 = 3xFP16: kind::f16 MMAs at twice the TF32 rate on Xh.Ah + Xh.Al + Xl'.Ah' with Xh = fp16(x),
+ * Xl' = fp16((x - Xh) * 2^11), Ah = fp16(a), Al = fp16(a - Ah), Ah' = fp16(Ah * 2^-11) (parity-gated;
+ * |x|, |a| must stay below 65504, fp16's range: an overflowing element comes back as INT32_MIN and
+ * is counted as non-finite). Other precision values: EINVAL. Requires n % 4 == 0 and X 16-byte
+ * aligned (else EUNSUPPORTED); the coefficient operands are built on the device on first use. */
 fastlsh_status e2lsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
                           int32_t precision, fastlsh_stream_t stream);
 

@@ -381,7 +381,7 @@ def fastlsh_project(params: Params, X, out=None, stream=None):
 
 
 def e2lsh_hash(params: Params, X, out=None, precision: int = 3, stream=None):
-    """Dense baseline codes on tcgen05 (3xTF32 by default)."""
+    """Dense baseline codes on tcgen05: precision 3 = 3xTF32 (default), 2 = 3xFP16, 1 = plain TF32."""
     import torch
     params._ready()
     _check_X(params, X)

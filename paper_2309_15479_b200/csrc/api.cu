@@ -139,7 +139,7 @@ fastlsh_status ready_params(const fastlsh_params* p, int* dev_out) {
 void free_device_copy(DeviceCopy& d) {
     cudaFree(d.offp); cudaFree(d.coef); cudaFree(d.unit_lane); cudaFree(d.b);
     cudaFree(d.block_h0); cudaFree(d.block_kb); cudaFree(d.flags);
-    cudaFree(d.dense_hi); cudaFree(d.dense_lo);
+    cudaFree(d.dense_hi); cudaFree(d.dense_lo); cudaFree(d.dense_h16);
     cudaFree(d.t_recs); cudaFree(d.t_counts); cudaFree(d.t_offs); cudaFree(d.t_hinfo); cudaFree(d.t_groups);
     cudaFree(d.r_offp); cudaFree(d.r_coef); cudaFree(d.r_lane_hash); cudaFree(d.r_block_h0); cudaFree(d.r_block_kb);
     cudaFree(d.j_idx); cudaFree(d.j_a);
@@ -511,7 +511,7 @@ fastlsh_status fastlsh_project(const fastlsh_params* p, const float* X, int64_t 
 
 fastlsh_status e2lsh_hash(const fastlsh_params* p, const float* X, int64_t N, int32_t* codes,
                           int32_t precision, fastlsh_stream_t stream) {
-    if (!p || N < 0 || (precision != 1 && precision != 3)) return FASTLSH_EINVAL;
+    if (!p || N < 0 || (precision < 1 || precision > 3)) return FASTLSH_EINVAL;
     if (N == 0) return FASTLSH_OK;
     if (!X || !codes) return FASTLSH_EINVAL;
     int dev = 0;
@@ -524,7 +524,7 @@ fastlsh_status e2lsh_hash(const fastlsh_params* p, const float* X, int64_t N, in
 
 fastlsh_status e2lsh_project(const fastlsh_params* p, const float* X, int64_t N, float* proj,
                              int32_t precision, fastlsh_stream_t stream) {
-    if (!p || N < 0 || (precision != 1 && precision != 3)) return FASTLSH_EINVAL;
+    if (!p || N < 0 || (precision < 1 || precision > 3)) return FASTLSH_EINVAL;
     if (N == 0) return FASTLSH_OK;
     if (!X || !proj) return FASTLSH_EINVAL;
     int dev = 0;

@@ -4,7 +4,13 @@
 // coefficient matrix of the params (a_i itself for E2LSH params; the duplicates-merged sampled
 // matrix for FastLSH params). fp32 accuracy from TF32 tensor cores by the 3xTF32 split
 //     X.A ~= Xhi.Ahi + Xhi.Alo + Xlo.Ahi,   hi = fp32 with the low 13 mantissa bits cleared
-// (precision 3; precision 1 = plain Xhi.Ahi, the ungated reference point).
+// (precision 3; precision 1 = plain Xhi.Ahi, the ungated reference point), or at twice the MMA rate
+// from fp16 tensor cores by the 3xFP16 split (precision 2, single-CTA kernel)
+//     X.A ~= Xh.Ah + Xh.Al + Xl'.Ah',   Xh = fp16(x), Xl' = fp16((x - Xh) 2^11),
+//                                        Ah = fp16(a), Al = fp16(a - Ah), Ah' = fp16(Ah 2^-11)
+// (the 2^11 scaling keeps the low part of x out of fp16's subnormal range; all three products
+// accumulate in one fp32 TMEM accumulator). Needs |x|, |a| < 65504: larger values overflow to inf
+// and come back flagged like any non-finite projection.
 //
 // One CTA computes a 256-row x 256-hash output tile (non-persistent grid). fp32 operands make the
 // GEMM bandwidth-hungry (A is re-read by every row tile), so rows per tile are 256: two UMMA
@@ -19,6 +25,7 @@
 //             N=256, K=8 per instruction; 2 halves x 2 k-steps x 3 products per K-block);
 //             tcgen05.commit releases the smem stage and finally signals the epilogue.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -41,6 +48,11 @@ constexpr int kThreadsE = 320;  // 10 warps
 constexpr uint32_t kXTileBytes = BM * BK * 4;   // 16 KB
 constexpr uint32_t kATileBytes = BN * BK * 4;   // 16 KB
 constexpr uint32_t kStageBytesE = 2 * kXTileBytes + 2 * kATileBytes;  // X, Xlo, Ahi, Alo
+// 3xFP16 stages: the f32 X tile (converted in place into Xh | Xl', 8 KB each) and Ah | Al | Ah'
+// (fp16 [256 x 16], 32-byte rows, 32-byte swizzle): 40 KB, 5 stages (C1: 5.01 / 4.70 / 4.51 ms at 3 / 4 / 5)
+constexpr uint32_t kHTile = BN * BK * 2;                              // 8 KB
+constexpr uint32_t kStageBytesH = kXTileBytes + 3 * kHTile;           // 40 KB
+constexpr int kStagesH = 5;
 
 struct E2Args {
     long long N;
@@ -61,6 +73,7 @@ struct E2Args {
     // together share their X tiles through L2 (X is read from HBM once instead of kpad/256 times);
     // 0 = row tiles in blockIdx.x (more than 65535 row tiles)
     int hash_fast;
+    int stages_h16;  // 3xFP16 ring depth (40 KB stages)
 };
 
 // A FastLSH hash sees only its sampled coordinates. The merged-coefficient GEMM
@@ -152,6 +165,29 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
     return d;
 }
 
+// K-major, 32-byte swizzle (fp16 rows of 16 elements): 8-row atoms of 256 B (SBO), layout type 6.
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (16 B units)
+    d |= (uint64_t)(256 >> 4) << 32;        // SBO
+    d |= (uint64_t)1 << 46;                 // version
+    d |= (uint64_t)6 << 61;                 // SWIZZLE_32B
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B f16, both K-major, N = 256, M = 128.
+constexpr uint32_t kIdescF16 = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kIdescF16), "r"(accumulate)
+        : "memory");
+}
+
 // Instruction descriptor: D f32, A/B tf32, both K-major, N = 256, M = 128.
 constexpr uint32_t kIdescTF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                 ((uint32_t)(128 >> 4) << 24);
@@ -186,14 +222,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 __global__ void __launch_bounds__(kThreadsE, 1)
 e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_ahi,
-                     const __grid_constant__ CUtensorMap map_alo, const E2Args a) {
+                     const __grid_constant__ CUtensorMap map_alo, const __grid_constant__ CUtensorMap map_ahs,
+                     const E2Args a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment for the swizzle atoms
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // 1xTF32 stages carry only X and Ahi (32 KB), so twice as many fit: the same bytes in flight for
     // a third of the MMA work per stage (measured 4.19 ms on C1 with 3 stages: latency-bound)
-    const int kStagesE = a.precision == 3 ? 3 : 6;
-    const uint32_t kStageBytes = a.precision == 3 ? kStageBytesE : kXTileBytes + kATileBytes;
+    const bool h16 = a.precision == 2;
+    const int kStagesE = h16 ? a.stages_h16 : a.precision == 3 ? 3 : 6;
+    const uint32_t kStageBytes = h16 ? kStageBytesH : a.precision == 3 ? kStageBytesE : kXTileBytes + kATileBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagesE * kStageBytes);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStagesE + 1);
     constexpr int kConvThreads = kThreadsE - 64;
@@ -237,12 +275,18 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            const uint32_t bytes = kXTileBytes + (a.precision == 3 ? 2 : 1) * kATileBytes;
+            const uint32_t bytes = h16 ? kStageBytesH : kXTileBytes + (a.precision == 3 ? 2 : 1) * kATileBytes;
             for (int kb = 0; kb < KB; ++kb) {
                 const int s = kb % kStagesE;
                 if (kb >= kStagesE) mbar_wait(EMPTY(s), (uint32_t)(((kb - kStagesE) / kStagesE) & 1));
                 mbar_arrive_tx(FULL(s), bytes);
                 tma_load_2d(XT(s), &map_x, kb * BK, (int)m0, FULL(s));
+                if (h16) {  // Ah | Al | Ah' behind the f32 X tile
+                    tma_load_2d(XT(s) + kXTileBytes, &map_ahi, kb * BK, h0, FULL(s));
+                    tma_load_2d(XT(s) + kXTileBytes + kHTile, &map_alo, kb * BK, h0, FULL(s));
+                    tma_load_2d(XT(s) + kXTileBytes + 2 * kHTile, &map_ahs, kb * BK, h0, FULL(s));
+                    continue;
+                }
                 tma_load_2d(AH(s), &map_ahi, kb * BK, h0, FULL(s));
                 if (a.precision == 3) tma_load_2d(AL(s), &map_alo, kb * BK, h0, FULL(s));
             }
@@ -254,6 +298,22 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
                 const int s = kb % kStagesE;
                 mbar_wait(CONV(s), (uint32_t)((kb / kStagesE) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (h16) {  // one K=16 MMA per product and row half: Xh.Ah + Xh.Al + Xl'.Ah'
+                    const uint64_t dah = umma_desc_sw32(XT(s) + kXTileBytes);
+                    const uint64_t dal = umma_desc_sw32(XT(s) + kXTileBytes + kHTile);
+                    const uint64_t das = umma_desc_sw32(XT(s) + kXTileBytes + 2 * kHTile);
+#pragma unroll
+                    for (int mh = 0; mh < 2; ++mh) {
+                        const uint32_t xo = mh * (kHTile / 2);  // rows 128*mh.. of Xh / Xl' (32 B each)
+                        const uint32_t td = tmem + mh * BN;
+                        const uint64_t dxh = umma_desc_sw32(XT(s) + xo);
+                        umma_f16(td, dxh, dah, kb > 0 ? 1u : 0u);
+                        umma_f16(td, dxh, dal, 1u);
+                        umma_f16(td, umma_desc_sw32(XT(s) + kHTile + xo), das, 1u);
+                    }
+                    umma_commit(EMPTY(s));
+                    continue;
+                }
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
                     const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
@@ -282,7 +342,38 @@ e2lsh_tcgen05_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_con
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % kStagesE;
             mbar_wait(FULL(s), (uint32_t)((kb / kStagesE) & 1));
-            if (a.precision == 3) {
+            if (h16) {
+                // f32 tile [256 x 16] (64-byte rows, 64-byte swizzle: 16-byte chunk c of row r at
+                // c ^ ((r >> 1) & 3)) -> Xh | Xl' fp16 [256 x 16] (32-byte rows, 32-byte swizzle: chunk
+                // c at c ^ ((r >> 2) & 1)), in place: every converter thread reads its four float4s,
+                // then all 256 meet at a named barrier before any writes
+                unsigned char* st = smem + s * kStageBytes;
+                float4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = reinterpret_cast<const float4*>(st)[t + kConvThreads * i];
+                asm volatile("bar.sync 1, %0;" ::"r"(kConvThreads) : "memory");
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int u = t + kConvThreads * i;        // physical float4 slot of the f32 tile
+                    const int r = u >> 2;
+                    const int q = (u & 3) ^ ((r >> 1) & 3);    // logical float4 (columns 4q..4q+3)
+                    const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                    __half2 hp[2], lp[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const __half h0 = __float2half_rn(x[2 * e]), h1 = __float2half_rn(x[2 * e + 1]);
+                        hp[e] = __halves2half2(h0, h1);
+                        lp[e] = __halves2half2(__float2half_rn((x[2 * e] - __half2float(h0)) * 2048.0f),
+                                               __float2half_rn((x[2 * e + 1] - __half2float(h1)) * 2048.0f));
+                    }
+                    const uint32_t off = r * 32 + (((q >> 1) ^ ((r >> 2) & 1)) << 4) + ((q & 1) << 3);
+                    *reinterpret_cast<uint2*>(st + off) =
+                        make_uint2(*reinterpret_cast<uint32_t*>(&hp[0]), *reinterpret_cast<uint32_t*>(&hp[1]));
+                    *reinterpret_cast<uint2*>(st + kHTile + off) =
+                        make_uint2(*reinterpret_cast<uint32_t*>(&lp[0]), *reinterpret_cast<uint32_t*>(&lp[1]));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            } else if (a.precision == 3) {
                 float4* xt = reinterpret_cast<float4*>(smem + s * kStageBytes);
                 float4* xl = reinterpret_cast<float4*>(smem + s * kStageBytes + kXTileBytes + kATileBytes);
 #pragma unroll
@@ -659,18 +750,74 @@ static fastlsh_status ensure_dense(const fastlsh_params* p, DeviceCopy& d) {
     return FASTLSH_OK;
 }
 
+// 3xFP16 operands (precision 2): Ah | Al | Ah' as fp16 [3][kpad][n8] (n8 = n rounded up to 8: 16-byte
+// row pitch for TMA; the padding columns are zero), from the same f32 coefficients as the tf32 split.
+static fastlsh_status ensure_dense16(const fastlsh_params* p, DeviceCopy& d) {
+    if (d.dense_h16) return FASTLSH_OK;
+    const int kpad = (p->k + BN - 1) / BN * BN;
+    const int n8 = (p->n + 7) / 8 * 8;
+    std::vector<double> A((size_t)kpad * p->n, 0.0);
+    for (int i = 0; i < p->k; ++i)
+        for (int j = 0; j < p->m; ++j) A[(size_t)i * p->n + p->idx[(size_t)i * p->m + j]] += p->a[(size_t)i * p->m + j];
+    const size_t plane = (size_t)kpad * n8;
+    std::vector<__half> H(3 * plane, __float2half_rn(0.0f));
+    for (int i = 0; i < kpad; ++i)
+        for (int c = 0; c < p->n; ++c) {
+            const float f = (float)A[(size_t)i * p->n + c];
+            const __half h = __float2half_rn(f);
+            const float hf = __half2float(h);
+            H[(size_t)i * n8 + c] = h;
+            H[plane + (size_t)i * n8 + c] = __float2half_rn(f - hf);
+            H[2 * plane + (size_t)i * n8 + c] = __float2half_rn(hf * (1.0f / 2048.0f));
+        }
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d.dense_h16), H.size() * sizeof(__half));
+    if (e == cudaSuccess) e = cudaMemcpy(d.dense_h16, H.data(), H.size() * sizeof(__half), cudaMemcpyHostToDevice);
+    static_assert(sizeof(__half) == sizeof(uint16_t), "fp16 bits");
+    if (e != cudaSuccess) {
+        cudaFree(d.dense_h16);
+        d.dense_h16 = nullptr;
+        return set_cuda_error(e);
+    }
+    d.dense_n8 = n8;
+    return FASTLSH_OK;
+}
+
+// 2D fp16 tensor map over [rows][n8], box [box_rows][16 halves] (32-byte rows), 32-byte swizzle.
+static bool make_map_h16(CUtensorMap* m, const void* base, long long rows, int n8, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)n8, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)n8 * 2};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float* X, int64_t N, int32_t* codes,
                             float* proj, int precision, cudaStream_t stream) {
     if (p->n % 4 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0) return FASTLSH_EUNSUPPORTED;
     {
         std::lock_guard<std::mutex> g(const_cast<fastlsh_params*>(p)->dense_mu);
         fastlsh_status st = ensure_dense(p, d);
+        if (st == FASTLSH_OK && precision == 2) st = ensure_dense16(p, d);
         if (st != FASTLSH_OK) return st;
     }
-    CUtensorMap mx, mh, ml;
-    if (!make_map(&mx, X, N, p->n, BM) || !make_map(&mh, d.dense_hi, d.dense_kpad, p->n, BN) ||
-        !make_map(&ml, d.dense_lo, d.dense_kpad, p->n, BN))
+    CUtensorMap mx, mh, ml, ms;
+    if (!make_map(&mx, X, N, p->n, BM)) return FASTLSH_EUNSUPPORTED;
+    if (precision == 2) {
+        const size_t plane = (size_t)d.dense_kpad * d.dense_n8;
+        if (!make_map_h16(&mh, d.dense_h16, d.dense_kpad, d.dense_n8, BN) ||
+            !make_map_h16(&ml, d.dense_h16 + plane, d.dense_kpad, d.dense_n8, BN) ||
+            !make_map_h16(&ms, d.dense_h16 + 2 * plane, d.dense_kpad, d.dense_n8, BN))
+            return FASTLSH_EUNSUPPORTED;
+    } else if (!make_map(&mh, d.dense_hi, d.dense_kpad, p->n, BN) ||
+               !make_map(&ml, d.dense_lo, d.dense_kpad, p->n, BN)) {
         return FASTLSH_EUNSUPPORTED;
+    } else {
+        ms = ml;  // unused
+    }
     E2Args a;
     a.N = N;
     a.n = p->n;
@@ -690,7 +837,7 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     // K loops (C3: 7.35 vs 10.8 ms), but its converter relay costs more than it saves on long K loops
     // at 1xTF32 (C1: 4.54 vs 3.77 ms), where the single-CTA kernel stays.
     static const bool single = std::getenv("FASTLSH_K4_SINGLE") != nullptr;  // experiment knob, read once
-    if (!single && (precision == 3 || p->n <= 256)) {
+    if (!single && precision != 2 && (precision == 3 || p->n <= 256)) {
         CUtensorMap px, ph, pl;
         if (!make_map(&px, X, N, p->n, 128) || !make_map(&ph, d.dense_hi, d.dense_kpad, p->n, 128) ||
             !make_map(&pl, d.dense_lo, d.dense_kpad, p->n, 128))
@@ -724,7 +871,14 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
         pe = cudaLaunchKernelEx(&cfg, e2lsh_pair_kernel, px, ph, pl, a);
         return pe == cudaSuccess ? FASTLSH_OK : set_cuda_error(pe);
     }
-    const size_t smem = 3 * kStageBytesE + 1024 + 256;  // 3 x 64 KB (3xTF32) or 6 x 32 KB (1xTF32)
+    // 3 x 64 KB (3xTF32), 6 x 32 KB (1xTF32) or kStagesH x 40 KB (3xFP16)
+    static const int stages_h16 = [] {  // experiment knob, read once
+        const char* e = std::getenv("FASTLSH_K4_H16_STAGES");
+        const int v = e ? std::atoi(e) : kStagesH;
+        return v >= 2 && v <= kMaxStagesE && v * kStageBytesH + 1280 <= 227 * 1024 ? v : kStagesH;
+    }();
+    a.stages_h16 = stages_h16;
+    const size_t smem = (precision == 2 ? (size_t)stages_h16 * kStageBytesH : 3 * kStageBytesE) + 1024 + 256;
     if (fastlsh_status so = smem_optin_once(reinterpret_cast<const void*>(e2lsh_tcgen05_kernel)); so != FASTLSH_OK)
         return so;
     cudaError_t e;
@@ -732,7 +886,7 @@ fastlsh_status launch_e2lsh(const fastlsh_params* p, DeviceCopy& d, const float*
     a.hash_fast = tiles <= 65535 ? 1 : 0;
     dim3 grid = a.hash_fast ? dim3((unsigned)(d.dense_kpad / BN), (unsigned)tiles)
                             : dim3((unsigned)tiles, (unsigned)(d.dense_kpad / BN));
-    e2lsh_tcgen05_kernel<<<grid, kThreadsE, smem, stream>>>(mx, mh, ml, a);
+    e2lsh_tcgen05_kernel<<<grid, kThreadsE, smem, stream>>>(mx, mh, ml, ms, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e);
     return FASTLSH_OK;

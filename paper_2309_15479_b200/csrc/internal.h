@@ -158,6 +158,8 @@ struct DeviceCopy {
     float* dense_hi = nullptr;            // dense E2LSH operand A (tf32 hi) [kpad][n]
     float* dense_lo = nullptr;            // A - hi (tf32 lo)
     int dense_kpad = 0;
+    uint16_t* dense_h16 = nullptr;        // 3xFP16 operands (fp16 bits) Ah | Al | Ah' (fp16 [3][kpad][dense_n8])
+    int dense_n8 = 0;
     // host-pipeline workspace (fastlsh_hash_host)
     float* ws_x[2] = {nullptr, nullptr};
     int32_t* ws_codes[2] = {nullptr, nullptr};

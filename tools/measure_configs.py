@@ -105,10 +105,10 @@ def main():
             del keys
         try:
             Pd = fl.Params.e2lsh(c.n, c.k, c.w, seed=c.seed)
-            for prec in (3, 1):
+            for prec in (3, 2, 1):
                 ms = timed(lambda: fl.e2lsh_hash(Pd, X, out=codes, precision=prec), 3)
-                rec[f"dense_tf32x{prec}"] = {"ms": ms, "hashes_per_s": N * c.k / (ms / 1e3),
-                                             "fastlsh_speedup": ms / best}
+                rec["dense_fp16x3" if prec == 2 else f"dense_tf32x{prec}"] = {
+                    "ms": ms, "hashes_per_s": N * c.k / (ms / 1e3), "fastlsh_speedup": ms / best}
             del Pd
         except fl.FastLSHError as ex:
             rec["dense"] = {"unavailable": str(ex)}
