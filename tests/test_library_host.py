@@ -92,6 +92,18 @@ def test_gpu_calls_without_device_fail_loudly(lib):
     assert rc in (fl.ESTATE, fl.ECUDA, fl.EUNSUPPORTED)
 
 
+def test_e2lsh_precision_argument(lib):
+    """e2lsh_hash / e2lsh_project: precision 1 (1xTF32), 2 (3xFP16) and 3 (3xTF32) are accepted (and
+    then need a device), anything else is EINVAL before any device work."""
+    p = fl.Params.e2lsh(16, 8, 1.0, seed=1)
+    V = ctypes.c_void_p(16)
+    for prec in (0, 4, -1, 16):
+        assert lib.e2lsh_hash(p._h, V, 1, V, prec, None) == fl.EINVAL
+        assert lib.e2lsh_project(p._h, V, 1, V, prec, None) == fl.EINVAL
+    for prec in (1, 2, 3):
+        assert lib.e2lsh_hash(p._h, V, 1, V, prec, None) in (fl.ESTATE, fl.ECUDA, fl.EUNSUPPORTED)
+
+
 def _unpack(p):
     """Decode the packing into per-(hash, part) slot multisets and check its invariants."""
     pk = p.packing()
