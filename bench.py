@@ -559,6 +559,10 @@ def main():
     if lpc > 1:
         roofline["note"] = "the per-chunk time covers the hashing kernel and the key kernel (two launches)"
     roofline["launch_ms_min_max"] = [min(full), max(full)]
+    # kernel_share_of_step is ONE launch's share; the kernel's share of the step over all of its
+    # launches (what the ncu launch list's "share" corresponds to) is the sum over the chunks
+    roofline["launches_per_step"] = len(bounds) * lpc
+    roofline["kernel_share_of_step_all_launches"] = statistics.mean(hash_ms) / (total_ms / args.steps)
 
     # the HBM ceiling of the dominant kernel's own traffic mix (a plain streaming kernel reading and
     # writing the same bytes per row: roofline.mix_ceiling), on the same rows
